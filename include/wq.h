@@ -1,0 +1,229 @@
+/*
+ * wq.h — C ABI of the B200-native WindowQuant hot path (libwq.so).
+ *
+ * WindowQuant = "Mixed-Precision KV Cache Quantization based on Window-Level
+ * Similarity for VLMs Inference Optimization" (arxiv 2605.02262).  Citations:
+ * "P:n" = /root/reference/PAPER.md line n (LaTeX source), Eq.k in LaTeX order,
+ * Alg.1 = window-level quantization search, Alg.2 = window-level KV
+ * cache computation.  Readings where the paper is silent are named
+ * Qn and listed in DESIGN.md §3 (same numbering as SURVEY.md §8(c)).
+ *
+ * Conventions (all calls)
+ *  - Pointers are DEVICE pointers unless the parameter name ends in `_host`.
+ *  - The caller owns every buffer.  The library never allocates, frees or keeps
+ *    a pointer after the call returns.  Scratch space comes from an explicit
+ *    `workspace` argument whose size is returned by the matching *_workspace()
+ *    query; workspaces must be zero-filled once after allocation (kernels leave
+ *    them zeroed again on exit).
+ *  - Device calls are asynchronous on `stream` (a cudaStream_t passed as void*,
+ *    NULL = legacy default stream).  Argument validation is synchronous: a call
+ *    that returns anything but WQ_OK launched nothing, and wq_last_error()
+ *    names the offending argument and shape.
+ *  - fp16 tensors are IEEE binary16 (the paper's KV precision).
+ *  - No floating-point atomics anywhere: every output is bit-reproducible run
+ *    to run and GPU to GPU.
+ *  - There is no CPU fallback: every device call launches CUDA kernels.
+ */
+#ifndef WQ_H_
+#define WQ_H_
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  WQ_OK = 0,
+  WQ_EINVAL = 1,        /* bad scalar argument (NULL pointer, alpha <= 0, ...) */
+  WQ_ESHAPE = 2,        /* inconsistent or unsupported shape               */
+  WQ_EBUDGET = 3,       /* average-bit budget infeasible (data independent) */
+  WQ_EUNSUPPORTED = 4,  /* valid but not built (e.g. head dim 96)           */
+  WQ_ECUDA = 5          /* a CUDA launch/runtime error                      */
+} wq_status;
+
+/* Geometry of one layer call.  W = M / S full windows (Eq.7); the
+ * M mod S tail tokens are not a window and stay FP16 (reading Q2). */
+typedef struct {
+  int32_t B;            /* requests in the batch                            */
+  int32_t H;            /* KV heads                                        */
+  int32_t Hq;           /* query heads, Hq % H == 0; group g = Hq / H (Q26) */
+  int32_t d;            /* head dim, 64 or 128                             */
+  int32_t M;            /* visual tokens per request (Eq.4-5)   */
+  int32_t S;            /* window size: 16, 32, 64 or 128 (Eq.7)           */
+  int32_t n_widths;     /* 1..4 */
+  int32_t widths[4];    /* strictly ascending subset of {2,4,8,16} (Q9)    */
+} wq_geom;
+
+typedef struct {
+  double  budget_avg_bits; /* <= 0: no budget.  Else sum_w bits_w <= budget*W (Q13) */
+  int32_t pin_first;       /* 1 (default): window 0 is FP16 in every layer */
+  int32_t batch_vote;      /* 0 (default); 1: per-(layer, window) mode over the batch (Q14) */
+} wq_assign_opts;
+
+/* The canonical width classes; segment k of a packed image holds width
+ * WQ_CLASS_BITS[k].  (Alg.2 concatenates INT2, INT4, FP16 in that order,
+ * P:451-453; 8-bit is the north-star extension, Q9.) */
+#define WQ_N_CLASSES 4
+/* class k <-> bits {2, 4, 8, 16}[k] */
+
+/* ---------------------------------------------------------------------------
+ * Packed KV image (contract D-1; the oracle writes the same bytes).
+ *
+ * One image per layer: for each (b, h) in b-major order a contiguous byte
+ * range starting at offs[b*H + h] (offs from wq_layer_layout); inside it the
+ * window records of request b in SLOT order.  Slots [seg_off[b][k],
+ * seg_off[b][k+1]) form segment k and have width {2,4,8,16}[k]; segments are
+ * precision-contiguous as in Alg.2.  All K/V heads of a
+ * request share its slot list (bits are per (layer, request, window)).
+ *
+ * Window record, width b < 16 (head dim d, window S, T16 = 16-token tile):
+ *   [K codes: S/16 tiles x 2*d*b bytes][V codes: S/16 tiles x 2*d*b bytes]
+ *   [K params: 4*d bytes][V params: 4*S bytes]           size S*d*b/4 + 4d + 4S
+ * Width 16: [K values: S/16 x 32*d bytes][V values: S/16 x 32*d bytes]  size 4*S*d
+ *
+ * Code tiles are in "fragment order": a tile is 32 lane chunks of d*b/16
+ * bytes, chunk L belongs to lane L (g = L/4, q = L%4).  A chunk holds d/4
+ * element PAIRS P = 0..d/4-1 with m = P/4, r = P%4:
+ *   K tile (tokens x channels): row = g + 8*(r&1) (token in tile),
+ *                               col = 16*m + 2*q + 8*(r>>1) (channel)
+ *   V tile (channels x tokens): row = 16*m + g + 8*(r&1) (channel),
+ *                               col = 2*q + 8*(r>>1) (token in tile)
+ *   element e in {0,1} of a pair is (row, col + e).
+ * Pairs are packed into little-endian 32-bit words: word P / (16/b), slot
+ * j = P % (16/b); element e occupies bits [16*e + b*j, 16*e + b*j + b).
+ * (For b = 16 a pair is one word holding two raw fp16 values.)
+ *
+ * K params (per channel c over the window's S tokens, Q19): 4 x d/16 groups
+ * of 16 bytes, group (q, m) at byte (q*(d/16) + m)*16 holds fp16
+ *   { s(c0), s(c0+1), s(c0+8), s(c0+9), mn(c0), mn(c0+1), mn(c0+8), mn(c0+9) },
+ *   c0 = 16*m + 2*q.
+ * V params (per token t over the d channels, Q19): S/16 x 4 groups of 16 B,
+ * group (i, q) at byte (4*i + q)*16 holds the same pattern for tokens
+ *   t0 = 16*i + 2*q of the window.
+ *
+ * Quantizer (Eq.14-16, reading Q17/Q18/Q21).  Per group x[0..n),
+ * q_max = 2^b - 1, all arithmetic IEEE fp32 with one rounding per operation:
+ *   mn = min x, mx = max x
+ *   s  = max(RoundUp_fp16(fl(mx - mn) / q_max), 2^-24)        (stored fp16)
+ *   r  = fl(1 / s)
+ *   code_i = clamp(rint_half_even(fl(fl(x_i - mn) * r)), 0, q_max)
+ *   dequantized x^_i = mn + s * code_i      (error <= s*(1/2 + 2^-14))
+ * -------------------------------------------------------------------------*/
+
+/* Thresholds of Eq.10-11 (Alg.1 lines 4-7).  HOST call.
+ * s_host[L]: layer sensitivities s_l (Eq.9; calibration is out of scope), clamped
+ * to [0, 1] (Q10).  alpha > 0 (default 2).  thr_host[L][n_widths-1]:
+ *   n=3: (f1, f2); n=4: (f1, (f1+f2)/2, f2); n=2: ((f1+f2)/2); n=1: none (Q9).
+ * Errors: WQ_EINVAL (NULL, L < 1, alpha <= 0 or not finite, n_widths outside 1..4). */
+wq_status wq_thresholds(const double *s_host, int32_t L, double alpha,
+                        int32_t n_widths, double *thr_host);
+
+/* Window-prompt similarity, Eq.8 (Alg.1 lines 9-12):
+ *   scores[b][w] = 1/(S*N) * sum_{j<N} sum_{k<S} cos(t_j, v_{w*S+k}),  w < W = M/S
+ * computed through the exact identity sum_j sum_k t^_j . v^_k = (sum_k v^_k).(sum_j t^_j)
+ * with x^ = x/||x|| (Q3), fp64 accumulation and output (Q6).  A zero-norm row
+ * contributes 0 (Q5).
+ * vis: fp16, element (b, m, c) at vis[b*vis_batch_stride + m*vis_row_stride + c];
+ * txt: fp16, element (b, j, c) at txt[b*txt_batch_stride + j*txt_row_stride + c]
+ * (strides in elements, rows 16-byte aligned).  scores: fp64 [B][W].
+ * workspace: wq_window_scores_workspace(B, D) bytes.
+ * Errors: WQ_ESHAPE if M < S, D % 8 != 0, N < 1, S not in {16,32,64,128}. */
+wq_status wq_window_scores_workspace(int32_t B, int32_t D, size_t *bytes_host);
+wq_status wq_window_scores(const void *vis, int64_t vis_row_stride, int64_t vis_batch_stride,
+                           const void *txt, int64_t txt_row_stride, int64_t txt_batch_stride,
+                           int32_t B, int32_t M, int32_t N, int32_t D, int32_t S,
+                           double *scores, void *workspace, size_t workspace_bytes,
+                           void *stream);
+
+/* Bit assignment + permutation (Alg.1 lines 8-16, P:313, P:316-322, P:395;
+ * Alg.2 lines 2-13).  For each layer l and request b:
+ *   1. rank[b][w]: position of window w in (-score, w) order (0 = most similar, Q7)
+ *   2. band: level = [x >= T_1] + sum_{1<j<n-1} [x >= T_j] + [x > T_{n-1}]
+ *      (n >= 3; n = 2: [x > T_1]; n = 1: 0), bits = widths[level] (Q8)
+ *   3. pin: window 0 -> 16 if opts->pin_first (Q12)
+ *   4. vote (opts->batch_vote): per (l, w) the mode over b, ties -> higher
+ *      width (Q14); the budget then ranks by the batch-mean score
+ *   5. budget: while sum_w bits > budget*W, demote the lowest-ranked
+ *      non-pinned window with bits > widths[0] one width step (Q13)
+ *   6. stable partition of windows by width class -> perm (slot -> window),
+ *      seg_off[5] (class boundaries in slots).  The pinned window is in the
+ *      16 class even if 16 is not in widths (Q9, Q15).
+ * scores: fp64 [B][W] (device).  thr_host: [L][n_widths-1] HOST (copied into
+ * kernel parameters; L <= 64).  Outputs (device): bits u8 [L][B][W],
+ * rank i32 [B][W] (may be NULL), perm i32 [L][B][W], seg_off i32 [L][B][5].
+ * Errors: WQ_EBUDGET if 16*pin + widths[0]*(W-pin) > budget*W (checked on host). */
+wq_status wq_assign_bits(const double *scores, const double *thr_host, int32_t L,
+                         const wq_geom *g, const wq_assign_opts *opts,
+                         uint8_t *bits, int32_t *rank, int32_t *perm, int32_t *seg_off,
+                         void *stream);
+
+/* Bytes of one (b, h) image holding n_per_class_host[k] windows of class k
+ * ({2,4,8,16}[k]) under contract D-1.  HOST.  With code_bytes_only = 1 the
+ * params are not counted and the result is the paper's accounting. */
+wq_status wq_packed_bytes(const wq_geom *g, const int32_t n_per_class_host[4],
+                          int32_t code_bytes_only, int64_t *bytes_host);
+
+/* Byte offsets of the (b, h) images of one layer: offs[B*H + 1] (i64, device),
+ * offs[0] = 0, offs[B*H] = total bytes.  seg_off_l: i32 [B][5] (device). */
+wq_status wq_layer_layout(const wq_geom *g, const int32_t *seg_off_l, int64_t *offs,
+                          void *stream);
+
+/* Reorder + group-quantize + pack one layer (Alg.2 lines 2-15, Eq.14-16,
+ * group = window P:508; per-channel K / per-token V parameters, Q19).
+ * k, v: fp16, element (b, h, t, c) at x[b*strides[0] + h*strides[1] + t*strides[2] + c]
+ *   (strides in elements; rows 16-byte aligned).  Window w of request b covers
+ *   tokens vis_off + w*S .. vis_off + w*S + S-1 (Q1).
+ * perm_l: i32 [B][perm_stride]: slot -> window (any subset of windows; the
+ *   multi-GPU sequence split passes each rank its own slot list).
+ * seg_off_l: i32 [B][5]: slot boundaries of the width classes.
+ * offs: i64 [B*H+1] from wq_layer_layout.  packed: u8 image (>= offs[B*H] bytes,
+ *   16-byte aligned).  Output bytes are bit-exact with the oracle.
+ * Errors: WQ_ESHAPE (d not 64/128, S not 16/32/64/128), WQ_EINVAL. */
+wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t strides[3],
+                                   int32_t vis_off, const wq_geom *g,
+                                   const int32_t *perm_l, int32_t perm_stride,
+                                   const int32_t *seg_off_l, const int64_t *offs,
+                                   uint8_t *packed, void *stream);
+
+/* Decode attention over the reordered mixed-precision cache (Alg.2 decode
+ * branch P:450-458, Eq.2-3 without mask P:214, reorder invariance Eq.12-13
+ * P:462-473, fused dequantization P:510).  For each request b and query head
+ * hq (KV head h = hq / (Hq/H)):
+ *   out[b][hq] = sum_t softmax_t(sm_scale * q[b][hq] . k^_t) v^_t
+ * over every slot of the (b, h) image (dequantized on load) and the FP16 rest
+ * tokens t < rest_len[b] (text, tail, generated: P:257, Q29).  Split-KV
+ * online softmax with a log-sum-exp merge (Q24).
+ * q: fp16 [B][Hq][d] contiguous.  packed/offs/seg_off_l: as produced above.
+ * k_rest, v_rest: fp16, element (b, h, t, c) at x[b*rest_strides[0] + h*rest_strides[1] + t*d + c];
+ *   rest_len: i32 [B] (device), each in [0, R_max].
+ * out: fp16 [B][Hq][d] (may be NULL).  partial: fp32 [B][Hq][d+2] =
+ *   (m, l, o[d]) with m = max logit, l = sum exp(logit - m), o = sum exp(logit - m) v
+ *   (unnormalized; m = -inf, l = 0 for an empty cache), may be NULL.
+ * workspace: wq_decode_workspace(g) bytes, zero-filled once.
+ * Errors: WQ_ESHAPE (unsupported d/S, Hq/H > 8), WQ_EINVAL (both outputs NULL). */
+wq_status wq_decode_workspace(const wq_geom *g, size_t *bytes_host);
+wq_status wq_decode_attention(const void *q, const uint8_t *packed, const int64_t *offs,
+                              const int32_t *seg_off_l, const wq_geom *g,
+                              const void *k_rest, const void *v_rest,
+                              const int64_t rest_strides[2], const int32_t *rest_len,
+                              int32_t R_max, float sm_scale,
+                              void *out, float *partial,
+                              void *workspace, size_t workspace_bytes, void *stream);
+
+/* LSE merge of G partials (the cross-GPU step of the sequence split, §8(e)):
+ * parts fp32 [G][B][Hq][d+2] as written by wq_decode_attention;
+ * out[b][hq] = sum_g e^{m_g - m*} o_g / sum_g e^{m_g - m*} l_g, m* = max_g m_g.
+ * out: fp16 [B][Hq][d]. */
+wq_status wq_merge_partials(const float *parts, int32_t G, const wq_geom *g,
+                            void *out, void *stream);
+
+/* Thread-local message of the last non-OK status of this thread. */
+const char *wq_last_error(void);
+
+/* Library build id (git describe at build time) and the SM arch it targets. */
+const char *wq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WQ_H_ */

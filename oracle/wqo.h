@@ -1,0 +1,102 @@
+/*
+ * wqo.h — CPU ORACLE for the WindowQuant hot path.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+ * leg may load this library.  It shares no code, header, table or constant
+ * generator with the CUDA path (paper_2605_02262_b200/csrc); it re-derives
+ * everything from the paper (PAPER.md, "P:n" = line n) and the readings Qn
+ * listed in DESIGN.md §3.  Arithmetic is fp64 except where the contract fixes
+ * fp32 (the quantizer, Q17).  Compiled with -O2 -ffp-contract=off -fno-fast-math.
+ *
+ * Every function is the slow literal form of the definition it cites:
+ *   wqo_window_score      Eq.8 double sum over (text token, window token) pairs
+ *   wqo_thresholds        Eq.10-11
+ *   wqo_assign_bits       P:313 bands, P:322 pin, P:395 vote, Q13 budget loop,
+ *                         Alg.2 P:420-444 stable partition
+ *   wqo_quantize_group    Eq.14-16 under reading Q17
+ *   wqo_reorder_quantize_pack   Alg.2 prefill branch -> the D-1 byte image
+ *   wqo_decode_attention  Eq.2-3 (no mask) over the dequantized cache
+ *                         rebuilt in ORIGINAL token order (Eq.12-13)
+ *   wqo_bruteforce_attention    Eq.2-3 on the unquantized fp16 K/V
+ *   wqo_merge             LSE merge of shard partials
+ */
+#ifndef WQO_H_
+#define WQO_H_
+#include <stdint.h>
+
+typedef struct {
+  int32_t B, H, Hq, d, M, S, n_widths;
+  int32_t widths[4];
+} wqo_geom;
+
+/* fp16 <-> float conversions written out bit by bit */
+double   wqo_f16_to_f64(uint16_t h);
+uint16_t wqo_f32_to_f16_ru(float x);   /* round toward +infinity */
+uint16_t wqo_f32_to_f16_rn(float x);   /* round to nearest, ties to even */
+
+/* Eq.10-11 */
+double wqo_f1(double s, double alpha);
+double wqo_f2(double s, double alpha);
+int    wqo_thresholds(const double *s, int32_t L, double alpha, int32_t n, double *thr);
+
+/* Eq.8 for one window / all windows (OpenMP over (b, w)) */
+double wqo_window_score(const uint16_t *vis_b, int64_t vis_row_stride,
+                        const uint16_t *txt_b, int64_t txt_row_stride,
+                        int32_t N, int32_t D, int32_t S, int32_t w);
+void   wqo_window_scores(const uint16_t *vis, int64_t vrs, int64_t vbs,
+                         const uint16_t *txt, int64_t trs, int64_t tbs,
+                         int32_t B, int32_t M, int32_t N, int32_t D, int32_t S,
+                         double *scores);
+
+/* Alg.1 band/pin/vote + budget + Alg.2 partition.  Returns 0, or 3 if the
+ * budget is infeasible. */
+int wqo_assign_bits(const double *scores, const double *thr, int32_t L,
+                    const wqo_geom *g, double budget, int32_t pin, int32_t vote,
+                    uint8_t *bits, int32_t *rank, int32_t *perm, int32_t *seg_off);
+
+/* Byte accounting (D-1) */
+int64_t wqo_record_bytes(int32_t b, int32_t d, int32_t S);
+int64_t wqo_packed_bytes(const wqo_geom *g, const int32_t n_per_class[4], int32_t code_only);
+int64_t wqo_kv_code_bytes(const int64_t tokens_per_class[4], int32_t d, int32_t H);
+void    wqo_layer_layout(const wqo_geom *g, const int32_t *seg_off_l, int64_t *offs);
+
+/* Eq.14-16 (Q17) for one group of n fp16 values x[i*stride] */
+void wqo_quantize_group(const uint16_t *x, int32_t n, int64_t stride, int32_t bits,
+                        uint16_t *s_out, uint16_t *mn_out, uint8_t *codes);
+
+/* Position of element (row, col) of a code tile (D-1): byte offset of its
+ * 32-bit word inside the tile and its bit offset inside that word. */
+void wqo_code_pos(int32_t is_v, int32_t d, int32_t b, int32_t t, int32_t c,
+                  int64_t *byte_off, int32_t *bit);
+
+void wqo_reorder_quantize_pack(const uint16_t *k, const uint16_t *v, const int64_t strides[3],
+                               int32_t vis_off, const wqo_geom *g,
+                               const int32_t *perm_l, int32_t perm_stride,
+                               const int32_t *seg_off_l, const int64_t *offs,
+                               uint8_t *packed);
+
+/* Dequantize the record of one (b, h, slot) into fp64 K^[S][d], V^[S][d]. */
+void wqo_dequant_record(const uint8_t *rec, int32_t bits, int32_t d, int32_t S,
+                        double *kh, double *vh);
+
+/* out: fp64 [B][Hq][d]; partial: fp64 [B][Hq][d+2] or NULL. */
+void wqo_decode_attention(const uint16_t *q, const uint8_t *packed, const int64_t *offs,
+                          const int32_t *seg_off_l, const int32_t *perm_l, int32_t perm_stride,
+                          const wqo_geom *g,
+                          const uint16_t *k_rest, const uint16_t *v_rest,
+                          const int64_t rest_strides[2], const int32_t *rest_len,
+                          float sm_scale, double *out, double *partial);
+
+/* Attention of each (b, hq) over the unquantized fp16 tokens of the windows
+ * listed in win_l[b][0..n_win[b]) (window order as listed) plus the rest. */
+void wqo_bruteforce_attention(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                              const int64_t strides[3], int32_t vis_off, const wqo_geom *g,
+                              const int32_t *win_l, int32_t win_stride, const int32_t *n_win,
+                              const uint16_t *k_rest, const uint16_t *v_rest,
+                              const int64_t rest_strides[2], const int32_t *rest_len,
+                              float sm_scale, double *out);
+
+/* parts [G][B*Hq][d+2] (m, l, o) -> out [B*Hq][d] */
+void wqo_merge(const double *parts, int32_t G, int32_t BHq, int32_t d, double *out);
+
+#endif
