@@ -1,0 +1,493 @@
+#!/usr/bin/env python
+"""bench.py -- the WindowQuant hot path on B200 (driver contract).
+
+One STEP = one pass of the whole hot path over one batch in the
+paper's serving setting (T5: the search and quantization run once per
+request batch, then 50 tokens are generated):
+    wq_window_scores -> wq_assign_bits (all L layers) -> L x (wq_layer_layout +
+    wq_reorder_quantize_pack) -> 50 x L x wq_decode_attention
+(+ one NCCL all-gather of (m, l, o) partials and wq_merge_partials per decode call
+under the N > 1 sequence split).  value = generated tokens / s = B * 50 / step time.
+
+Default workload: C5, the 7B long-video config the north-star targets are quoted
+on (256 frames x 196 = 50,176 visual tokens, B = 4, 28 layers, S = 32,
+widths {2,4,8,16}).  Inputs are seeded synthetic tensors resident in HBM;
+28 layers x ~108 MB packed images >> 126 MB L2, so every decode call reads HBM.
+
+--impl reference times the CPU oracle (oracle/, plain C fp64) on a bounded sample
+of the same workload (there is no reference implementation; BASELINE.json).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode-attn tokens/s + achieved HBM GB/s vs peak; quantize-pack GB/s (1/2/4/8 B200)"
+UNIT = "tokens/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampled DURING the timed region
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# the CUDA path
+# ------------------------------------------------------------------------------------------
+class Workload:
+    """All inputs of one batch of cfg resident on the device, plus the output and
+    scratch buffers of the path.  Under a sequence split each rank quantizes and
+    decodes its share of every width segment (wq_shard_slots)."""
+
+    def __init__(self, cfg, device, rank=0, world=1, n_gen=None):
+        import torch
+        from paper_2605_02262_b200 import synth, wq
+        self.torch, self.wq = torch, wq
+        self.cfg, self.dev, self.rank, self.world = cfg, device, rank, world
+        m = cfg.model
+        self.m = m
+        self.L = cfg.layers
+        self.n_gen = cfg.n_gen if n_gen is None else n_gen
+        B = cfg.B
+        self.g = wq.geom(B, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
+        self.opts = wq.AssignOpts(cfg.budget, 1, 0)
+        self.thr = wq.wq_thresholds(cfg.sensitivities(), cfg.alpha, len(cfg.widths))
+        self.sm_scale = 1.0 / math.sqrt(m.d)
+        # inputs
+        self.vis, self.txt = synth.embeddings(B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, device)
+        self.K, self.V, self.kr, self.vr = [], [], [], []
+        for l in range(self.L):
+            K, V, kr, vr, rest_len = synth.layer_tensors(cfg, l, device)
+            self.K.append(K); self.V.append(V); self.kr.append(kr); self.vr.append(vr)
+        base = int(rest_len[0].item())
+        steps = [[base + t + 1] * B for t in range(self.n_gen)]
+        self.rest_len = torch.tensor(steps, dtype=torch.int32, device=device)       # [n_gen][B]
+        self.rest_zero = torch.zeros((B,), dtype=torch.int32, device=device)
+        self.q = torch.stack([torch.stack([synth.queries(B, m.Hq, m.H, m.d, cfg.seed, l, t, device)
+                                           for l in range(self.L)]) for t in range(self.n_gen)])
+        # path buffers
+        W = cfg.W
+        self.scores = torch.empty((B, W), dtype=torch.float64, device=device)
+        self.sws = torch.empty(wq.wq_window_scores_workspace(B, m.D), dtype=torch.uint8, device=device)
+        self.bits = torch.empty((self.L, B, W), dtype=torch.uint8, device=device)
+        self.rank_t = torch.empty((B, W), dtype=torch.int32, device=device)
+        self.perm = torch.empty((self.L, B, W), dtype=torch.int32, device=device)
+        self.seg = torch.empty((self.L, B, 5), dtype=torch.int32, device=device)
+        self.perm_r = torch.empty((self.L, B, W), dtype=torch.int32, device=device)
+        self.seg_r = torch.empty((self.L, B, 5), dtype=torch.int32, device=device)
+        self.offs = torch.empty((self.L, B * m.H + 1), dtype=torch.int64, device=device)
+        self.dws = torch.zeros(wq.wq_decode_workspace(self.g), dtype=torch.uint8, device=device)
+        self.out = torch.empty((self.n_gen, self.L, B, m.Hq, m.d), dtype=torch.float16, device=device)
+        self.part = torch.empty((B, m.Hq, m.d + 2), dtype=torch.float32, device=device) if world > 1 else None
+        self.gathered = (torch.empty((world, B, m.Hq, m.d + 2), dtype=torch.float32, device=device)
+                         if world > 1 else None)
+        # size the packed images once (setup, untimed): they depend only on the inputs
+        self.packed = None
+        self._setup_pass()
+
+    def _setup_pass(self):
+        torch, wq = self.torch, self.wq
+        self.search()
+        for l in range(self.L):
+            wq.wq_layer_layout(self.g, self.seg_r[l], self.offs[l])
+        torch.cuda.synchronize()
+        sizes = self.offs[:, -1].cpu().tolist()
+        self.packed = [torch.zeros(int(s) + 16, dtype=torch.uint8, device=self.dev) for s in sizes]
+        self.packed_bytes = [int(s) for s in sizes]
+        seg = self.seg.cpu().numpy()
+        self.class_windows = (seg[:, :, 1:] - seg[:, :, :-1]).sum(axis=(0, 1)).tolist()
+
+    # --- the four calls ---
+    def search(self):
+        wq = self.wq
+        wq.wq_window_scores(self.vis, self.txt, self.cfg.S, scores=self.scores, workspace=self.sws)
+        wq.wq_assign_bits(self.scores, self.thr, self.L, self.g, self.opts, self.bits, self.rank_t, self.perm,
+                          self.seg)
+        if self.world > 1:
+            for l in range(self.L):
+                wq.wq_shard_slots(self.perm[l], self.seg[l], self.world, self.rank, self.perm_r[l], self.seg_r[l])
+        else:
+            self.perm_r, self.seg_r = self.perm, self.seg
+
+    def quantize(self):
+        wq = self.wq
+        for l in range(self.L):
+            wq.wq_layer_layout(self.g, self.seg_r[l], self.offs[l])
+            wq.wq_reorder_quantize_pack(self.K[l], self.V[l], 0, self.g, self.perm_r[l], self.seg_r[l],
+                                        self.offs[l], self.packed[l])
+
+    def decode(self, group=None):
+        torch, wq = self.torch, self.wq
+        for t in range(self.n_gen):
+            rl = self.rest_len[t] if self.rank == 0 else self.rest_zero
+            for l in range(self.L):
+                if self.world == 1:
+                    wq.wq_decode_attention(self.q[t, l], self.packed[l], self.offs[l], self.seg_r[l], self.g,
+                                           self.kr[l], self.vr[l], rl, self.sm_scale, out=self.out[t, l],
+                                           workspace=self.dws)
+                else:
+                    wq.wq_decode_attention(self.q[t, l], self.packed[l], self.offs[l], self.seg_r[l], self.g,
+                                           self.kr[l], self.vr[l], rl, self.sm_scale, partial=self.part,
+                                           workspace=self.dws)
+                    torch.distributed.all_gather_into_tensor(self.gathered, self.part, group=group)
+                    wq.wq_merge_partials(self.gathered, self.g, out=self.out[t, l])
+
+    def launches_per_step(self):
+        per_dec = 1 if self.world == 1 else 2
+        shard = self.L if self.world > 1 else 0
+        return 2 + 2 + shard + 2 * self.L + self.n_gen * self.L * per_dec
+
+    def decode_bytes_per_call(self, l):
+        """Algorithmic bytes of one wq_decode_attention launch: the
+        packed image + FP16 rest tokens (K and V) + q read + out written."""
+        cfg, m = self.cfg, self.m
+        rest_tok = (cfg.tail + cfg.n_text + self.n_gen / 2 + 0.5) if self.rank == 0 else 0
+        rest = cfg.B * m.H * rest_tok * m.d * 4
+        qo = 2 * cfg.B * m.Hq * m.d * 2
+        return self.packed_bytes[l] + rest + qo
+
+    def quant_bytes_per_call(self, l):
+        """read fp16 K+V of the rank's windows + write the packed image."""
+        cfg, m = self.cfg, self.m
+        n_win = int(self.seg_r[l][:, 4].sum().item())
+        return n_win * m.H * cfg.S * m.d * 4 + self.packed_bytes[l]
+
+
+def run_wq(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_02262_b200 import configs, wq
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    wq.load(build_if_missing=False)
+    cfg = configs.CONFIGS[args.config]
+    if args.layers:
+        cfg = cfg.with_(layers=args.layers)
+    w = Workload(cfg, dev, rank, world, n_gen=args.n_gen)
+    group = dist.group.WORLD if world > 1 else None
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        w.search()
+        w.quantize()
+        if ev is not None:
+            ev[0].record(stream)
+        w.decode(group)
+        if ev is not None:
+            ev[1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev_all = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev_dec = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        ev_all[0].record(stream)
+        for s in range(args.steps):
+            step(ev_dec[s])
+        ev_all[1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = ev_all[0].elapsed_time(ev_all[1])
+    dec_ms = sum(e[0].elapsed_time(e[1]) for e in ev_dec)
+    # isolated quantize timing (one pass over the L layers), for the quantize GB/s figure
+    qe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    qe[0].record(stream)
+    w.quantize()
+    qe[1].record(stream)
+    torch.cuda.synchronize()
+    quant_ms = qe[0].elapsed_time(qe[1])
+    t = torch.tensor([total_ms, dec_ms, quant_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, dec_ms, quant_ms = t.tolist()
+
+    ms_per_step = total_ms / args.steps
+    tokens = cfg.B * w.n_gen
+    value = tokens / (ms_per_step / 1e3)
+    n_dec = args.steps * w.n_gen * cfg.layers
+    dec_launch_us = dec_ms * 1e3 / n_dec
+    dec_bytes = float(np.mean([w.decode_bytes_per_call(l) for l in range(cfg.layers)]))
+    peak, peak_src = peaks()
+    achieved = dec_bytes / (dec_launch_us * 1e-6) / 1e9
+    q_bytes = float(sum(w.quant_bytes_per_call(l) for l in range(cfg.layers)))
+    q_gbs = q_bytes / (quant_ms * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "decode_dram_bytes.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(cfg.name)
+        except Exception:
+            traffic = None
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f16",
+        "data": "synthetic (seeded; shapes of LLaVA-OneVision-7B / Qwen2-7B video workloads)",
+        "config": {"workload": cfg.name, "model_shape": cfg.model.name, "layers": cfg.layers, "batch": cfg.B,
+                   "visual_tokens": cfg.M, "window": cfg.S, "widths": list(cfg.widths), "gen_tokens": w.n_gen,
+                   "parallelism": f"seqsplit{world}" if world > 1 else "single",
+                   "l2": f"inputs > L2: {cfg.layers} layers x {w.packed_bytes[0] / 1e6:.0f} MB packed rotated",
+                   "window_mix": dict(zip(["2", "4", "8", "16"], [int(x) for x in w.class_windows]))},
+        "roofline": {"bound": "hbm", "kernel": "wq_decode_attention", "achieved": round(achieved, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "bytes_per_launch": round(dec_bytes), "avg_launch_us": round(dec_launch_us, 3),
+                     "peak_source": peak_src},
+        "quantize": {"kernel": "wq_reorder_quantize_pack", "GB/s": round(q_gbs, 1),
+                     "frac": round(q_gbs / peak, 4), "ms_per_L_layers": round(quant_ms, 3),
+                     "bytes_L_layers": round(q_bytes)},
+        "decode_only_tokens_per_s": round(cfg.B / (dec_launch_us * 1e-6 * cfg.layers), 1),
+        "gpu_launches": w.launches_per_step() * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_e2e:
+        result["e2e"] = run_e2e(w, args, stream)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(cfg, w, args)
+    return result
+
+
+def run_e2e(w, args, stream):
+    """Same metric through the public API with HOST inputs: every step copies its
+    inputs (embeddings, per-layer K/V + rest, queries) from pinned host memory and
+    reads all decode outputs back, inside the timed region."""
+    import torch
+    dev = w.dev
+    host = {}
+    names = ["vis", "txt"]
+    for n in names:
+        host[n] = getattr(w, n).cpu().pin_memory()
+    hK = [k.cpu().pin_memory() for k in w.K]
+    hV = [v.cpu().pin_memory() for v in w.V]
+    hkr = [k.cpu().pin_memory() for k in w.kr]
+    hvr = [v.cpu().pin_memory() for v in w.vr]
+    hq = w.q.cpu().pin_memory()
+    hout = torch.empty(w.out.shape, dtype=w.out.dtype).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in [host["vis"], host["txt"], hq] + hK + hV + hkr + hvr)
+    d2h = hout.numel() * hout.element_size()
+    steps = max(1, min(args.steps, 3))
+
+    def step():
+        w.vis.copy_(host["vis"], non_blocking=True)
+        w.txt.copy_(host["txt"], non_blocking=True)
+        for l in range(w.L):
+            w.K[l].copy_(hK[l], non_blocking=True)
+            w.V[l].copy_(hV[l], non_blocking=True)
+            w.kr[l].copy_(hkr[l], non_blocking=True)
+            w.vr[l].copy_(hvr[l], non_blocking=True)
+        w.q.copy_(hq, non_blocking=True)
+        w.search()
+        w.quantize()
+        w.decode()
+        hout.copy_(w.out, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"value": round(w.cfg.B * w.n_gen / (ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "steps": steps}
+
+
+# ------------------------------------------------------------------------------------------
+# the CPU oracle (reference arm / cpu_baseline)
+# ------------------------------------------------------------------------------------------
+def oracle_sample_time(cfg, tensors):
+    """Oracle seconds for a bounded sample of one step: request 0, the last layer,
+    one generated token; extrapolated linearly in requests, layers and tokens."""
+    import oracle
+    vis, txt, K, V, kr, vr, rest_len, q = tensors
+    m = cfg.model
+    og1 = oracle.geom(1, m.H, m.Hq, m.d, cfg.M, cfg.S, list(cfg.widths))
+    t0 = time.perf_counter()
+    sc = oracle.window_scores(vis[:1], txt[:1], cfg.S)
+    t1 = time.perf_counter()
+    thr = oracle.thresholds(cfg.sensitivities(), cfg.alpha, len(cfg.widths))
+    bits, rank, perm, seg = oracle.assign_bits(sc, thr, og1, cfg.budget, 1, 0)
+    t2 = time.perf_counter()
+    l = cfg.layers - 1
+    pk, offs = oracle.reorder_quantize_pack(K[:1], V[:1], 0, og1, perm[l], seg[l])
+    t3 = time.perf_counter()
+    oracle.decode_attention(q[:1], pk, offs, seg[l], perm[l], og1, kr[:1], vr[:1], rest_len[:1],
+                            1 / math.sqrt(m.d))
+    t4 = time.perf_counter()
+    per = {"scores_1req": t1 - t0, "assign_1req_all_layers": t2 - t1, "quantize_1req_1layer": t3 - t2,
+           "decode_1req_1layer_1token": t4 - t3}
+    est = (per["scores_1req"] * cfg.B + per["assign_1req_all_layers"] * cfg.B
+           + per["quantize_1req_1layer"] * cfg.B * cfg.layers
+           + per["decode_1req_1layer_1token"] * cfg.B * cfg.layers * cfg.n_gen)
+    return est, per, t4 - t0
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, w, args):
+    vis, txt = w.vis[:1].cpu().numpy(), w.txt[:1].cpu().numpy()
+    l = cfg.layers - 1
+    tensors = (vis, txt, w.K[l][:1].cpu().numpy(), w.V[l][:1].cpu().numpy(), w.kr[l][:1].cpu().numpy(),
+               w.vr[l][:1].cpu().numpy(), w.rest_len[0][:1].cpu().numpy(), w.q[0, l][:1].cpu().numpy())
+    est, per, wall = oracle_sample_time(cfg, tensors)
+    return {"value": round(cfg.B * cfg.n_gen / est, 4), "unit": UNIT, "cores": _cores(), "kind": "oracle",
+            "sample": (f"request 0, layer {l}, 1 generated token of {cfg.name} (scores + assign + quantize + decode), "
+                       f"{wall:.1f}s of CPU work, extrapolated linearly to B={cfg.B} x {cfg.layers} layers x "
+                       f"{cfg.n_gen} tokens"),
+            "per_phase_s": {k: round(v, 4) for k, v in per.items()}}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands on this box's host cores."""
+    if rank != 0:
+        return None
+    import torch
+    from paper_2605_02262_b200 import configs, synth
+    cfg = configs.CONFIGS[args.config]
+    m = cfg.model
+    l = cfg.layers - 1
+    vis, txt = synth.embeddings(1, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, "cpu")
+    K, V, kr, vr, rest_len = synth.layer_tensors(cfg, l, "cpu", B=1)
+    rest_len = rest_len + 1
+    q = synth.queries(1, m.Hq, m.H, m.d, cfg.seed, l, 0, "cpu")
+    tensors = tuple(t.numpy() for t in (vis, txt, K, V, kr, vr, rest_len, q))
+    times = []
+    for _ in range(args.warmup):
+        oracle_sample_time(cfg, tensors)
+    for _ in range(args.steps):
+        est, per, wall = oracle_sample_time(cfg, tensors)
+        times.append(est)
+    ms = float(np.mean(times)) * 1e3
+    value = cfg.B * cfg.n_gen / (ms / 1e3)
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "layers": cfg.layers, "batch": cfg.B, "visual_tokens": cfg.M,
+                       "window": cfg.S, "widths": list(cfg.widths), "gen_tokens": cfg.n_gen},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "kind": "oracle", "cores": _cores(),
+                             "sample": (f"each step: request 0, layer {l}, 1 token of {cfg.name}; "
+                                        f"time extrapolated to the full step")},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="wq", choices=["wq", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--layers", type=int, default=0, help="override the layer count (profiling only)")
+    ap.add_argument("--n-gen", type=int, default=None, help="override generated tokens (profiling only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_wq(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -217,6 +217,17 @@ wq_status wq_decode_attention(const void *q, const uint8_t *packed, const int64_
 wq_status wq_merge_partials(const float *parts, int32_t G, const wq_geom *g,
                             void *out, void *stream);
 
+/* Sequence split of the long-video case (§8(e)): rank r of G keeps, in every
+ * width segment k of request b, the contiguous slot chunk
+ *   [seg[k] + n_k*r/G, seg[k] + n_k*(r+1)/G),  n_k = seg[k+1] - seg[k]
+ * (integer division), so every rank holds the same precision mix and bytes.
+ * perm_l/seg_off_l: i32 [B][W] / [B][5] (device) as from wq_assign_bits;
+ * outputs perm_r i32 [B][W] (first seg_off_r[b][4] entries valid), seg_off_r
+ * i32 [B][5].  The rank's image is then built and decoded with perm_r/seg_off_r
+ * and its (m, l, o) partials merged with wq_merge_partials after an all-gather. */
+wq_status wq_shard_slots(const int32_t *perm_l, const int32_t *seg_off_l, int32_t B, int32_t W,
+                         int32_t G, int32_t r, int32_t *perm_r, int32_t *seg_off_r, void *stream);
+
 /* Thread-local message of the last non-OK status of this thread. */
 const char *wq_last_error(void);
 

@@ -1,0 +1,243 @@
+// abi.cu -- the extern "C" boundary of libwq.so (include/wq.h).  Host-side argument
+// validation (synchronous, status + wq_last_error) and kernel launches; no compute
+// happens here and there is no CPU fallback.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/wq.h"
+#include "wq_device.cuh"
+#include "wq_internal.h"
+
+#ifndef WQ_BUILD_ID
+#define WQ_BUILD_ID "dev"
+#endif
+
+namespace {
+thread_local char g_err[512] = "";
+
+wq_status fail(wq_status s, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+wq_status cuda_status(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return WQ_OK;
+  return fail(WQ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+wq_status check_geom(const wq_geom *g, bool need_heads) {
+  if (!g) return fail(WQ_EINVAL, "geom is NULL");
+  if (g->B < 1 || g->M < 0) return fail(WQ_ESHAPE, "B=%d M=%d", g->B, g->M);
+  if (!(g->S == 16 || g->S == 32 || g->S == 64 || g->S == 128))
+    return fail(WQ_ESHAPE, "window S=%d not in {16,32,64,128}", g->S);
+  if (g->n_widths < 1 || g->n_widths > 4) return fail(WQ_ESHAPE, "n_widths=%d not in 1..4", g->n_widths);
+  for (int i = 0; i < g->n_widths; i++) {
+    int w = g->widths[i];
+    if (!(w == 2 || w == 4 || w == 8 || w == 16)) return fail(WQ_ESHAPE, "widths[%d]=%d not in {2,4,8,16}", i, w);
+    if (i && w <= g->widths[i - 1]) return fail(WQ_ESHAPE, "widths must be strictly ascending");
+  }
+  if (need_heads) {
+    if (!(g->d == 64 || g->d == 128)) return fail(WQ_EUNSUPPORTED, "head dim d=%d not in {64,128}", g->d);
+    if (g->H < 1 || g->Hq < g->H || g->Hq % g->H) return fail(WQ_ESHAPE, "Hq=%d not a multiple of H=%d", g->Hq, g->H);
+    if (g->Hq / g->H > 8) return fail(WQ_EUNSUPPORTED, "GQA group Hq/H=%d > 8", g->Hq / g->H);
+    if ((int64_t)g->B * g->H > 1024) return fail(WQ_EUNSUPPORTED, "B*H=%lld > 1024", (long long)g->B * g->H);
+  }
+  return WQ_OK;
+}
+
+cudaStream_t S_(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace
+
+namespace wq {
+int device_sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 1;
+}
+}  // namespace wq
+
+extern "C" {
+
+const char *wq_last_error(void) { return g_err; }
+const char *wq_version(void) { return WQ_BUILD_ID " sm_100a"; }
+
+wq_status wq_thresholds(const double *s_host, int32_t L, double alpha, int32_t n_widths, double *thr_host) {
+  if (!s_host || (n_widths > 1 && !thr_host)) return fail(WQ_EINVAL, "NULL pointer");
+  if (L < 1) return fail(WQ_EINVAL, "L=%d < 1", L);
+  if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(WQ_EINVAL, "alpha=%g must be > 0 (P:358)", alpha);
+  if (n_widths < 1 || n_widths > 4) return fail(WQ_EINVAL, "n_widths=%d not in 1..4", n_widths);
+  for (int l = 0; l < L; l++) {
+    double s = s_host[l];
+    s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);                       // Q10
+    double f1 = (std::exp(alpha * s) - 1.0) / (std::exp(alpha) - 1.0);    // Eq.10
+    double f2 = (std::exp(-alpha * s) - 1.0) / (std::exp(-alpha) - 1.0);  // Eq.11
+    double *t = thr_host + (int64_t)l * (n_widths - 1);
+    if (n_widths == 2) t[0] = (f1 + f2) / 2.0;
+    if (n_widths == 3) { t[0] = f1; t[1] = f2; }
+    if (n_widths == 4) { t[0] = f1; t[1] = (f1 + f2) / 2.0; t[2] = f2; }
+  }
+  return WQ_OK;
+}
+
+wq_status wq_window_scores_workspace(int32_t B, int32_t D, size_t *bytes_host) {
+  if (!bytes_host) return fail(WQ_EINVAL, "bytes_host is NULL");
+  if (B < 1 || D < 8) return fail(WQ_ESHAPE, "B=%d D=%d", B, D);
+  *bytes_host = (size_t)B * D * sizeof(double);
+  return WQ_OK;
+}
+
+wq_status wq_window_scores(const void *vis, int64_t vrs, int64_t vbs, const void *txt, int64_t trs,
+                           int64_t tbs, int32_t B, int32_t M, int32_t N, int32_t D, int32_t S,
+                           double *scores, void *workspace, size_t workspace_bytes, void *stream) {
+  if (!vis || !txt || !scores || !workspace) return fail(WQ_EINVAL, "NULL pointer");
+  if (!(S == 16 || S == 32 || S == 64 || S == 128)) return fail(WQ_ESHAPE, "S=%d not in {16,32,64,128}", S);
+  if (B < 1 || N < 1 || M < S) return fail(WQ_ESHAPE, "B=%d N=%d M=%d (need M >= S=%d)", B, N, M, S);
+  if (D % 8 || D < 8 || D > 4096) return fail(WQ_ESHAPE, "D=%d must be a multiple of 8 in [8, 4096]", D);
+  if (vrs % 8 || vbs % 8 || trs % 8 || tbs % 8 || !aligned16(vis) || !aligned16(txt))
+    return fail(WQ_EINVAL, "rows must be 16-byte aligned (strides multiple of 8 elements)");
+  if (workspace_bytes < (size_t)B * D * sizeof(double)) return fail(WQ_EINVAL, "workspace too small");
+  double *tbar = reinterpret_cast<double *>(workspace);
+  wq_status s = cuda_status(wq::launch_text_pool((const __half *)txt, trs, tbs, B, N, D, tbar, S_(stream)),
+                            "text pool");
+  if (s != WQ_OK) return s;
+  return cuda_status(
+      wq::launch_window_scores((const __half *)vis, vrs, vbs, B, M, N, D, S, tbar, scores, S_(stream)),
+      "window scores");
+}
+
+wq_status wq_assign_bits(const double *scores, const double *thr_host, int32_t L, const wq_geom *g,
+                         const wq_assign_opts *opts, uint8_t *bits, int32_t *rank, int32_t *perm,
+                         int32_t *seg_off, void *stream) {
+  wq_status s = check_geom(g, false);
+  if (s != WQ_OK) return s;
+  if (!scores || !bits || !perm || !seg_off || (g->n_widths > 1 && !thr_host))
+    return fail(WQ_EINVAL, "NULL pointer");
+  if (L < 1 || L > wq::MAX_LAYERS) return fail(WQ_EINVAL, "L=%d not in 1..%d", L, wq::MAX_LAYERS);
+  const int W = g->M / g->S;
+  if (W < 1 || W > 4096) return fail(WQ_ESHAPE, "W=M/S=%d not in 1..4096", W);
+  wq::AssignParams p{};
+  p.L = L; p.B = g->B; p.W = W; p.n_widths = g->n_widths;
+  for (int i = 0; i < 4; i++) p.widths[i] = i < g->n_widths ? g->widths[i] : 0;
+  p.pin = opts ? opts->pin_first : 1;
+  p.vote = opts ? opts->batch_vote : 0;
+  p.budget = opts ? opts->budget_avg_bits : 0.0;
+  const int np = p.pin ? 1 : 0;
+  if (p.budget > 0.0 && (double)(16 * np + g->widths[0] * (W - np)) > p.budget * (double)W)
+    return fail(WQ_EBUDGET, "budget %.4f bits infeasible: pinned window + %d x %d-bit windows exceed it",
+                p.budget, W - np, g->widths[0]);
+  for (int l = 0; l < L; l++)
+    for (int j = 0; j < g->n_widths - 1; j++) p.thr[l * 3 + j] = thr_host[(int64_t)l * (g->n_widths - 1) + j];
+  if (rank) {
+    s = cuda_status(wq::launch_rank(scores, g->B, W, rank, S_(stream)), "rank");
+    if (s != WQ_OK) return s;
+  }
+  return cuda_status(wq::launch_assign(scores, p, bits, perm, seg_off, S_(stream)), "assign");
+}
+
+wq_status wq_packed_bytes(const wq_geom *g, const int32_t n_per_class_host[4], int32_t code_bytes_only,
+                          int64_t *bytes_host) {
+  if (!g || !n_per_class_host || !bytes_host) return fail(WQ_EINVAL, "NULL pointer");
+  static const int cb[4] = {2, 4, 8, 16};
+  int64_t t = 0;
+  for (int k = 0; k < 4; k++) {
+    int64_t rec = code_bytes_only ? (int64_t)g->S * g->d * cb[k] / 4 : wq::record_bytes(cb[k], g->d, g->S);
+    t += (int64_t)n_per_class_host[k] * rec;
+  }
+  *bytes_host = t;
+  return WQ_OK;
+}
+
+wq_status wq_layer_layout(const wq_geom *g, const int32_t *seg_off_l, int64_t *offs, void *stream) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!seg_off_l || !offs) return fail(WQ_EINVAL, "NULL pointer");
+  if (g->B > 4096) return fail(WQ_ESHAPE, "B=%d > 4096", g->B);
+  return cuda_status(wq::launch_layer_layout(seg_off_l, g->B, g->H, g->d, g->S, offs, S_(stream)), "layout");
+}
+
+wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t strides[3], int32_t vis_off,
+                                   const wq_geom *g, const int32_t *perm_l, int32_t perm_stride,
+                                   const int32_t *seg_off_l, const int64_t *offs, uint8_t *packed,
+                                   void *stream) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!k || !v || !strides || !perm_l || !seg_off_l || !offs || !packed) return fail(WQ_EINVAL, "NULL pointer");
+  if (perm_stride < 1) return fail(WQ_EINVAL, "perm_stride=%d", perm_stride);
+  if (strides[0] % 8 || strides[1] % 8 || strides[2] % 8 || !aligned16(k) || !aligned16(v) || !aligned16(packed))
+    return fail(WQ_EINVAL, "K/V rows and the packed image must be 16-byte aligned");
+  if (strides[2] < g->d) return fail(WQ_ESHAPE, "token stride %lld < d=%d", (long long)strides[2], g->d);
+  if (vis_off < 0) return fail(WQ_EINVAL, "vis_off=%d", vis_off);
+  return cuda_status(wq::launch_quant((const __half *)k, (const __half *)v, strides, vis_off, g->B, g->H, g->d,
+                                      g->S, perm_l, perm_stride, seg_off_l, offs, packed, S_(stream)),
+                     "quantize");
+}
+
+wq_status wq_decode_workspace(const wq_geom *g, size_t *bytes_host) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!bytes_host) return fail(WQ_EINVAL, "bytes_host is NULL");
+  *bytes_host = wq::decode_workspace_bytes(g->B, g->H, g->Hq, g->d, wq::device_sm_count());
+  return WQ_OK;
+}
+
+wq_status wq_decode_attention(const void *q, const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l,
+                              const wq_geom *g, const void *k_rest, const void *v_rest,
+                              const int64_t rest_strides[2], const int32_t *rest_len, int32_t R_max,
+                              float sm_scale, void *out, float *partial, void *workspace,
+                              size_t workspace_bytes, void *stream) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!q || !packed || !offs || !seg_off_l || !workspace) return fail(WQ_EINVAL, "NULL pointer");
+  if (!out && !partial) return fail(WQ_EINVAL, "both out and partial are NULL");
+  if (R_max < 0) return fail(WQ_EINVAL, "R_max=%d", R_max);
+  if (R_max > 0 && (!k_rest || !v_rest || !rest_len || !rest_strides))
+    return fail(WQ_EINVAL, "rest buffers NULL with R_max=%d", R_max);
+  if (R_max > 0 && (rest_strides[0] % 8 || rest_strides[1] % 8 || !aligned16(k_rest) || !aligned16(v_rest)))
+    return fail(WQ_EINVAL, "rest rows must be 16-byte aligned");
+  if (!aligned16(packed) || !aligned16(q)) return fail(WQ_EINVAL, "packed / q must be 16-byte aligned");
+  if (!(sm_scale > 0.f) || !std::isfinite(sm_scale)) return fail(WQ_EINVAL, "sm_scale=%g", (double)sm_scale);
+  const int sms = wq::device_sm_count();
+  if (workspace_bytes < wq::decode_workspace_bytes(g->B, g->H, g->Hq, g->d, sms))
+    return fail(WQ_EINVAL, "workspace too small (see wq_decode_workspace)");
+  wq::DecodeArgs a{};
+  a.q = (const __half *)q; a.packed = packed; a.offs = offs; a.seg_off = seg_off_l;
+  a.k_rest = (const __half *)k_rest; a.v_rest = (const __half *)v_rest;
+  a.rs_b = R_max > 0 ? rest_strides[0] : 0; a.rs_h = R_max > 0 ? rest_strides[1] : 0;
+  a.rest_len = R_max > 0 ? rest_len : nullptr; a.R_max = R_max;
+  a.B = g->B; a.H = g->H; a.Hq = g->Hq; a.grp = g->Hq / g->H; a.d = g->d; a.S = g->S;
+  a.scale_log2 = sm_scale * 1.4426950408889634f;
+  a.out = (__half *)out; a.partial = partial;
+  const int grp = a.grp;
+  size_t part = (size_t)(sms + g->B * g->H) * grp * (g->d + 2) * sizeof(float);
+  part = (part + 255) / 256 * 256;
+  a.ws_part = reinterpret_cast<float *>(workspace);
+  a.ws_cnt = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(workspace) + part);
+  return cuda_status(wq::launch_decode(a, sms, S_(stream)), "decode");
+}
+
+wq_status wq_merge_partials(const float *parts, int32_t G, const wq_geom *g, void *out, void *stream) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!parts || !out) return fail(WQ_EINVAL, "NULL pointer");
+  if (G < 1) return fail(WQ_EINVAL, "G=%d", G);
+  return cuda_status(wq::launch_merge(parts, G, g->B * g->Hq, g->d, (__half *)out, S_(stream)), "merge");
+}
+
+wq_status wq_shard_slots(const int32_t *perm_l, const int32_t *seg_off_l, int32_t B, int32_t W, int32_t G,
+                         int32_t r, int32_t *perm_r, int32_t *seg_off_r, void *stream) {
+  if (!perm_l || !seg_off_l || !perm_r || !seg_off_r) return fail(WQ_EINVAL, "NULL pointer");
+  if (B < 1 || W < 1) return fail(WQ_ESHAPE, "B=%d W=%d", B, W);
+  if (G < 1 || r < 0 || r >= G) return fail(WQ_EINVAL, "rank %d of %d", r, G);
+  return cuda_status(wq::launch_shard_slots(perm_l, seg_off_l, B, W, G, r, perm_r, seg_off_r, S_(stream)),
+                     "shard");
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// wq_internal.h -- launchers shared between the kernels (*.cu) and the C ABI (abi.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace wq {
+
+constexpr int MAX_LAYERS = 64;
+
+struct AssignParams {
+  int L, B, W, n_widths, widths[4];
+  int pin, vote;
+  double budget;
+  double thr[MAX_LAYERS * 3];
+};
+
+cudaError_t launch_text_pool(const __half *txt, int64_t trs, int64_t tbs, int B, int N, int D,
+                             double *tbar, cudaStream_t st);
+cudaError_t launch_window_scores(const __half *vis, int64_t vrs, int64_t vbs, int B, int M, int N,
+                                 int D, int S, const double *tbar, double *scores, cudaStream_t st);
+
+cudaError_t launch_rank(const double *scores, int B, int W, int32_t *rank, cudaStream_t st);
+cudaError_t launch_assign(const double *scores, const AssignParams &p, uint8_t *bits, int32_t *perm,
+                          int32_t *seg_off, cudaStream_t st);
+
+cudaError_t launch_layer_layout(const int32_t *seg_off, int B, int H, int d, int S, int64_t *offs,
+                                cudaStream_t st);
+cudaError_t launch_shard_slots(const int32_t *perm, const int32_t *seg, int B, int W, int G, int r,
+                               int32_t *perm_r, int32_t *seg_r, cudaStream_t st);
+cudaError_t launch_quant(const __half *k, const __half *v, const int64_t strides[3], int vis_off,
+                         int B, int H, int d, int S, const int32_t *perm, int perm_stride,
+                         const int32_t *seg_off, const int64_t *offs, uint8_t *packed,
+                         cudaStream_t st);
+
+struct DecodeArgs {
+  const __half *q;
+  const uint8_t *packed;
+  const int64_t *offs;
+  const int32_t *seg_off;
+  const __half *k_rest, *v_rest;
+  int64_t rs_b, rs_h;
+  const int32_t *rest_len;
+  int R_max;
+  int B, H, Hq, grp, d, S;
+  float scale_log2;          // sm_scale * log2(e)
+  __half *out;
+  float *partial;
+  float *ws_part;            // [(G + B*H)][grp][d + 2]
+  int32_t *ws_cnt;           // [B*H]
+};
+size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms);
+cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st);
+cudaError_t launch_merge(const float *parts, int G, int BHq, int d, __half *out, cudaStream_t st);
+
+int device_sm_count();
+
+}  // namespace wq

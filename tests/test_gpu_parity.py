@@ -1,0 +1,312 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Integer outputs (ranks, bits, perms, segment offsets, packed
+bytes) must be bit-exact; scores within 1e-12 absolute (Q6); attention within
+2e-3 max row-wise relative error (north star, Q30)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2605_02262_b200 import configs, synth
+from paper_2605_02262_b200 import wq
+
+pytestmark = pytest.mark.gpu
+
+ATTN_TOL = 2e-3
+
+
+def rel_err(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    num = np.abs(got - ref).max(axis=-1)
+    den = np.maximum(np.abs(ref).max(axis=-1), 1e-6)
+    return float((num / den).max())
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    wq.load()
+
+
+def ogeom(orc, g):
+    return orc.geom(g.B, g.H, g.Hq, g.d, g.M, g.S, list(g.widths)[:g.n_widths])
+
+
+def run_layer(g, K, V, kr, vr, rest_len, perm, seg, q, sm, partial=False):
+    """GPU path for one layer: layout -> quantize -> decode."""
+    dev = K.device
+    offs = wq.wq_layer_layout(g, seg)
+    total = int(offs[-1].item())
+    packed = torch.zeros(max(total, 16), dtype=torch.uint8, device=dev)
+    wq.wq_reorder_quantize_pack(K, V, 0, g, perm, seg, offs, packed)
+    out = torch.empty((g.B, g.Hq, g.d), dtype=torch.float16, device=dev)
+    part = torch.empty((g.B, g.Hq, g.d + 2), dtype=torch.float32, device=dev) if partial else None
+    wq.wq_decode_attention(q, packed, offs, seg, g, kr, vr, rest_len, sm, out=out, partial=part)
+    torch.cuda.synchronize()
+    return offs, packed, out, part
+
+
+def small_case(seed, B=2, H=2, Hq=14, d=64, S=16, W=9, tail=5, R=21, widths=(2, 4, 8, 16), s=0.5):
+    torch.manual_seed(seed)
+    M = W * S + tail
+    K, V = synth.kv_layer(B, H, M, d, S, seed, 0, "cuda")
+    kr, vr = synth.rest_layer(B, H, R, d, seed, 0, "cuda")
+    rest_len = torch.tensor([R - 3 * b for b in range(B)], dtype=torch.int32, device="cuda")
+    q = synth.queries(B, Hq, H, d, seed, 0, device="cuda")
+    vis, txt = synth.embeddings(B, M, 8, 64, S, seed, "cuda")
+    g = wq.geom(B, H, Hq, d, M, S, widths)
+    return dict(g=g, K=K, V=V, kr=kr, vr=vr, rest_len=rest_len, q=q, vis=vis, txt=txt, s=s)
+
+
+# ---------------------------------------------------------------------------------------
+def test_scores_parity(orc):
+    for (B, M, N, D, S) in [(2, 16 * 9 + 5, 8, 64, 16), (1, 1568, 32, 896, 64), (3, 700, 5, 3584, 32)]:
+        vis, txt = synth.embeddings(B, M, N, D, S, 123 + D, "cuda")
+        sc = wq.wq_window_scores(vis, txt, S)
+        torch.cuda.synchronize()
+        ref = orc.window_scores(vis.cpu().numpy(), txt.cpu().numpy(), S)
+        assert np.max(np.abs(sc.cpu().numpy() - ref)) <= 1e-12
+
+
+def _assign_both(orc, scores_gpu, thr, g, budget=0.0, pin=1, vote=0):
+    L = thr.shape[0]
+    opts = wq.AssignOpts(budget, pin, vote)
+    bits, rank, perm, seg = wq.wq_assign_bits(scores_gpu, thr, L, g, opts)
+    torch.cuda.synchronize()
+    ob, orank, operm, oseg = orc.assign_bits(scores_gpu.cpu().numpy(), thr, ogeom(orc, g), budget, pin, vote)
+    return (bits.cpu().numpy(), rank.cpu().numpy(), perm.cpu().numpy(), seg.cpu().numpy()), (ob, orank, operm, oseg)
+
+
+@pytest.mark.parametrize("widths,budget,pin,vote", [
+    ((2, 4, 16), 0.0, 1, 0), ((2, 4, 8, 16), 0.0, 1, 0), ((2, 4, 8), 0.0, 1, 0),
+    ((2, 4, 8, 16), 4.0, 1, 0), ((2, 4, 8, 16), 3.0, 0, 0), ((2, 4, 16), 0.0, 1, 1),
+    ((2, 4, 8, 16), 4.5, 1, 1), ((4, 8), 0.0, 1, 0), ((16,), 0.0, 1, 0)])
+def test_assign_parity(orc, widths, budget, pin, vote):
+    B, W, S = 5, 197, 16
+    rng = np.random.default_rng(len(widths) * 7 + int(budget))
+    scores = rng.uniform(0.0, 0.95, (B, W))
+    scores[1, 10:20] = scores[1, 30]                       # exact ties -> index order (Q7)
+    scores[2, :] = np.round(scores[2, :], 1)               # many ties and threshold hits
+    sc = torch.tensor(scores, dtype=torch.float64, device="cuda")
+    s_prof = [0.5, 0.3, 0.9, 0.05, 0.5]
+    thr = orc.thresholds(s_prof, 2.0, len(widths))
+    g = wq.geom(B, 2, 14, 64, W * S + 3, S, widths)
+    gpu, ref = _assign_both(orc, sc, thr, g, budget, pin, vote)
+    for a, b, name in zip(gpu, ref, ("bits", "rank", "perm", "seg_off")):
+        assert np.array_equal(a, b), name
+
+
+def test_assign_parity_large_W(orc):
+    """C5 geometry: W = 1568 windows, 28 layers, budget on."""
+    cfg = configs.CONFIGS["C5"]
+    vis, txt = synth.embeddings(2, cfg.M, 32, 256, cfg.S, cfg.seed, "cuda")
+    sc = wq.wq_window_scores(vis, txt, cfg.S)
+    thr = orc.thresholds([0.5] * 27 + [0.1], 2.0, 4)
+    g = wq.geom(2, 4, 28, 128, cfg.M, cfg.S, cfg.widths)
+    for budget in (0.0, 3.5):
+        gpu, ref = _assign_both(orc, sc, thr, g, budget)
+        for a, b in zip(gpu, ref):
+            assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("d,S,W,tail", [(64, 16, 9, 5), (64, 32, 5, 0), (128, 32, 6, 7), (128, 64, 3, 0),
+                                        (128, 128, 2, 3), (64, 128, 2, 0), (128, 16, 11, 0)])
+def test_quantize_pack_bit_exact(orc, d, S, W, tail):
+    c = small_case(10 + d + S, d=d, S=S, W=W, tail=tail, Hq=4 if d == 64 else 28, H=2 if d == 64 else 4)
+    g = c["g"]
+    sc = wq.wq_window_scores(c["vis"], c["txt"], S)
+    thr = orc.thresholds([0.4], 2.0, 4)
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
+    offs, packed, _, _ = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm[0], seg[0], c["q"],
+                                   1 / math.sqrt(d))
+    opk, ooffs = orc.reorder_quantize_pack(c["K"].cpu().numpy(), c["V"].cpu().numpy(), 0, ogeom(orc, g),
+                                           perm[0].cpu().numpy(), seg[0].cpu().numpy())
+    assert np.array_equal(offs.cpu().numpy(), ooffs)
+    n = int(ooffs[-1])
+    assert np.array_equal(packed.cpu().numpy()[:n], opk[:n])
+
+
+def test_quantize_all_classes_present(orc):
+    """Force every width class (and a permuted, non-identity slot order)."""
+    c = small_case(77, d=128, S=32, W=8, tail=0, Hq=28, H=4, B=1)
+    g = c["g"]
+    bits = [16, 2, 8, 4, 2, 16, 8, 4]
+    order = [i for k in (2, 4, 8, 16) for i, b in enumerate(bits) if b == k]
+    perm = torch.tensor([order], dtype=torch.int32, device="cuda")
+    seg = torch.tensor([[0, 2, 4, 6, 8]], dtype=torch.int32, device="cuda")
+    offs, packed, out, _ = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm, seg, c["q"],
+                                     1 / math.sqrt(128))
+    opk, ooffs = orc.reorder_quantize_pack(c["K"].cpu().numpy(), c["V"].cpu().numpy(), 0, ogeom(orc, g),
+                                           perm.cpu().numpy(), seg.cpu().numpy())
+    assert np.array_equal(packed.cpu().numpy()[:int(ooffs[-1])], opk[:int(ooffs[-1])])
+
+
+# ---------------------------------------------------------------------------------------
+def _decode_ref(orc, c, g, offs, packed, perm, seg, sm):
+    return orc.decode_attention(c["q"].cpu().numpy(), packed.cpu().numpy(), offs.cpu().numpy(),
+                                seg.cpu().numpy(), perm.cpu().numpy(), ogeom(orc, g), c["kr"].cpu().numpy(),
+                                c["vr"].cpu().numpy(), c["rest_len"].cpu().numpy(), sm, want_partial=True)
+
+
+@pytest.mark.parametrize("d,S,W,tail,B,H,Hq", [(64, 16, 9, 5, 2, 2, 14), (64, 32, 17, 0, 3, 2, 14),
+                                               (128, 32, 12, 7, 2, 4, 28), (128, 64, 5, 0, 1, 4, 28),
+                                               (128, 128, 3, 9, 2, 2, 8), (64, 64, 6, 1, 2, 1, 5),
+                                               (128, 16, 30, 0, 4, 4, 28)])
+def test_decode_parity(orc, d, S, W, tail, B, H, Hq):
+    c = small_case(200 + d + S + W, d=d, S=S, W=W, tail=tail, B=B, H=H, Hq=Hq)
+    g = c["g"]
+    sc = wq.wq_window_scores(c["vis"], c["txt"], S)
+    thr = orc.thresholds([0.45], 2.0, 4)
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
+    sm = 1 / math.sqrt(d)
+    offs, packed, out, part = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm[0], seg[0],
+                                        c["q"], sm, partial=True)
+    ref, rpart = _decode_ref(orc, c, g, offs, packed, perm[0], seg[0], sm)
+    assert rel_err(out.float().cpu().numpy(), ref) <= ATTN_TOL
+    # partial (m, l, o): compare normalized output and the log-sum-exp
+    p = part.double().cpu().numpy()
+    assert rel_err(p[..., 2:] / p[..., 1:2], ref) <= ATTN_TOL
+    lse = p[..., 0] + np.log(p[..., 1])
+    rlse = rpart[..., 0] + np.log(rpart[..., 1])
+    assert np.max(np.abs(lse - rlse)) < 1e-3
+
+
+def test_decode_all16_equals_bruteforce(orc):
+    """North star: all windows at 16 bits -> fp64 brute-force attention."""
+    c = small_case(31, d=128, S=32, W=10, tail=3, B=2, H=4, Hq=28, widths=(16,))
+    g = c["g"]
+    W = 10
+    perm = torch.arange(W, dtype=torch.int32, device="cuda").repeat(2, 1)
+    seg = torch.tensor([[0, 0, 0, 0, W]] * 2, dtype=torch.int32, device="cuda")
+    sm = 1 / math.sqrt(128)
+    _, _, out, _ = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm, seg, c["q"], sm)
+    win = np.tile(np.arange(W, dtype=np.int32), (2, 1))
+    ref = orc.bruteforce_attention(c["q"].cpu().numpy(), c["K"].cpu().numpy(), c["V"].cpu().numpy(), 0,
+                                   ogeom(orc, g), win, np.array([W, W], np.int32), c["kr"].cpu().numpy(),
+                                   c["vr"].cpu().numpy(), c["rest_len"].cpu().numpy(), sm)
+    assert rel_err(out.float().cpu().numpy(), ref) <= ATTN_TOL
+
+
+def test_decode_edge_cases(orc):
+    """Empty rest, rest-only (no windows), one token, ragged rest tiles."""
+    c = small_case(41, d=64, S=16, W=4, tail=0, B=3, H=2, Hq=14)
+    g = c["g"]
+    sm = 0.125
+    sc = wq.wq_window_scores(c["vis"], c["txt"], 16)
+    thr = orc.thresholds([0.5], 2.0, 4)
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
+    for rl in ([0, 0, 0], [1, 17, 33], [16, 15, 21]):
+        c["rest_len"] = torch.tensor(rl, dtype=torch.int32, device="cuda")
+        offs, packed, out, part = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm[0], seg[0],
+                                            c["q"], sm, partial=True)
+        ref, _ = _decode_ref(orc, c, g, offs, packed, perm[0], seg[0], sm)
+        assert rel_err(out.float().cpu().numpy(), ref) <= ATTN_TOL
+    # no windows at all: only rest tokens (request 1 has a single token)
+    seg0 = torch.zeros((3, 5), dtype=torch.int32, device="cuda")
+    c["rest_len"] = torch.tensor([5, 1, 21], dtype=torch.int32, device="cuda")
+    offs, packed, out, _ = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm[0], seg0, c["q"], sm)
+    ref, _ = _decode_ref(orc, c, g, offs, packed, perm[0], seg0, sm)
+    assert rel_err(out.float().cpu().numpy(), ref) <= ATTN_TOL
+    # single rest token -> output equals v_0 exactly up to fp16 rounding
+    assert np.allclose(out[1].float().cpu().numpy(), c["vr"][1, :, 0].float().cpu().numpy().repeat(7, 0),
+                       atol=2e-3, rtol=2e-3)
+
+
+def test_merge_partials_parity(orc):
+    """Sequence split (§8(e)): two shards' partials merged on the GPU = unsplit."""
+    c = small_case(55, d=128, S=32, W=14, tail=0, B=2, H=4, Hq=28)
+    g = c["g"]
+    sm = 1 / math.sqrt(128)
+    sc = wq.wq_window_scores(c["vis"], c["txt"], 32)
+    thr = orc.thresholds([0.45], 2.0, 4)
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
+    _, _, full, _ = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm[0], seg[0], c["q"], sm)
+    parts = []
+    for r in range(2):
+        pl, sl = [], []
+        for b in range(2):
+            so = seg[0, b].cpu().numpy()
+            pb = perm[0, b].cpu().numpy()
+            slots, s5 = [], []
+            for k in range(4):
+                lo, hi = so[k], so[k + 1]
+                mid = lo + (hi - lo) // 2
+                s5.append(len(slots))
+                slots += list(pb[lo:mid] if r == 0 else pb[mid:hi])
+            s5.append(len(slots))
+            pl.append(slots + [0] * (14 - len(slots)))
+            sl.append(s5)
+        pr = torch.tensor(pl, dtype=torch.int32, device="cuda")
+        sr = torch.tensor(sl, dtype=torch.int32, device="cuda")
+        rl = c["rest_len"] if r == 0 else torch.zeros_like(c["rest_len"])
+        _, _, _, part = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], rl, pr, sr, c["q"], sm, partial=True)
+        parts.append(part)
+    merged = wq.wq_merge_partials(torch.stack(parts), g)
+    torch.cuda.synchronize()
+    ref = orc.merge(torch.stack(parts).double().cpu().numpy())
+    assert rel_err(merged.float().cpu().numpy(), ref) <= 1e-3
+    assert rel_err(merged.float().cpu().numpy(), full.float().cpu().numpy()) <= ATTN_TOL
+
+
+def test_abi_errors():
+    g = wq.geom(1, 2, 14, 96, 64, 16, (2, 4))
+    with pytest.raises(wq.WQError) as e:
+        wq.wq_decode_workspace(g)
+    assert e.value.status == wq.WQ_EUNSUPPORTED
+    g = wq.geom(1, 2, 14, 64, 64, 16, (4, 2))
+    sc = torch.zeros((1, 4), dtype=torch.float64, device="cuda")
+    with pytest.raises(wq.WQError):
+        wq.wq_assign_bits(sc, np.zeros((1, 1)), 1, g)
+    g = wq.geom(1, 2, 14, 64, 64, 16, (2, 4, 8, 16))
+    with pytest.raises(wq.WQError) as e:
+        wq.wq_assign_bits(sc, np.zeros((1, 3)), 1, g, wq.AssignOpts(2.0, 1, 0))
+    assert e.value.status == wq.WQ_EBUDGET
+
+
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5"])
+def test_config_layer_parity(orc, name):
+    """One layer of each config at FULL size, in the launch configuration bench.py
+    times: scores (sampled windows), assign (all), packed bytes (one request, all
+    heads) and attention (sampled (b, h) units through the oracle)."""
+    cfg = configs.CONFIGS[name]
+    m = cfg.model
+    B = cfg.B
+    layer = cfg.layers - 1
+    vis, txt = synth.embeddings(B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, "cuda")
+    sc = wq.wq_window_scores(vis, txt, cfg.S)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(cfg.idx)
+    vh, th = vis.cpu().numpy(), txt.cpu().numpy()
+    for _ in range(6):
+        b, w = int(rng.integers(B)), int(rng.integers(cfg.W))
+        assert abs(sc[b, w].item() - orc.window_score(vh[b], th[b], cfg.S, w)) <= 1e-12
+    thr = orc.thresholds(cfg.sensitivities(), cfg.alpha, len(cfg.widths))
+    g = wq.geom(B, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
+    gpu, ref = _assign_both(orc, sc, thr, g, cfg.budget)
+    for a, b_ in zip(gpu, ref):
+        assert np.array_equal(a, b_)
+    perm = torch.tensor(ref[2][layer], device="cuda")
+    seg = torch.tensor(ref[3][layer], device="cuda")
+    K, V, kr, vr, rest_len = synth.layer_tensors(cfg, layer, "cuda")
+    q = synth.queries(B, m.Hq, m.H, m.d, cfg.seed, layer, device="cuda")
+    sm = 1 / math.sqrt(m.d)
+    offs, packed, out, _ = run_layer(g, K, V, kr, vr, rest_len, perm, seg, q, sm)
+    # packed bytes of request 0 (all heads) bit-exact
+    g1 = orc.geom(1, m.H, m.Hq, m.d, cfg.M, cfg.S, list(cfg.widths))
+    opk, ooffs = orc.reorder_quantize_pack(K[:1].cpu().numpy(), V[:1].cpu().numpy(), 0, g1,
+                                           ref[2][layer][:1], ref[3][layer][:1])
+    n0 = int(ooffs[-1])
+    assert np.array_equal(packed[:n0].cpu().numpy(), opk[:n0])
+    # attention of sampled requests through the oracle (full cache of those requests)
+    bs = sorted(set([0, B - 1]))
+    for b in bs:
+        sub = dict(q=q[b:b + 1], kr=kr[b:b + 1], vr=vr[b:b + 1], rest_len=rest_len[b:b + 1])
+        gb = wq.geom(1, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
+        ob = offs[b * m.H:(b + 1) * m.H + 1] - offs[b * m.H]
+        pk = packed[int(offs[b * m.H].item()):int(offs[(b + 1) * m.H].item())]
+        r = _decode_ref(orc, sub, gb, ob, pk, perm[b:b + 1], seg[b:b + 1], sm)[0]
+        assert rel_err(out[b:b + 1].float().cpu().numpy(), r) <= ATTN_TOL
