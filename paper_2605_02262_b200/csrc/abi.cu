@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/wq.h"
@@ -214,12 +215,16 @@ wq_status wq_decode_attention(const void *q, const uint8_t *packed, const int64_
   a.rest_len = R_max > 0 ? rest_len : nullptr; a.R_max = R_max;
   a.B = g->B; a.H = g->H; a.Hq = g->Hq; a.grp = g->Hq / g->H; a.d = g->d; a.S = g->S;
   a.scale_log2 = sm_scale * 1.4426950408889634f;
+  { const char *dbg = getenv("WQ_DECODE_DEBUG"); a.debug = dbg ? atoi(dbg) : 0; }
   a.out = (__half *)out; a.partial = partial;
   const int grp = a.grp;
   size_t part = (size_t)(sms + g->B * g->H) * grp * (g->d + 2) * sizeof(float);
   part = (part + 255) / 256 * 256;
   a.ws_part = reinterpret_cast<float *>(workspace);
   a.ws_cnt = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(workspace) + part);
+  size_t cntb = ((size_t)g->B * g->H * sizeof(int32_t) + 255) / 256 * 256;
+  a.ws_ts = (a.debug & 8) ? reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(workspace) + part + cntb)
+                          : nullptr;
   return cuda_status(wq::launch_decode(a, sms, S_(stream)), "decode");
 }
 

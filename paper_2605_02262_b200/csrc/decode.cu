@@ -28,26 +28,29 @@
 
 namespace wq {
 
-constexpr int NCW = 8;                  // consumer warps
+constexpr int NCW = 15;                 // consumer warps (16 warps: 4 per SM sub-partition)
 constexpr int DT = (NCW + 1) * 32;      // threads per CTA
-constexpr int MAXIT = 48;               // items per stage
 constexpr int MAX_UNITS = 1024;         // B * H
 constexpr int64_t MIN_CTA_BYTES = 49152;
 constexpr float LAZY_TH = 8.0f;         // log2 headroom of the lazy softmax rescale
 constexpr int KIND_REST = 4;
 
-struct StageDesc {
-  int unit, nitems, flags;              // flags: 1 = last stage of unit, 2 = last of CTA
-  uint8_t kind[MAXIT];                  // 0..3 = width class, 4 = rest tile
-  uint8_t ntok[MAXIT];                  // valid tokens of a rest tile
-  uint16_t off[MAXIT];                  // byte offset in the stage
-};
-
+// Geometry of one unit (request b, kv head h).  Work is partitioned across CTAs in
+// COST space, not bytes: every item costs its bytes plus a per-item compute term
+// (a window's dequant + MMA work is nearly independent of its width), so CTAs that
+// get many narrow windows get fewer of them.  kappa ~ bytes the HBM delivers to
+// one SM while it computes one window (0.75 B per element of a quantized window).
 struct UnitGeo {
   int b, h, nslots, rl, ntiles;
   int so[5];
   int64_t cs[5];                        // byte start of each class segment; cs[4] = image bytes
+  int64_t cc[5];                        // cost start of each class segment; cc[4] = windows' cost
 };
+
+WQ_DEV int64_t item_cost(int k, int d, int S) {   // k = 0..3 class, 4 = rest tile
+  if (k == 4) return 64LL * d + 6LL * d;
+  return record_bytes(class_bits(k), d, S) + (k == 3 ? 3LL * S * d / 8 : 3LL * S * d / 4);
+}
 
 WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
   g.b = u / a.H;
@@ -55,28 +58,58 @@ WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
   const int32_t *so = a.seg_off + 5 * g.b;
   for (int k = 0; k < 5; k++) g.so[k] = so[k];
   g.cs[0] = 0;
-  for (int k = 0; k < 4; k++)
-    g.cs[k + 1] = g.cs[k] + (int64_t)(g.so[k + 1] - g.so[k]) * record_bytes(class_bits(k), a.d, a.S);
+  g.cc[0] = 0;
+  for (int k = 0; k < 4; k++) {
+    const int64_t n = g.so[k + 1] - g.so[k];
+    g.cs[k + 1] = g.cs[k] + n * record_bytes(class_bits(k), a.d, a.S);
+    g.cc[k + 1] = g.cc[k] + n * item_cost(k, a.d, a.S);
+  }
   g.nslots = g.so[4];
   g.rl = a.rest_len ? a.rest_len[g.b] : 0;
   g.ntiles = (g.rl + 15) / 16;
 }
-WQ_DEV int64_t unit_bytes(const DecodeArgs &a, const UnitGeo &g) { return g.cs[4] + (int64_t)g.rl * 4 * a.d; }
+WQ_DEV int64_t unit_cost(const DecodeArgs &a, const UnitGeo &g) {
+  return g.cc[4] + (int64_t)g.ntiles * item_cost(4, a.d, a.S);
+}
 
-// first item whose start offset (relative to the unit) is >= x
+// first item whose start (in cost units, relative to the unit) is >= x
 WQ_DEV int first_item(const DecodeArgs &a, const UnitGeo &g, int64_t x) {
   if (x <= 0) return 0;
   for (int k = 0; k < 4; k++) {
-    if (x <= g.cs[k]) return g.so[k];
-    if (x < g.cs[k + 1]) {
-      int64_t rb = record_bytes(class_bits(k), a.d, a.S);
-      return g.so[k] + (int)((x - g.cs[k] + rb - 1) / rb);
+    if (x <= g.cc[k]) return g.so[k];
+    if (x < g.cc[k + 1]) {
+      const int64_t c = item_cost(k, a.d, a.S);
+      return g.so[k] + (int)((x - g.cc[k] + c - 1) / c);
     }
   }
-  if (x <= g.cs[4]) return g.nslots;
-  int64_t tb = 64LL * a.d;
-  int64_t t = (x - g.cs[4] + tb - 1) / tb;
+  if (x <= g.cc[4]) return g.nslots;
+  const int64_t tc = item_cost(4, a.d, a.S);
+  const int64_t t = (x - g.cc[4] + tc - 1) / tc;
   return g.nslots + (int)(t < g.ntiles ? t : g.ntiles);
+}
+
+// Stage plan of one unit's item range [i0, i1): five "pieces" (the width-class
+// segments 2|4|8|16 and the FP16 rest tiles), each cut into stages of cap
+// equal-size items.  Producer and consumers evaluate the same arithmetic, so no
+// per-item descriptors are exchanged.
+struct UnitPlan {
+  int lo[5], hi[5], cap[5], nst[5];
+  int sz[5];
+};
+template <int STAGE>
+WQ_DEV void plan_unit(const DecodeArgs &a, const UnitGeo &g, int i0, int i1, UnitPlan &pl) {
+  for (int p = 0; p < 5; p++) {
+    const int a0 = p < 4 ? g.so[p] : g.nslots;
+    const int a1 = p < 4 ? g.so[p + 1] : g.nslots + g.ntiles;
+    const int lo = i0 > a0 ? i0 : a0;
+    const int hi = i1 < a1 ? i1 : a1;
+    const int sz = p < 4 ? (int)record_bytes(class_bits(p), a.d, a.S) : 64 * a.d;
+    pl.lo[p] = lo;
+    pl.hi[p] = hi > lo ? hi : lo;
+    pl.sz[p] = sz;
+    pl.cap[p] = STAGE / sz;
+    pl.nst[p] = (pl.hi[p] - pl.lo[p] + pl.cap[p] - 1) / pl.cap[p];
+  }
 }
 
 WQ_DEV int64_t cta_lo(int c, int G, int64_t T) { return (int64_t)c * T / G; }
@@ -96,97 +129,43 @@ struct WarpState {
 // -------------------------------------------------------------------------------------
 // consumer: one window (BITS in {2,4,8,16}) or one rest tile
 // -------------------------------------------------------------------------------------
-// K-side scores for NT token tiles of one quantized / fp16-fragment window.
-template <int D, int NT, int BITS>
-WQ_DEV void window_scores(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float (&sc)[NT][4],
-                          int lane) {
-  constexpr int KT = D / 16;
-  constexpr int WPL = D * BITS / 64;          // words per lane per tile
-  constexpr int PPW = 16 / BITS;              // pairs per word
-  float bias[4] = {0.f, 0.f, 0.f, 0.f};
-  uint32_t qh[KT][2], ql[KT][2];
-  if constexpr (BITS < 16) {
-    const uint8_t *kp = rec + 2 * (NT * 16 * D * BITS / 8);
-    const int q = lane & 3;
-#pragma unroll
-    for (int kt = 0; kt < KT; kt++) {
-      uint4 pr = lds128(kp + (q * KT + kt) * 16);   // {s01, s89, mn01, mn89}
-      uint32_t am[4] = {pr.z, pr.z, pr.w, pr.w};
-      mma16816(bias, am, qf[kt][0], qf[kt][1], bias);
-      qh[kt][0] = hmul2u(qf[kt][0], pr.x);
-      ql[kt][0] = hfma2u(qf[kt][0], pr.x, hneg2u(qh[kt][0]));
-      qh[kt][1] = hmul2u(qf[kt][1], pr.y);
-      ql[kt][1] = hfma2u(qf[kt][1], pr.y, hneg2u(qh[kt][1]));
+// Exact fp16 value pair of pair-slot P (compile-time after unrolling) of a lane chunk.
+template <int BITS>
+WQ_DEV uint32_t deq_pair(const uint32_t *wd, int P) {
+  constexpr int PPW = 16 / BITS;
+  const uint32_t w = wd[P / PPW];
+  if constexpr (BITS == 16) {
+    return w;
+  } else if constexpr (BITS == 8) {
+    return (P % 2) == 0 ? dq_pair<8, 0>(w, 0) : dq_pair<8, 1>(w, 0);
+  } else if constexpr (BITS == 4) {
+    const uint32_t w8 = w >> 8;
+    switch (P % 4) {
+      case 0: return dq_pair<4, 0>(w, w8);
+      case 1: return dq_pair<4, 1>(w, w8);
+      case 2: return dq_pair<4, 2>(w, w8);
+      default: return dq_pair<4, 3>(w, w8);
     }
-  }
-#pragma unroll
-  for (int nt = 0; nt < NT; nt++) {
-    const uint8_t *ch = rec + nt * (2 * D * BITS) + lane * (D * BITS / 16);
-    uint32_t wd[WPL];
-    if constexpr (WPL >= 4) {
-#pragma unroll
-      for (int i = 0; i < WPL / 4; i++) {
-        uint4 v = lds128(ch + 16 * i);
-        wd[4 * i] = v.x; wd[4 * i + 1] = v.y; wd[4 * i + 2] = v.z; wd[4 * i + 3] = v.w;
-      }
-    } else {
-      uint2 v = lds64(ch);
-      wd[0] = v.x; wd[1] = v.y;
+  } else {
+    const uint32_t w8 = w >> 8;
+    switch (P % 8) {
+      case 0: return dq_pair<2, 0>(w, w8);
+      case 1: return dq_pair<2, 1>(w, w8);
+      case 2: return dq_pair<2, 2>(w, w8);
+      case 3: return dq_pair<2, 3>(w, w8);
+      case 4: return dq_pair<2, 4>(w, w8);
+      case 5: return dq_pair<2, 5>(w, w8);
+      case 6: return dq_pair<2, 6>(w, w8);
+      default: return dq_pair<2, 7>(w, w8);
     }
-    float acc[4] = {bias[0], bias[1], bias[2], bias[3]};
-#pragma unroll
-    for (int kt = 0; kt < KT; kt++) {
-      uint32_t a[4];
-#pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const int P = 4 * kt + r;
-        const uint32_t w = wd[P / PPW];
-        if constexpr (BITS == 16) a[r] = w;
-        else if constexpr (BITS == 2) {
-          const uint32_t w8 = w >> 8;
-          switch (P % PPW) {
-            case 0: a[r] = dq_pair<2, 0>(w, w8); break;
-            case 1: a[r] = dq_pair<2, 1>(w, w8); break;
-            case 2: a[r] = dq_pair<2, 2>(w, w8); break;
-            case 3: a[r] = dq_pair<2, 3>(w, w8); break;
-            case 4: a[r] = dq_pair<2, 4>(w, w8); break;
-            case 5: a[r] = dq_pair<2, 5>(w, w8); break;
-            case 6: a[r] = dq_pair<2, 6>(w, w8); break;
-            default: a[r] = dq_pair<2, 7>(w, w8); break;
-          }
-        } else if constexpr (BITS == 4) {
-          const uint32_t w8 = w >> 8;
-          switch (P % PPW) {
-            case 0: a[r] = dq_pair<4, 0>(w, w8); break;
-            case 1: a[r] = dq_pair<4, 1>(w, w8); break;
-            case 2: a[r] = dq_pair<4, 2>(w, w8); break;
-            default: a[r] = dq_pair<4, 3>(w, w8); break;
-          }
-        } else {
-          a[r] = (P % PPW) == 0 ? dq_pair<8, 0>(w, 0) : dq_pair<8, 1>(w, 0);
-        }
-      }
-      if constexpr (BITS < 16) {
-        mma16816(acc, a, qh[kt][0], qh[kt][1], acc);
-        mma16816(acc, a, ql[kt][0], ql[kt][1], acc);
-      } else {
-        mma16816(acc, a, qf[kt][0], qf[kt][1], acc);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; i++) sc[nt][i] = acc[i];
   }
 }
 
-// V side for tile nt of a window: o[mt] += Vcode^T(16 ch x 16 tok) * P'(16 tok x 8 heads)
+// Load a lane's chunk of one code tile (D*BITS/16 bytes) into words.
 template <int D, int BITS>
-WQ_DEV void window_pv(const uint8_t *vtile, uint32_t pb0, uint32_t pb1, float (&o)[D / 16][4],
-                      int lane) {
-  constexpr int KT = D / 16;
+WQ_DEV void load_chunk(uint32_t (&wd)[D * BITS / 64], const uint8_t *tile, int lane) {
   constexpr int WPL = D * BITS / 64;
-  constexpr int PPW = 16 / BITS;
-  const uint8_t *ch = vtile + lane * (D * BITS / 16);
-  uint32_t wd[WPL];
+  const uint8_t *ch = tile + lane * (D * BITS / 16);
   if constexpr (WPL >= 4) {
 #pragma unroll
     for (int i = 0; i < WPL / 4; i++) {
@@ -197,38 +176,17 @@ WQ_DEV void window_pv(const uint8_t *vtile, uint32_t pb0, uint32_t pb1, float (&
     uint2 v = lds64(ch);
     wd[0] = v.x; wd[1] = v.y;
   }
+}
+
+// V side of one tile: o[mt] += Vcode^T(16 ch x 16 tok) * P'(16 tok x 8 heads)
+template <int D, int BITS>
+WQ_DEV void tile_pv(const uint32_t (&wd)[D * BITS / 64], uint32_t pb0, uint32_t pb1, float (&o)[D / 16][4]) {
+  constexpr int KT = D / 16;
 #pragma unroll
   for (int mt = 0; mt < KT; mt++) {
     uint32_t a[4];
 #pragma unroll
-    for (int r = 0; r < 4; r++) {
-      const int P = 4 * mt + r;
-      const uint32_t w = wd[P / PPW];
-      if constexpr (BITS == 16) a[r] = w;
-      else if constexpr (BITS == 2) {
-        const uint32_t w8 = w >> 8;
-        switch (P % PPW) {
-          case 0: a[r] = dq_pair<2, 0>(w, w8); break;
-          case 1: a[r] = dq_pair<2, 1>(w, w8); break;
-          case 2: a[r] = dq_pair<2, 2>(w, w8); break;
-          case 3: a[r] = dq_pair<2, 3>(w, w8); break;
-          case 4: a[r] = dq_pair<2, 4>(w, w8); break;
-          case 5: a[r] = dq_pair<2, 5>(w, w8); break;
-          case 6: a[r] = dq_pair<2, 6>(w, w8); break;
-          default: a[r] = dq_pair<2, 7>(w, w8); break;
-        }
-      } else if constexpr (BITS == 4) {
-        const uint32_t w8 = w >> 8;
-        switch (P % PPW) {
-          case 0: a[r] = dq_pair<4, 0>(w, w8); break;
-          case 1: a[r] = dq_pair<4, 1>(w, w8); break;
-          case 2: a[r] = dq_pair<4, 2>(w, w8); break;
-          default: a[r] = dq_pair<4, 3>(w, w8); break;
-        }
-      } else {
-        a[r] = (P % PPW) == 0 ? dq_pair<8, 0>(w, 0) : dq_pair<8, 1>(w, 0);
-      }
-    }
+    for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS>(wd, 4 * mt + r);
     mma16816(o[mt], a, pb0, pb1, o[mt]);
   }
 }
@@ -264,13 +222,14 @@ WQ_DEV void softmax_tiles(float (&s)[NT][4], WarpState &st, float (&o)[KT][4],
       o[mt][0] *= a0; o[mt][1] *= a1; o[mt][2] *= a0; o[mt][3] *= a1;
     }
   }
-  const float m0 = st.m[0], m1 = st.m[1];
+  const float m0 = st.m[0] == -INFINITY ? 0.f : st.m[0];
+  const float m1 = st.m[1] == -INFINITY ? 0.f : st.m[1];
 #pragma unroll
   for (int nt = 0; nt < NT; nt++) {
-    float p0 = m0 == -INFINITY ? 0.f : exp2f(s[nt][0] - m0);
-    float p1 = m1 == -INFINITY ? 0.f : exp2f(s[nt][1] - m1);
-    float p2 = m0 == -INFINITY ? 0.f : exp2f(s[nt][2] - m0);
-    float p3 = m1 == -INFINITY ? 0.f : exp2f(s[nt][3] - m1);
+    float p0 = exp2f(s[nt][0] - m0);
+    float p1 = exp2f(s[nt][1] - m1);
+    float p2 = exp2f(s[nt][2] - m0);
+    float p3 = exp2f(s[nt][3] - m1);
     st.l[0] += p0 + p2;
     st.l[1] += p1 + p3;
     if (has_vparams) {
@@ -285,42 +244,93 @@ WQ_DEV void softmax_tiles(float (&s)[NT][4], WarpState &st, float (&o)[KT][4],
   __syncwarp();
 }
 
+// One window, processed in chunks of CH 16-token tiles.  Per k-tile the channel
+// scales/zero points are read once, q' = q*s is formed as an fp16 hi+lo pair
+// (HMUL2 + exact-residual HFMA2) and the bias q.mn accumulates on the tensor core;
+// each tile keeps independent hi/lo accumulators (short dependency chains).
 template <int D, int S, int BITS>
 WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float scale2,
                       WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane) {
-  constexpr int NT = S / 16;
+  constexpr int NTT = S / 16;
+  constexpr int CH = (BITS == 16 || NTT < 2) ? 1 : 2;
   constexpr int KT = D / 16;
-  float sc[NT][4];
-  window_scores<D, NT, BITS>(rec, qf, sc, lane);
-#pragma unroll
-  for (int nt = 0; nt < NT; nt++)
-#pragma unroll
-    for (int i = 0; i < 4; i++) sc[nt][i] *= scale2;
-  float vs[NT][2], vm[NT][2];
-  const int g = lane >> 2;
-  if constexpr (BITS < 16) {
-    const uint8_t *vp = rec + 2 * (S * D * BITS / 8) + 4 * D;
-#pragma unroll
-    for (int nt = 0; nt < NT; nt++) {
-      uint4 pr = lds128(vp + (4 * nt + (g >> 1)) * 16);
-      const __half *hp = reinterpret_cast<const __half *>(&pr);
-      const int e = g & 1;
-      vs[nt][0] = __half2float(hp[e]);
-      vs[nt][1] = __half2float(hp[2 + e]);
-      vm[nt][0] = __half2float(hp[4 + e]);
-      vm[nt][1] = __half2float(hp[6 + e]);
-    }
-  }
-  softmax_tiles<NT, KT>(sc, st, o, vs, vm, BITS < 16, scratch, lane);
+  constexpr int WPL = D * BITS / 64;
+  constexpr int TILE = 2 * D * BITS;          // bytes of one 16-token code tile
+  const uint8_t *kcodes = rec;
   const uint8_t *vcodes = rec + S * D * BITS / 8;
+  const uint8_t *kp = rec + 2 * (S * D * BITS / 8);
+  const int g = lane >> 2, q = lane & 3;
+  float b0[4] = {0.f, 0.f, 0.f, 0.f}, b1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int nt = 0; nt < NT; nt++) {
-    uint32_t pb[2];
-    // lanes 0-7: tokens 16nt+0..7, lanes 8-15: tokens 16nt+8..15 (rows of 16 B)
-    ldsm_x2_t(pb, scratch + (16 * nt + (lane & 15)) * 16);
-    window_pv<D, BITS>(vcodes + nt * (2 * D * BITS), pb[0], pb[1], o, lane);
+  for (int c0 = 0; c0 < NTT; c0 += CH) {
+    uint32_t wk[CH][WPL];
+#pragma unroll
+    for (int t = 0; t < CH; t++) load_chunk<D, BITS>(wk[t], kcodes + (c0 + t) * TILE, lane);
+    float ah[CH][4], al[CH][4];
+#pragma unroll
+    for (int t = 0; t < CH; t++)
+#pragma unroll
+      for (int i = 0; i < 4; i++) { ah[t][i] = 0.f; al[t][i] = 0.f; }
+#pragma unroll
+    for (int kt = 0; kt < KT; kt++) {
+      uint32_t h0, h1, l0, l1;
+      if constexpr (BITS < 16) {
+        const uint4 pr = lds128(kp + (q * KT + kt) * 16);   // {s01, s89, mn01, mn89}
+        if (c0 == 0) {
+          const uint32_t am[4] = {pr.z, pr.z, pr.w, pr.w};
+          if (kt & 1) mma16816(b1, am, qf[kt][0], qf[kt][1], b1);
+          else mma16816(b0, am, qf[kt][0], qf[kt][1], b0);
+        }
+        h0 = hmul2u(qf[kt][0], pr.x);
+        l0 = h2u(__hfma2(u2h(qf[kt][0]), u2h(pr.x), __hneg2(u2h(h0))));
+        h1 = hmul2u(qf[kt][1], pr.y);
+        l1 = h2u(__hfma2(u2h(qf[kt][1]), u2h(pr.y), __hneg2(u2h(h1))));
+      }
+#pragma unroll
+      for (int t = 0; t < CH; t++) {
+        uint32_t a[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS>(wk[t], 4 * kt + r);
+        if constexpr (BITS < 16) {
+          mma16816(ah[t], a, h0, h1, ah[t]);
+          mma16816(al[t], a, l0, l1, al[t]);
+        } else {
+          if (kt & 1) mma16816(al[t], a, qf[kt][0], qf[kt][1], al[t]);
+          else mma16816(ah[t], a, qf[kt][0], qf[kt][1], ah[t]);
+        }
+      }
+    }
+    float sc[CH][4];
+#pragma unroll
+    for (int t = 0; t < CH; t++)
+#pragma unroll
+      for (int i = 0; i < 4; i++) sc[t][i] = ((ah[t][i] + al[t][i]) + (b0[i] + b1[i])) * scale2;
+    float vs[CH][2], vm[CH][2];
+    if constexpr (BITS < 16) {
+      const uint8_t *vp = kp + 4 * D;
+#pragma unroll
+      for (int t = 0; t < CH; t++) {
+        // group (tile, g/2): {s(t0),s(t0+1)}, {s(t0+8),s(t0+9)}, {mn..}, {mn..}; token g = t0 + (g&1)
+        const uint4 pr = lds128(vp + (4 * (c0 + t) + (g >> 1)) * 16);
+        const uint32_t sh = (g & 1) * 16;
+        vs[t][0] = __half2float(__ushort_as_half((unsigned short)(pr.x >> sh)));
+        vs[t][1] = __half2float(__ushort_as_half((unsigned short)(pr.y >> sh)));
+        vm[t][0] = __half2float(__ushort_as_half((unsigned short)(pr.z >> sh)));
+        vm[t][1] = __half2float(__ushort_as_half((unsigned short)(pr.w >> sh)));
+      }
+    }
+    softmax_tiles<CH, KT>(sc, st, o, vs, vm, BITS < 16, scratch, lane);
+#pragma unroll
+    for (int t = 0; t < CH; t++) {
+      uint32_t pb[2];
+      // lanes 0-7: tokens 16t+0..7, lanes 8-15: tokens 16t+8..15 (rows of 16 B)
+      ldsm_x2_t(pb, scratch + (16 * t + (lane & 15)) * 16);
+      uint32_t wv[WPL];
+      load_chunk<D, BITS>(wv, vcodes + (c0 + t) * TILE, lane);
+      tile_pv<D, BITS>(wv, pb[0], pb[1], o);
+    }
+    __syncwarp();
   }
-  __syncwarp();
 }
 
 // FP16 rest tile: K rows [16][D] at base, V rows [16][D] at base + 32*D (natural layout)
@@ -365,20 +375,77 @@ WQ_DEV void do_rest(const uint8_t *base, int ntok, const uint32_t (&qf)[D / 16][
 // -------------------------------------------------------------------------------------
 template <int D, int S>
 struct DecodeSmem {
-  // a stage must hold the largest item (an FP16 window: 4*S*D bytes)
-  static constexpr int STAGE = (4 * S * D > 32768) ? 4 * S * D : 32768;
-  static constexpr int NST = (STAGE >= 65536) ? 2 : 4;
+  // a stage must hold the largest item (an FP16 window: 4*S*D bytes); small stages
+  // release shared memory item-group by item-group, a deep ring gives lookahead.
+  static constexpr int STAGE = (4 * S * D > 16384) ? 4 * S * D : 16384;
+  static constexpr int RING = 163840;
+  static constexpr int NST = (RING / STAGE) < 2 ? 2 : RING / STAGE;
   static constexpr int KT = D / 16;
-  static constexpr int SCRATCH = S * 16;                 // P' rows per warp
-  static constexpr int EP_WARP = 8 * D + 24;             // floats per warp in the epilogue
+  static constexpr int SCRATCH = 2 * 16 * 16;            // P' rows of one 2-tile chunk per warp
+  static constexpr int EPW = (KT * 4 + 6) * 32;          // floats of one warp state (fragment layout)
+  static constexpr int EP_SLOTS = 7;                     // merge tree 15 -> 8 -> 4 -> 2 -> 1
   static constexpr size_t ring = (size_t)NST * STAGE;
   static constexpr size_t scratch_off = ring;
   static constexpr size_t ep_off = scratch_off + (size_t)NCW * SCRATCH;
-  static constexpr size_t units_off = ep_off + (size_t)NCW * EP_WARP * 4;
-  static constexpr size_t desc_off = units_off + (size_t)(MAX_UNITS + 1) * 8;
-  static constexpr size_t bar_off = desc_off + NST * sizeof(StageDesc);
+  static constexpr size_t units_off = ep_off + (size_t)EP_SLOTS * EPW * 4;
+  static constexpr size_t cnt_off = units_off + (size_t)(MAX_UNITS + 1) * 8;
+  static constexpr size_t bar_off = (cnt_off + (size_t)(3 * NST + 4) * 4 + 15) / 16 * 16;
   static constexpr size_t total = bar_off + 2 * NST * 8 + 16;
 };
+
+WQ_DEV uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+WQ_DEV void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(64);
+  }
+}
+
+// merge warp state B (m, l, vb, o as seen by this lane) into A
+template <int KT>
+WQ_DEV void merge_state(WarpState &A, float (&oA)[KT][4], const float *Bst, int lane) {
+  // Bst layout: [KT*4 o][m0 m1 l0 l1 vb0 vb1] per lane, lane-major stride 32
+  const float bm0 = Bst[(KT * 4 + 0) * 32 + lane], bm1 = Bst[(KT * 4 + 1) * 32 + lane];
+  const float M0 = fmaxf(A.m[0], bm0), M1 = fmaxf(A.m[1], bm1);
+  const float fa0 = M0 == -INFINITY ? 0.f : exp2f(A.m[0] - M0), fb0 = M0 == -INFINITY ? 0.f : exp2f(bm0 - M0);
+  const float fa1 = M1 == -INFINITY ? 0.f : exp2f(A.m[1] - M1), fb1 = M1 == -INFINITY ? 0.f : exp2f(bm1 - M1);
+  A.m[0] = M0; A.m[1] = M1;
+  A.l[0] = fa0 * A.l[0] + fb0 * Bst[(KT * 4 + 2) * 32 + lane];
+  A.l[1] = fa1 * A.l[1] + fb1 * Bst[(KT * 4 + 3) * 32 + lane];
+  A.vb[0] = fa0 * A.vb[0] + fb0 * Bst[(KT * 4 + 4) * 32 + lane];
+  A.vb[1] = fa1 * A.vb[1] + fb1 * Bst[(KT * 4 + 5) * 32 + lane];
+#pragma unroll
+  for (int mt = 0; mt < KT; mt++) {
+    oA[mt][0] = fa0 * oA[mt][0] + fb0 * Bst[(mt * 4 + 0) * 32 + lane];
+    oA[mt][1] = fa1 * oA[mt][1] + fb1 * Bst[(mt * 4 + 1) * 32 + lane];
+    oA[mt][2] = fa0 * oA[mt][2] + fb0 * Bst[(mt * 4 + 2) * 32 + lane];
+    oA[mt][3] = fa1 * oA[mt][3] + fb1 * Bst[(mt * 4 + 3) * 32 + lane];
+  }
+}
+template <int KT>
+WQ_DEV void store_state(const WarpState &A, const float (&oA)[KT][4], float *Bst, int lane) {
+#pragma unroll
+  for (int mt = 0; mt < KT; mt++)
+#pragma unroll
+    for (int i = 0; i < 4; i++) Bst[(mt * 4 + i) * 32 + lane] = oA[mt][i];
+  Bst[(KT * 4 + 0) * 32 + lane] = A.m[0];
+  Bst[(KT * 4 + 1) * 32 + lane] = A.m[1];
+  Bst[(KT * 4 + 2) * 32 + lane] = A.l[0];
+  Bst[(KT * 4 + 3) * 32 + lane] = A.l[1];
+  Bst[(KT * 4 + 4) * 32 + lane] = A.vb[0];
+  Bst[(KT * 4 + 5) * 32 + lane] = A.vb[1];
+}
 
 template <int D, int S>
 __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
@@ -389,13 +456,18 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint8_t *ring = sm;
   int64_t *ustart = reinterpret_cast<int64_t *>(sm + SM::units_off);
-  StageDesc *desc = reinterpret_cast<StageDesc *>(sm + SM::desc_off);
+  int *stage_n = reinterpret_cast<int *>(sm + SM::cnt_off);      // items per stage fill
+  int *stage_done = stage_n + NST;                                // completed items per stage
+  int *stage_fill = stage_done + NST;                             // fill number a slot holds
+  int *claim = stage_fill + NST;                                  // [2] per-unit claim counters
+  int *s_flag = claim + 2;
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + SM::bar_off);
   uint64_t *empty = full + NST;
-  int *s_flag = reinterpret_cast<int *>(empty + NST);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int U = a.B * a.H;
+  uint64_t *ts = a.ws_ts ? a.ws_ts + (size_t)blockIdx.x * 72 : nullptr;
+  if (ts && tid == 0) ts[0] = gtime();
 
   // ---- unit byte prefix (warp 0) ----
   if (warp == 0) {
@@ -406,7 +478,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       if (u < U) {
         UnitGeo gg;
         unit_geo(a, u, gg);
-        v = unit_bytes(a, gg);
+        v = unit_cost(a, gg);
       }
       int64_t x = v;
       for (int o = 1; o < 32; o <<= 1) {
@@ -421,8 +493,12 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   if (tid == 0) {
     for (int s = 0; s < NST; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCW);
+      mbar_init(&empty[s], 1);
+      stage_n[s] = 0;
+      stage_done[s] = 0;
+      stage_fill[s] = -1;
     }
+    claim[0] = claim[1] = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -432,123 +508,94 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   const int c = blockIdx.x;
   if (c >= G) return;
   const int64_t lo = cta_lo(c, G, T), hi = cta_lo(c + 1, G, T);
+  if (ts && tid == 0) ts[1] = gtime();
 
   if (warp == NCW) {
     // =========================== producer ===========================
+    // One elected lane walks the stage plan: per stage, wait until the ring slot
+    // is free, arm the tx bytes and issue one bulk copy (a run of equal-size
+    // records) or two per FP16 rest tile.
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
-      int last_u = -1;
+      const bool nocopy = (a.debug & 2) != 0;
+      int sg = 0;                                  // global stage number of this CTA
       for (int u = 0; u < U; u++) {
         const int64_t us = ustart[u], ue = ustart[u + 1];
-        if (ue > us) {
-          if (ue <= lo || us >= hi) continue;
-        } else if (owner_of(us, G, T) != c) {
-          continue;
-        }
-        last_u = u;
-      }
-      for (int u = 0; u < U; u++) {
-        const int64_t us = ustart[u], ue = ustart[u + 1];
-        if (ue > us) {
-          if (ue <= lo || us >= hi) continue;
-        } else if (owner_of(us, G, T) != c) {
-          continue;
-        }
+        if (ue <= us || ue <= lo || us >= hi) continue;
         UnitGeo gg;
         unit_geo(a, u, gg);
         const int nitems = gg.nslots + gg.ntiles;
-        int i = first_item(a, gg, lo - us);
+        const int i0 = first_item(a, gg, lo - us);
         const int i1 = hi >= ue ? nitems : first_item(a, gg, hi - us);
+        UnitPlan pl;
+        plan_unit<STAGE>(a, gg, i0, i1, pl);
         const uint8_t *img = a.packed + a.offs[u];
         const __half *kr = a.k_rest + gg.b * a.rs_b + gg.h * a.rs_h;
         const __half *vr = a.v_rest + gg.b * a.rs_b + gg.h * a.rs_h;
-        do {
-          mbar_wait(&empty[stage], phase ^ 1);
-          StageDesc &dsc = desc[stage];
-          uint8_t *dst = ring + (size_t)stage * STAGE;
-          int n = 0;
-          uint32_t bytes = 0, tx = 0;
-          int k = 0;
-          while (i < i1 && n < MAXIT) {
-            uint32_t sz;
-            int kind, ntok = 0;
-            if (i < gg.nslots) {
-              while (i >= gg.so[k + 1]) k++;
-              kind = k;
-              sz = (uint32_t)record_bytes(class_bits(k), D, S);
+        for (int p = 0; p < 5; p++) {
+          for (int t = 0; t < pl.nst[p]; t++, sg++) {
+            const int slot = sg % NST;
+            const uint32_t fill = (uint32_t)(sg / NST);
+            const int f0 = pl.lo[p] + t * pl.cap[p];
+            const int f1 = min(pl.hi[p], f0 + pl.cap[p]);
+            mbar_wait(&empty[slot], (fill & 1) ^ 1);
+            stage_n[slot] = f1 - f0;
+            *reinterpret_cast<volatile int *>(stage_fill + slot) = (int)fill;
+            uint8_t *dst = ring + (size_t)slot * STAGE;
+            if (nocopy) {
+              mbar_arrive(&full[slot]);
+            } else if (p < 4) {
+              const uint32_t nb = (uint32_t)(f1 - f0) * pl.sz[p];
+              mbar_arrive_expect_tx(&full[slot], nb);
+              bulk_g2s_evict_first(dst, img + gg.cs[p] + (int64_t)(f0 - gg.so[p]) * pl.sz[p], nb, &full[slot], pol);
             } else {
-              kind = KIND_REST;
-              int t0 = 16 * (i - gg.nslots);
-              ntok = min(16, gg.rl - t0);
-              sz = 64u * D;
-            }
-            if (bytes + sz > (uint32_t)STAGE) break;
-            dsc.kind[n] = (uint8_t)kind;
-            dsc.ntok[n] = (uint8_t)ntok;
-            dsc.off[n] = (uint16_t)bytes;
-            tx += kind == KIND_REST ? (uint32_t)ntok * 4u * D : sz;
-            bytes += sz;
-            n++;
-            i++;
-          }
-          if (n == 0 && i < i1) __trap();   // an item larger than a stage (never: STAGE >= 4*S*D)
-          dsc.unit = u;
-          dsc.nitems = n;
-          dsc.flags = (i >= i1 ? 1 : 0) | ((i >= i1 && u == last_u) ? 2 : 0);
-          mbar_arrive_expect_tx(&full[stage], tx);
-          // issue the copies (contiguous runs of packed records merged into one copy)
-          int j = 0;
-          while (j < n) {
-            if (dsc.kind[j] != KIND_REST) {
-              int j2 = j + 1;
-              while (j2 < n && dsc.kind[j2] != KIND_REST) j2++;
-              int first = i - n + j;
-              int kk = 0;
-              while (first >= gg.so[kk + 1]) kk++;
-              int64_t src = gg.cs[kk] + (int64_t)(first - gg.so[kk]) * record_bytes(class_bits(kk), D, S);
-              uint32_t nb = (j2 < n ? dsc.off[j2] : bytes) - dsc.off[j];
-              bulk_g2s_evict_first(dst + dsc.off[j], img + src, nb, &full[stage], pol);
-              j = j2;
-            } else {
-              int t0 = 16 * (i - n + j - gg.nslots);
-              int nt = dsc.ntok[j];
-              bulk_g2s_evict_first(dst + dsc.off[j], kr + (int64_t)t0 * D, (uint32_t)nt * 2 * D,
-                                   &full[stage], pol);
-              bulk_g2s_evict_first(dst + dsc.off[j] + 32 * D, vr + (int64_t)t0 * D,
-                                   (uint32_t)nt * 2 * D, &full[stage], pol);
-              j++;
+              uint32_t tx = 0;
+              for (int i = f0; i < f1; i++) tx += (uint32_t)min(16, gg.rl - 16 * (i - gg.nslots)) * 4u * D;
+              mbar_arrive_expect_tx(&full[slot], tx);
+              for (int i = f0; i < f1; i++) {
+                const int t0 = 16 * (i - gg.nslots);
+                const uint32_t nb = (uint32_t)min(16, gg.rl - t0) * 2 * D;
+                uint8_t *d2 = dst + (size_t)(i - f0) * pl.sz[4];
+                bulk_g2s_evict_first(d2, kr + (int64_t)t0 * D, nb, &full[slot], pol);
+                bulk_g2s_evict_first(d2 + 32 * D, vr + (int64_t)t0 * D, nb, &full[slot], pol);
+              }
             }
           }
-          if (++stage == NST) { stage = 0; phase ^= 1; }
-        } while (i < i1);
+        }
       }
+      if (ts) ts[2] = gtime();
     }
     return;
   }
 
   // =========================== consumers ===========================
+  // Units in the same order as the producer; items of a unit are claimed
+  // dynamically (shared-memory ticket), so faster warps take more windows.
   uint8_t *scratch = sm + SM::scratch_off + warp * SM::SCRATCH;
   float *ep = reinterpret_cast<float *>(sm + SM::ep_off);
   const int g = lane >> 2, q = lane & 3;
-  int stage = 0;
-  uint32_t phase = 0;
-  int cur_u = -1;
   uint32_t qf[KT][2];
   float o[KT][4];
   WarpState st;
-  for (int mt = 0; mt < KT; mt++) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
-  st.m[0] = st.m[1] = -INFINITY;
-  st.l[0] = st.l[1] = st.vb[0] = st.vb[1] = 0.f;
-
-  for (;;) {
-    mbar_wait(&full[stage], phase);
-    const StageDesc &dsc = desc[stage];
-    const int u = dsc.unit, n = dsc.nitems, flags = dsc.flags;
-    if (u != cur_u) {
-      cur_u = u;
-      const int b = u / a.H, h = u % a.H;
+  int seq_base = 0, uidx = 0, sg_base = 0;
+  uint64_t acc_tag = 0, acc_full = 0, acc_comp = 0, t_ep = 0;
+  for (int u = 0; u < U; u++) {
+    const int64_t us = ustart[u], ue = ustart[u + 1];
+    const bool mine = (ue > us) ? !(ue <= lo || us >= hi) : owner_of(us, G, T) == c;
+    if (!mine) continue;
+    int n_u = 0;
+    UnitGeo gg;
+    UnitPlan pl;
+    if (ue > us) {
+      unit_geo(a, u, gg);
+      const int nitems = gg.nslots + gg.ntiles;
+      const int i0 = first_item(a, gg, lo - us);
+      const int i1 = hi >= ue ? nitems : first_item(a, gg, hi - us);
+      n_u = i1 - i0;
+      plan_unit<STAGE>(a, gg, i0, i1, pl);
+    }
+    const int b = u / a.H, h = u % a.H;
+    {
       const __half *qrow = a.q + ((int64_t)b * a.Hq + h * a.grp + g) * D;
 #pragma unroll
       for (int kt = 0; kt < KT; kt++) {
@@ -556,91 +603,161 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         qf[kt][1] = g < a.grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q + 8) : 0u;
       }
     }
-    const uint8_t *sbase = ring + (size_t)stage * STAGE;
-    for (int it = warp; it < n; it += NCW) {
-      const uint8_t *rec = sbase + dsc.off[it];
-      switch (dsc.kind[it]) {
+#pragma unroll
+    for (int mt = 0; mt < KT; mt++) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+    st.m[0] = st.m[1] = -INFINITY;
+    st.l[0] = st.l[1] = st.vb[0] = st.vb[1] = 0.f;
+    int *cl_ctr = claim + (uidx & 1);
+    for (;;) {
+      uint64_t t_a = ts ? gtime() : 0;
+      int j = 0;
+      if (lane == 0) j = atomicAdd(cl_ctr, 1);
+      j = __shfl_sync(0xffffffffu, j, 0);
+      if (j >= n_u) break;
+      // locate item j of the unit in the stage plan
+      int p = 0, sbase = sg_base, idx = 0;
+      {
+        int rem = j;
+#pragma unroll
+        for (int pp = 0; pp < 5; pp++) {
+          const int len = pl.hi[pp] - pl.lo[pp];
+          if (p == pp && rem >= len) { rem -= len; sbase += pl.nst[pp]; p = pp + 1; }
+        }
+        idx = rem;
+      }
+      const int cap = pl.cap[p];
+      const int sgi = sbase + idx / cap;
+      const int es = sgi % NST;
+      const int fill = sgi / NST;
+      const uint32_t par = (uint32_t)fill & 1u;
+      const int kind = p;
+      const int ii = pl.lo[p] + idx;
+      const int ntok = p == 4 ? min(16, gg.rl - 16 * (ii - gg.nslots)) : 0;
+      const uint8_t *rec = ring + (size_t)es * STAGE + (size_t)(idx % cap) * pl.sz[p];
+      uint64_t t_b = ts ? gtime() : 0;
+      // the slot must be on this fill before its parity is meaningful (a claim can
+      // run more than one ring lap ahead of a slot that is still loading)
+      while (*reinterpret_cast<volatile int *>(stage_fill + es) < fill) {
+      }
+      mbar_wait(&full[es], par);
+      uint64_t t_c = ts ? gtime() : 0;
+      if (ts) { acc_tag += t_b - t_a; acc_full += t_c - t_b; }
+      if (a.debug & 1) {
+        st.l[0] += (float)lds32(rec + 16 * lane);
+      } else switch (kind) {
         case 0: do_window<D, S, 2>(rec, qf, a.scale_log2, st, o, scratch, lane); break;
         case 1: do_window<D, S, 4>(rec, qf, a.scale_log2, st, o, scratch, lane); break;
         case 2: do_window<D, S, 8>(rec, qf, a.scale_log2, st, o, scratch, lane); break;
         case 3: do_window<D, S, 16>(rec, qf, a.scale_log2, st, o, scratch, lane); break;
-        default: do_rest<D>(rec, dsc.ntok[it], qf, a.scale_log2, st, o, scratch, lane); break;
+        default: do_rest<D>(rec, ntok, qf, a.scale_log2, st, o, scratch, lane); break;
+      }
+      __syncwarp();
+      if (ts) acc_comp += gtime() - t_c;
+      if (lane == 0) {
+        const int nd = atomicAdd(stage_done + es, 1) + 1;
+        if (nd == *reinterpret_cast<volatile int *>(stage_n + es)) {
+          stage_done[es] = 0;
+          mbar_arrive(&empty[es]);
+        }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == NST) { stage = 0; phase ^= 1; }
-    if (!(flags & 1)) continue;
+    if (n_u) for (int pp = 0; pp < 5; pp++) sg_base += pl.nst[pp];
+    seq_base += n_u;
+    if (ts && tid == 0) ts[3] = gtime();
+    const uint64_t t_e0 = ts ? gtime() : 0;
 
-    // ---------------- unit epilogue ----------------
+    // ---------------- unit epilogue: merge tree over the warps ----------------
+    named_bar_sync(1, NCW * 32);
+    if (tid == 0) claim[uidx & 1] = 0;            // reused by the unit after next
+    uidx++;
     {
-      // reduce lane partials over the 8 lanes sharing a head pair (xor 4, 8, 16)
-      for (int off = 4; off <= 16; off <<= 1) {
-        st.l[0] += __shfl_xor_sync(0xffffffffu, st.l[0], off);
-        st.l[1] += __shfl_xor_sync(0xffffffffu, st.l[1], off);
-        st.vb[0] += __shfl_xor_sync(0xffffffffu, st.vb[0], off);
-        st.vb[1] += __shfl_xor_sync(0xffffffffu, st.vb[1], off);
+      // 15 -> 8 -> 4 -> 2 -> 1 (warp w >= half hands its state to warp w - half)
+      for (int cnt = NCW; cnt > 1;) {
+        const int half = (cnt + 1) / 2;
+        if (warp >= half && warp < cnt) store_state<KT>(st, o, ep + (warp - half) * SM::EPW, lane);
+        named_bar_sync(1, NCW * 32);
+        if (warp < cnt - half) merge_state<KT>(st, o, ep + warp * SM::EPW, lane);
+        named_bar_sync(1, NCW * 32);
+        cnt = half;
       }
-      float *mine = ep + warp * SM::EP_WARP;     // [m 8][l 8][vb 8][o D x 8]
-      if (g == 0) {
-        mine[2 * q] = st.m[0]; mine[2 * q + 1] = st.m[1];
-        mine[8 + 2 * q] = st.l[0]; mine[8 + 2 * q + 1] = st.l[1];
-        mine[16 + 2 * q] = st.vb[0]; mine[16 + 2 * q + 1] = st.vb[1];
-      }
-#pragma unroll
-      for (int mt = 0; mt < KT; mt++) {
-        float *oc = mine + 24 + (16 * mt + g) * 8 + 2 * q;
-        oc[0] = o[mt][0]; oc[1] = o[mt][1];
-        oc[64] = o[mt][2]; oc[65] = o[mt][3];     // channel + 8
-      }
-      named_bar_sync(1, NCW * 32);
-      const int b = u / a.H, h = u % a.H;
-      const int64_t us = ustart[u], ue = ustart[u + 1];
       const int cf = owner_of(us, G, T);
       const int cl = ue > us ? owner_of(ue - 1, G, T) : cf;
       float *slot = a.ws_part + (int64_t)(c + u) * a.grp * (D + 2);
-      for (int idx = tid; idx < a.grp * (D + 2); idx += NCW * 32) {
-        const int j = idx / (D + 2), e = idx % (D + 2);
-        float M = -INFINITY;
-        for (int w = 0; w < NCW; w++) M = fmaxf(M, ep[w * SM::EP_WARP + j]);
-        float acc = 0.f;
-        for (int w = 0; w < NCW; w++) {
-          const float *pw = ep + w * SM::EP_WARP;
-          const float f = (M == -INFINITY) ? 0.f : exp2f(pw[j] - M);
-          if (e == 1) acc += f * pw[8 + j];
-          else if (e >= 2) acc += f * (pw[24 + (e - 2) * 8 + j] + pw[16 + j]);
+      if (warp == 0) {
+        // reduce lane partials of l and vb over the 8 lanes sharing a head pair
+        for (int off = 4; off <= 16; off <<= 1) {
+          st.l[0] += __shfl_xor_sync(0xffffffffu, st.l[0], off);
+          st.l[1] += __shfl_xor_sync(0xffffffffu, st.l[1], off);
+          st.vb[0] += __shfl_xor_sync(0xffffffffu, st.vb[0], off);
+          st.vb[1] += __shfl_xor_sync(0xffffffffu, st.vb[1], off);
         }
-        slot[idx] = e == 0 ? M : acc;
-      }
-      __threadfence();
-      named_bar_sync(1, NCW * 32);
-      if (tid == 0) {
-        const int old = atomicAdd(a.ws_cnt + u, 1);
-        *s_flag = (old == cl - cf);
+        // CTA partial: (m, l, o + vb) for heads j = 2q, 2q+1 < grp
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int j = 2 * q + e;
+          if (j < a.grp) {
+            float *sp = slot + j * (D + 2);
+            if (g == 0) { sp[0] = st.m[e]; sp[1] = st.l[e]; }
+#pragma unroll
+            for (int mt = 0; mt < KT; mt++) {
+              sp[2 + 16 * mt + g] = o[mt][e] + st.vb[e];
+              sp[2 + 16 * mt + g + 8] = o[mt][2 + e] + st.vb[e];
+            }
+          }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          const int old = atomicAdd(a.ws_cnt + u, 1);
+          *s_flag = (old == cl - cf);
+        }
+        __syncwarp();
       }
       named_bar_sync(1, NCW * 32);
       if (*s_flag) {
+        // last CTA of the unit: log-sum-exp merge of the unit's CTA partials.
+        // (m, l) of every partial -> per-partial weights in shared memory (reusing
+        // the merge-tree buffer), then each thread sums its output columns.
         __threadfence();
+        const int np = cl - cf + 1;
+        float *wgt = ep;                              // [np][8] weights, then [8] M, [8] L
+        float *Ms = ep + (size_t)np * 8, *Ls = Ms + 8;
+        if (tid < a.grp) {
+          const int j = tid;
+          float M = -INFINITY;
+          for (int c2 = 0; c2 < np; c2++)
+            M = fmaxf(M, __ldcg(a.ws_part + (int64_t)(cf + c2 + u) * a.grp * (D + 2) + j * (D + 2)));
+          float L = 0.f;
+          for (int c2 = 0; c2 < np; c2++) {
+            const float *sp = a.ws_part + (int64_t)(cf + c2 + u) * a.grp * (D + 2) + j * (D + 2);
+            const float f = (M == -INFINITY) ? 0.f : exp2f(__ldcg(sp) - M);
+            wgt[c2 * 8 + j] = f;
+            L += f * __ldcg(sp + 1);
+          }
+          Ms[j] = M;
+          Ls[j] = L;
+        }
+        named_bar_sync(1, NCW * 32);
         for (int idx = tid; idx < a.grp * D; idx += NCW * 32) {
           const int j = idx / D, cc = idx % D;
-          float M = -INFINITY;
-          for (int c2 = cf; c2 <= cl; c2++) {
-            const float *sp = a.ws_part + (int64_t)(c2 + u) * a.grp * (D + 2) + j * (D + 2);
-            M = fmaxf(M, __ldcg(sp));
+          float O = 0.f;
+          const float *base = a.ws_part + (int64_t)(cf + u) * a.grp * (D + 2) + j * (D + 2) + 2 + cc;
+          const int64_t stride = (int64_t)a.grp * (D + 2);
+          int c2 = 0;
+          for (; c2 + 4 <= np; c2 += 4) {
+            const float o0 = __ldcg(base + (c2 + 0) * stride), o1 = __ldcg(base + (c2 + 1) * stride);
+            const float o2 = __ldcg(base + (c2 + 2) * stride), o3 = __ldcg(base + (c2 + 3) * stride);
+            O += wgt[(c2 + 0) * 8 + j] * o0 + wgt[(c2 + 1) * 8 + j] * o1 + wgt[(c2 + 2) * 8 + j] * o2 +
+                 wgt[(c2 + 3) * 8 + j] * o3;
           }
-          float L = 0.f, O = 0.f;
-          for (int c2 = cf; c2 <= cl; c2++) {
-            const float *sp = a.ws_part + (int64_t)(c2 + u) * a.grp * (D + 2) + j * (D + 2);
-            const float f = (M == -INFINITY) ? 0.f : exp2f(__ldcg(sp) - M);
-            L += f * __ldcg(sp + 1);
-            O += f * __ldcg(sp + 2 + cc);
-          }
+          for (; c2 < np; c2++) O += wgt[c2 * 8 + j] * __ldcg(base + c2 * stride);
+          const float L = Ls[j];
           const int64_t row = (int64_t)b * a.Hq + h * a.grp + j;
           if (a.out) a.out[row * D + cc] = __float2half_rn(L > 0.f ? O / L : 0.f);
           if (a.partial) {
             float *pp = a.partial + row * (D + 2);
             if (cc == 0) {
-              pp[0] = M * 0.69314718055994530942f;   // log2 domain -> natural
+              pp[0] = Ms[j] * 0.69314718055994530942f;   // log2 domain -> natural
               pp[1] = L;
             }
             pp[2 + cc] = O;
@@ -649,12 +766,13 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         if (tid == 0) a.ws_cnt[u] = 0;
       }
       named_bar_sync(1, NCW * 32);
-      // reset warp state for the next unit
-      for (int mt = 0; mt < KT; mt++) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
-      st.m[0] = st.m[1] = -INFINITY;
-      st.l[0] = st.l[1] = st.vb[0] = st.vb[1] = 0.f;
     }
-    if (flags & 2) break;
+    if (ts && tid == 0) { ts[4] = gtime(); ts[5] = (uint64_t)seq_base; }
+    if (ts) t_ep += gtime() - t_e0;
+  }
+  if (ts && lane == 0) {
+    uint64_t *wt = ts + 8 + warp * 4;
+    wt[0] = acc_tag; wt[1] = acc_full; wt[2] = acc_comp; wt[3] = t_ep;
   }
 }
 
@@ -682,7 +800,8 @@ size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms) {
   const int grp = Hq / H;
   size_t part = (size_t)(num_sms + B * H) * grp * (d + 2) * sizeof(float);
   part = (part + 255) / 256 * 256;
-  return part + (size_t)B * H * sizeof(int32_t);
+  size_t cnt = ((size_t)B * H * sizeof(int32_t) + 255) / 256 * 256;
+  return part + cnt + (size_t)num_sms * 72 * sizeof(uint64_t);
 }
 
 template <int D, int S>

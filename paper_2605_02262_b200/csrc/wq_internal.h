@@ -44,10 +44,12 @@ struct DecodeArgs {
   int R_max;
   int B, H, Hq, grp, d, S;
   float scale_log2;          // sm_scale * log2(e)
+  int debug;                 // WQ_DECODE_DEBUG: 1 = stream only (no math), profiling aid
   __half *out;
   float *partial;
   float *ws_part;            // [(G + B*H)][grp][d + 2]
   int32_t *ws_cnt;           // [B*H]
+  uint64_t *ws_ts;           // [num_sms][8] timestamps when debug & 8, else NULL
 };
 size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms);
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st);
