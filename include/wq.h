@@ -81,8 +81,11 @@ typedef struct {
  *   [K params: 4*d bytes][V params: 4*S bytes]           size S*d*b/4 + 4d + 4S
  * Width 16: [K values: S/16 x 32*d bytes][V values: S/16 x 32*d bytes]  size 4*S*d
  *
- * Code tiles are in "fragment order": a tile is 32 lane chunks of d*b/16
- * bytes, chunk L belongs to lane L (g = L/4, q = L%4).  A chunk holds d/4
+ * Code tiles are in "fragment order": a tile holds 32 lane chunks of d*b/16
+ * bytes, chunk L belongs to lane L (g = L/4, q = L%4).  Chunks of >= 16 bytes
+ * are interleaved in 16-byte groups so a warp's 16-byte loads are contiguous:
+ * word w of chunk L is at byte (w/4)*512 + L*16 + (w%4)*4 of the tile; an
+ * 8-byte chunk (d = 64, b = 2) is at byte L*8.  A chunk holds d/4
  * element PAIRS P = 0..d/4-1 with m = P/4, r = P%4:
  *   K tile (tokens x channels): row = g + 8*(r&1) (token in tile),
  *                               col = 16*m + 2*q + 8*(r>>1) (channel)

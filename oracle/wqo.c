@@ -360,7 +360,10 @@ void wqo_code_pos(int32_t is_v, int32_t d, int32_t b, int32_t t, int32_t c,
   int word = P / pairs_per_word, j = P % pairs_per_word;
   int64_t tile_bytes = 2LL * d * b;                      /* 16 rows * d cols * b bits / 8 */
   int64_t chunk = (int64_t)d * b / 16;
-  *byte_off = tile * tile_bytes + lane * chunk + 4LL * word;
+  if (chunk >= 16)                                       /* 16-byte groups, lane-interleaved */
+    *byte_off = tile * tile_bytes + (word / 4) * 512LL + lane * 16LL + 4LL * (word % 4);
+  else
+    *byte_off = tile * tile_bytes + lane * chunk + 4LL * word;
   *bit = 16 * e + b * j;
 }
 

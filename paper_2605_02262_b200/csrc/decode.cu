@@ -28,10 +28,19 @@
 
 namespace wq {
 
-constexpr int NCW = 15;                 // consumer warps (16 warps: 4 per SM sub-partition)
+#ifndef WQ_DEC_NCW
+#define WQ_DEC_NCW 11
+#endif
+#ifndef WQ_DEC_RING
+#define WQ_DEC_RING 163840
+#endif
+constexpr int NCW = WQ_DEC_NCW;                 // consumer warps
 constexpr int DT = (NCW + 1) * 32;      // threads per CTA
 constexpr int MAX_UNITS = 1024;         // B * H
 constexpr int64_t MIN_CTA_BYTES = 49152;
+#ifndef WQ_DEC_STAGE
+#define WQ_DEC_STAGE 32768
+#endif
 constexpr float LAZY_TH = 8.0f;         // log2 headroom of the lazy softmax rescale
 constexpr int KIND_REST = 4;
 
@@ -48,8 +57,8 @@ struct UnitGeo {
 };
 
 WQ_DEV int64_t item_cost(int k, int d, int S) {   // k = 0..3 class, 4 = rest tile
-  if (k == 4) return 64LL * d + 6LL * d;
-  return record_bytes(class_bits(k), d, S) + (k == 3 ? 3LL * S * d / 8 : 3LL * S * d / 4);
+  if (k == 4) return 64LL * d + 176LL * d;
+  return record_bytes(class_bits(k), d, S) + (k == 3 ? 6LL * S * d : 12LL * S * d);
 }
 
 WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
@@ -68,12 +77,18 @@ WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
   g.rl = a.rest_len ? a.rest_len[g.b] : 0;
   g.ntiles = (g.rl + 15) / 16;
 }
+// Fixed per-unit costs: the unit epilogue (warp merge tree + CTA partial + ticket)
+// is charged at the unit's start and the cross-CTA log-sum-exp merge at its end,
+// so a CTA that crosses a unit boundary or finishes a unit gets fewer windows.
+constexpr int64_t COST_UNIT_HEAD = 0;
+constexpr int64_t COST_UNIT_TAIL = 0;
 WQ_DEV int64_t unit_cost(const DecodeArgs &a, const UnitGeo &g) {
-  return g.cc[4] + (int64_t)g.ntiles * item_cost(4, a.d, a.S);
+  return COST_UNIT_HEAD + g.cc[4] + (int64_t)g.ntiles * item_cost(4, a.d, a.S) + COST_UNIT_TAIL;
 }
 
 // first item whose start (in cost units, relative to the unit) is >= x
 WQ_DEV int first_item(const DecodeArgs &a, const UnitGeo &g, int64_t x) {
+  x -= COST_UNIT_HEAD;
   if (x <= 0) return 0;
   for (int k = 0; k < 4; k++) {
     if (x <= g.cc[k]) return g.so[k];
@@ -96,6 +111,15 @@ struct UnitPlan {
   int lo[5], hi[5], cap[5], nst[5];
   int sz[5];
 };
+// The unit the consumers work on, published in shared memory by warp 0 (keeps
+// the plan out of the per-thread registers of the window loop).
+struct UnitSm {
+  int u, n_u, sg_base, rl, nslots, tag;
+  int len[5], nst[5], cap[5], lo[5], sz[5];
+  float rcap[5];                        // 1 / cap (exact integer division for idx < 2^20)
+  int c0, c1;                           // CTAs sharing this unit
+};
+
 template <int STAGE>
 WQ_DEV void plan_unit(const DecodeArgs &a, const UnitGeo &g, int i0, int i1, UnitPlan &pl) {
   for (int p = 0; p < 5; p++) {
@@ -103,7 +127,7 @@ WQ_DEV void plan_unit(const DecodeArgs &a, const UnitGeo &g, int i0, int i1, Uni
     const int a1 = p < 4 ? g.so[p + 1] : g.nslots + g.ntiles;
     const int lo = i0 > a0 ? i0 : a0;
     const int hi = i1 < a1 ? i1 : a1;
-    const int sz = p < 4 ? (int)record_bytes(class_bits(p), a.d, a.S) : 64 * a.d;
+    const int sz = p < 4 ? (int)record_bytes(class_bits(p), a.d, a.S) : 32 * (2 * a.d + 16);
     pl.lo[p] = lo;
     pl.hi[p] = hi > lo ? hi : lo;
     pl.sz[p] = sz;
@@ -113,6 +137,24 @@ WQ_DEV void plan_unit(const DecodeArgs &a, const UnitGeo &g, int i0, int i1, Uni
 }
 
 WQ_DEV int64_t cta_lo(int c, int G, int64_t T) { return (int64_t)c * T / G; }
+
+// CTAs [c0, c1) that share unit u.  With at least as many units as CTAs, whole
+// units go to the CTA owning their cost midpoint (no cross-CTA merge); with fewer
+// units, every unit gets 1 + its cost share of the remaining CTAs, so no CTA
+// ever spans two split units (one epilogue per CTA).
+WQ_DEV void unit_ctas(int u, int U, int G, int64_t T, const int64_t *ustart, int &c0, int &c1) {
+  if (T <= 0) { c0 = 0; c1 = 1; return; }
+  if (U >= G) {
+    const int64_t mid = ustart[u] + (ustart[u + 1] - ustart[u]) / 2;
+    c0 = (int)((mid * G) / T);
+    if (c0 >= G) c0 = G - 1;
+    c1 = c0 + 1;
+  } else {
+    const int64_t extra = G - U;
+    c0 = u + (int)((ustart[u] * extra + T / 2) / T);
+    c1 = (u + 1 < U) ? (u + 1) + (int)((ustart[u + 1] * extra + T / 2) / T) : G;
+  }
+}
 WQ_DEV int owner_of(int64_t x, int G, int64_t T) {
   if (T <= 0) return 0;
   int c = (int)((x * G) / T);
@@ -165,15 +207,16 @@ WQ_DEV uint32_t deq_pair(const uint32_t *wd, int P) {
 template <int D, int BITS>
 WQ_DEV void load_chunk(uint32_t (&wd)[D * BITS / 64], const uint8_t *tile, int lane) {
   constexpr int WPL = D * BITS / 64;
-  const uint8_t *ch = tile + lane * (D * BITS / 16);
   if constexpr (WPL >= 4) {
+    // D-1: 16-byte groups interleaved across lanes (conflict-free LDS.128)
+    const uint8_t *ch = tile + lane * 16;
 #pragma unroll
     for (int i = 0; i < WPL / 4; i++) {
-      uint4 v = lds128(ch + 16 * i);
+      uint4 v = lds128(ch + 512 * i);
       wd[4 * i] = v.x; wd[4 * i + 1] = v.y; wd[4 * i + 2] = v.z; wd[4 * i + 3] = v.w;
     }
   } else {
-    uint2 v = lds64(ch);
+    uint2 v = lds64(tile + lane * (D * BITS / 16));
     wd[0] = v.x; wd[1] = v.y;
   }
 }
@@ -333,19 +376,20 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
   }
 }
 
-// FP16 rest tile: K rows [16][D] at base, V rows [16][D] at base + 32*D (natural layout)
+// FP16 rest tile: K rows [16][D] at base, V rows [16][D] after them, rows padded to 2D+16 bytes
 template <int D>
 WQ_DEV void do_rest(const uint8_t *base, int ntok, const uint32_t (&qf)[D / 16][2], float scale2,
                     WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane) {
   constexpr int KT = D / 16;
+  constexpr int RPH = D + 8;                       // padded row stride (halves)
   const __half *Ks = reinterpret_cast<const __half *>(base);
-  const __half *Vs = Ks + 16 * D;
+  const __half *Vs = Ks + 16 * RPH;
   const int g = lane >> 2, q = lane & 3, mi = lane >> 3, rr = lane & 7;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int kt = 0; kt < KT; kt++) {
     uint32_t a[4];
-    ldsm_x4(a, Ks + ((mi & 1) * 8 + rr) * D + 16 * kt + (mi >> 1) * 8);
+    ldsm_x4(a, Ks + ((mi & 1) * 8 + rr) * RPH + 16 * kt + (mi >> 1) * 8);
     mma16816(acc, a, qf[kt][0], qf[kt][1], acc);
   }
   float sc[1][4];
@@ -363,7 +407,7 @@ WQ_DEV void do_rest(const uint8_t *base, int ntok, const uint32_t (&qf)[D / 16][
 #pragma unroll
   for (int mt = 0; mt < KT; mt++) {
     uint32_t a[4];
-    ldsm_x4_t(a, Vs + ((mi >> 1) * 8 + rr) * D + 16 * mt + (mi & 1) * 8);
+    ldsm_x4_t(a, Vs + ((mi >> 1) * 8 + rr) * RPH + 16 * mt + (mi & 1) * 8);
     a[0] &= m01; a[1] &= m01; a[2] &= m89; a[3] &= m89;
     mma16816(o[mt], a, pb[0], pb[1], o[mt]);
   }
@@ -377,26 +421,28 @@ template <int D, int S>
 struct DecodeSmem {
   // a stage must hold the largest item (an FP16 window: 4*S*D bytes); small stages
   // release shared memory item-group by item-group, a deep ring gives lookahead.
-  static constexpr int STAGE = (4 * S * D > 16384) ? 4 * S * D : 16384;
-  static constexpr int RING = 163840;
+  static constexpr int STAGE = (4 * S * D > WQ_DEC_STAGE) ? 4 * S * D : WQ_DEC_STAGE;
+  static constexpr int RING = WQ_DEC_RING;
   static constexpr int NST = (RING / STAGE) < 2 ? 2 : RING / STAGE;
   static constexpr int KT = D / 16;
   static constexpr int SCRATCH = 2 * 16 * 16;            // P' rows of one 2-tile chunk per warp
-  static constexpr int EPW = (KT * 4 + 6) * 32;          // floats of one warp state (fragment layout)
-  static constexpr int EP_SLOTS = 7;                     // merge tree 15 -> 8 -> 4 -> 2 -> 1
+  // epilogue: every warp's o as [8 heads][D] + (m, l, vb)[8]; 1200+ floats reused by
+  // the cross-CTA merge of the last CTA
+  static constexpr int EPW = 8 * D + 24;
+  static constexpr int EP_SLOTS = NCW;
   static constexpr size_t ring = (size_t)NST * STAGE;
   static constexpr size_t scratch_off = ring;
   static constexpr size_t ep_off = scratch_off + (size_t)NCW * SCRATCH;
   static constexpr size_t units_off = ep_off + (size_t)EP_SLOTS * EPW * 4;
   static constexpr size_t cnt_off = units_off + (size_t)(MAX_UNITS + 1) * 8;
-  static constexpr size_t bar_off = (cnt_off + (size_t)(3 * NST + 4) * 4 + 15) / 16 * 16;
+  static constexpr size_t usm_off = (cnt_off + (size_t)(3 * NST + 4) * 4 + 15) / 16 * 16;
+  static constexpr int NUS = 4;                          // unit-plan ring published by the producer
+  static constexpr size_t bar_off = usm_off + NUS * sizeof(UnitSm);
   static constexpr size_t total = bar_off + 2 * NST * 8 + 16;
 };
 
-WQ_DEV uint64_t gtime() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+WQ_DEV uint64_t gtime() {      // profiling clock: SM cycles scaled to ~ns at 1.965 GHz
+  return (uint64_t)((double)clock64() * (1.0 / 1.965));
 }
 
 WQ_DEV void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
@@ -410,41 +456,6 @@ WQ_DEV void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
     if (done) return;
     __nanosleep(64);
   }
-}
-
-// merge warp state B (m, l, vb, o as seen by this lane) into A
-template <int KT>
-WQ_DEV void merge_state(WarpState &A, float (&oA)[KT][4], const float *Bst, int lane) {
-  // Bst layout: [KT*4 o][m0 m1 l0 l1 vb0 vb1] per lane, lane-major stride 32
-  const float bm0 = Bst[(KT * 4 + 0) * 32 + lane], bm1 = Bst[(KT * 4 + 1) * 32 + lane];
-  const float M0 = fmaxf(A.m[0], bm0), M1 = fmaxf(A.m[1], bm1);
-  const float fa0 = M0 == -INFINITY ? 0.f : exp2f(A.m[0] - M0), fb0 = M0 == -INFINITY ? 0.f : exp2f(bm0 - M0);
-  const float fa1 = M1 == -INFINITY ? 0.f : exp2f(A.m[1] - M1), fb1 = M1 == -INFINITY ? 0.f : exp2f(bm1 - M1);
-  A.m[0] = M0; A.m[1] = M1;
-  A.l[0] = fa0 * A.l[0] + fb0 * Bst[(KT * 4 + 2) * 32 + lane];
-  A.l[1] = fa1 * A.l[1] + fb1 * Bst[(KT * 4 + 3) * 32 + lane];
-  A.vb[0] = fa0 * A.vb[0] + fb0 * Bst[(KT * 4 + 4) * 32 + lane];
-  A.vb[1] = fa1 * A.vb[1] + fb1 * Bst[(KT * 4 + 5) * 32 + lane];
-#pragma unroll
-  for (int mt = 0; mt < KT; mt++) {
-    oA[mt][0] = fa0 * oA[mt][0] + fb0 * Bst[(mt * 4 + 0) * 32 + lane];
-    oA[mt][1] = fa1 * oA[mt][1] + fb1 * Bst[(mt * 4 + 1) * 32 + lane];
-    oA[mt][2] = fa0 * oA[mt][2] + fb0 * Bst[(mt * 4 + 2) * 32 + lane];
-    oA[mt][3] = fa1 * oA[mt][3] + fb1 * Bst[(mt * 4 + 3) * 32 + lane];
-  }
-}
-template <int KT>
-WQ_DEV void store_state(const WarpState &A, const float (&oA)[KT][4], float *Bst, int lane) {
-#pragma unroll
-  for (int mt = 0; mt < KT; mt++)
-#pragma unroll
-    for (int i = 0; i < 4; i++) Bst[(mt * 4 + i) * 32 + lane] = oA[mt][i];
-  Bst[(KT * 4 + 0) * 32 + lane] = A.m[0];
-  Bst[(KT * 4 + 1) * 32 + lane] = A.m[1];
-  Bst[(KT * 4 + 2) * 32 + lane] = A.l[0];
-  Bst[(KT * 4 + 3) * 32 + lane] = A.l[1];
-  Bst[(KT * 4 + 4) * 32 + lane] = A.vb[0];
-  Bst[(KT * 4 + 5) * 32 + lane] = A.vb[1];
 }
 
 template <int D, int S>
@@ -461,6 +472,8 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   int *stage_fill = stage_done + NST;                             // fill number a slot holds
   int *claim = stage_fill + NST;                                  // [2] per-unit claim counters
   int *s_flag = claim + 2;
+  int *units_done = s_flag + 1;
+  UnitSm *usm = reinterpret_cast<UnitSm *>(sm + SM::usm_off);
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + SM::bar_off);
   uint64_t *empty = full + NST;
 
@@ -499,6 +512,8 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       stage_fill[s] = -1;
     }
     claim[0] = claim[1] = 0;
+    *units_done = 0;
+    for (int i = 0; i < SM::NUS; i++) usm[i].tag = -1;
     fence_mbar_init();
   }
   __syncthreads();
@@ -507,7 +522,6 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   G = G < 1 ? 1 : (G > (int)gridDim.x ? (int)gridDim.x : G);
   const int c = blockIdx.x;
   if (c >= G) return;
-  const int64_t lo = cta_lo(c, G, T), hi = cta_lo(c + 1, G, T);
   if (ts && tid == 0) ts[1] = gtime();
 
   if (warp == NCW) {
@@ -519,16 +533,49 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       const uint64_t pol = policy_evict_first();
       const bool nocopy = (a.debug & 2) != 0;
       int sg = 0;                                  // global stage number of this CTA
+      int uix = 0;                                 // index of the unit among this CTA's units
+      // publish a unit plan for the consumers (ring of NUS slots, tag written last)
+      auto publish = [&](int u, int n_u, const UnitGeo *gg, const UnitPlan *pl, int c0, int c1) {
+        while (*reinterpret_cast<volatile int *>(units_done) < uix - (SM::NUS - 1)) {
+        }
+        UnitSm &d = usm[uix % SM::NUS];
+        d.u = u;
+        d.n_u = n_u;
+        d.sg_base = sg;
+        d.c0 = c0;
+        d.c1 = c1;
+        d.rl = gg ? gg->rl : 0;
+        d.nslots = gg ? gg->nslots : 0;
+        for (int pp = 0; pp < 5; pp++) {
+          d.len[pp] = pl ? pl->hi[pp] - pl->lo[pp] : 0;
+          d.nst[pp] = pl ? pl->nst[pp] : 0;
+          d.cap[pp] = pl ? pl->cap[pp] : 1;
+          d.rcap[pp] = 1.0f / (float)d.cap[pp];
+          d.lo[pp] = pl ? pl->lo[pp] : 0;
+          d.sz[pp] = pl ? pl->sz[pp] : 0;
+        }
+        __threadfence_block();
+        *reinterpret_cast<volatile int *>(&d.tag) = uix;
+        uix++;
+      };
       for (int u = 0; u < U; u++) {
+        int c0, c1;
+        unit_ctas(u, U, G, T, ustart, c0, c1);
+        if (c < c0 || c >= c1) continue;
         const int64_t us = ustart[u], ue = ustart[u + 1];
-        if (ue <= us || ue <= lo || us >= hi) continue;
+        if (ue <= us) {
+          publish(u, 0, nullptr, nullptr, c0, c1);
+          continue;
+        }
         UnitGeo gg;
         unit_geo(a, u, gg);
         const int nitems = gg.nslots + gg.ntiles;
-        const int i0 = first_item(a, gg, lo - us);
-        const int i1 = hi >= ue ? nitems : first_item(a, gg, hi - us);
+        const int64_t ucost = ue - us, k = c - c0, n = c1 - c0;
+        const int i0 = first_item(a, gg, k * ucost / n);
+        const int i1 = (k == n - 1) ? nitems : first_item(a, gg, (k + 1) * ucost / n);
         UnitPlan pl;
         plan_unit<STAGE>(a, gg, i0, i1, pl);
+        publish(u, i1 - i0, &gg, &pl, c0, c1);
         const uint8_t *img = a.packed + a.offs[u];
         const __half *kr = a.k_rest + gg.b * a.rs_b + gg.h * a.rs_h;
         const __half *vr = a.v_rest + gg.b * a.rs_b + gg.h * a.rs_h;
@@ -552,17 +599,23 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
               uint32_t tx = 0;
               for (int i = f0; i < f1; i++) tx += (uint32_t)min(16, gg.rl - 16 * (i - gg.nslots)) * 4u * D;
               mbar_arrive_expect_tx(&full[slot], tx);
+              // FP16 rest rows land in padded rows (stride 2D+16 B) so the ldmatrix
+              // reads of do_rest are bank-conflict free
+              constexpr int RP = 2 * D + 16;
               for (int i = f0; i < f1; i++) {
                 const int t0 = 16 * (i - gg.nslots);
-                const uint32_t nb = (uint32_t)min(16, gg.rl - t0) * 2 * D;
+                const int nt = min(16, gg.rl - t0);
                 uint8_t *d2 = dst + (size_t)(i - f0) * pl.sz[4];
-                bulk_g2s_evict_first(d2, kr + (int64_t)t0 * D, nb, &full[slot], pol);
-                bulk_g2s_evict_first(d2 + 32 * D, vr + (int64_t)t0 * D, nb, &full[slot], pol);
+                for (int r = 0; r < nt; r++) {
+                  bulk_g2s_evict_first(d2 + r * RP, kr + (int64_t)(t0 + r) * D, 2 * D, &full[slot], pol);
+                  bulk_g2s_evict_first(d2 + (16 + r) * RP, vr + (int64_t)(t0 + r) * D, 2 * D, &full[slot], pol);
+                }
               }
             }
           }
         }
       }
+      publish(-1, 0, nullptr, nullptr, 0, 1);     // terminator
       if (ts) ts[2] = gtime();
     }
     return;
@@ -577,23 +630,18 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   uint32_t qf[KT][2];
   float o[KT][4];
   WarpState st;
-  int seq_base = 0, uidx = 0, sg_base = 0;
+  int uidx = 0;
   uint64_t acc_tag = 0, acc_full = 0, acc_comp = 0, t_ep = 0;
-  for (int u = 0; u < U; u++) {
-    const int64_t us = ustart[u], ue = ustart[u + 1];
-    const bool mine = (ue > us) ? !(ue <= lo || us >= hi) : owner_of(us, G, T) == c;
-    if (!mine) continue;
-    int n_u = 0;
-    UnitGeo gg;
-    UnitPlan pl;
-    if (ue > us) {
-      unit_geo(a, u, gg);
-      const int nitems = gg.nslots + gg.ntiles;
-      const int i0 = first_item(a, gg, lo - us);
-      const int i1 = hi >= ue ? nitems : first_item(a, gg, hi - us);
-      n_u = i1 - i0;
-      plan_unit<STAGE>(a, gg, i0, i1, pl);
+  for (;;) {
+    const UnitSm &U_ = usm[uidx % SM::NUS];
+    while (*reinterpret_cast<const volatile int *>(&U_.tag) != uidx) {
     }
+    __threadfence_block();
+    const int u = *reinterpret_cast<const volatile int *>(&U_.u);
+    if (u < 0) break;
+    const int n_u = U_.n_u;
+    const int sg_base = U_.sg_base;
+    const int cf = U_.c0, cl = U_.c1 - 1;
     const int b = u / a.H, h = u % a.H;
     {
       const __half *qrow = a.q + ((int64_t)b * a.Hq + h * a.grp + g) * D;
@@ -608,32 +656,28 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
     st.m[0] = st.m[1] = -INFINITY;
     st.l[0] = st.l[1] = st.vb[0] = st.vb[1] = 0.f;
     int *cl_ctr = claim + (uidx & 1);
+    int j = 0;
+    if (lane == 0) j = atomicAdd(cl_ctr, 1);
+    j = __shfl_sync(0xffffffffu, j, 0);
     for (;;) {
       uint64_t t_a = ts ? gtime() : 0;
-      int j = 0;
-      if (lane == 0) j = atomicAdd(cl_ctr, 1);
-      j = __shfl_sync(0xffffffffu, j, 0);
       if (j >= n_u) break;
-      // locate item j of the unit in the stage plan
-      int p = 0, sbase = sg_base, idx = 0;
-      {
-        int rem = j;
-#pragma unroll
-        for (int pp = 0; pp < 5; pp++) {
-          const int len = pl.hi[pp] - pl.lo[pp];
-          if (p == pp && rem >= len) { rem -= len; sbase += pl.nst[pp]; p = pp + 1; }
-        }
-        idx = rem;
-      }
-      const int cap = pl.cap[p];
-      const int sgi = sbase + idx / cap;
+      // claim the next item now; its ticket is only needed after this window
+      int jn = 0;
+      if (lane == 0) jn = atomicAdd(cl_ctr, 1);
+      // locate item j of the unit in the stage plan (shared-memory plan)
+      int p = 0, sbase = sg_base, idx = j;
+      while (idx >= U_.len[p]) { idx -= U_.len[p]; sbase += U_.nst[p]; p++; }
+      const int cap = U_.cap[p];
+      const int qs = (int)(((float)idx + 0.5f) * U_.rcap[p]);   // idx / cap
+      const int sgi = sbase + qs;
       const int es = sgi % NST;
       const int fill = sgi / NST;
       const uint32_t par = (uint32_t)fill & 1u;
       const int kind = p;
-      const int ii = pl.lo[p] + idx;
-      const int ntok = p == 4 ? min(16, gg.rl - 16 * (ii - gg.nslots)) : 0;
-      const uint8_t *rec = ring + (size_t)es * STAGE + (size_t)(idx % cap) * pl.sz[p];
+      const int ii = U_.lo[p] + idx;
+      const int ntok = p == 4 ? min(16, U_.rl - 16 * (ii - U_.nslots)) : 0;
+      const uint8_t *rec = ring + (size_t)es * STAGE + (size_t)(idx - qs * cap) * U_.sz[p];
       uint64_t t_b = ts ? gtime() : 0;
       // the slot must be on this fill before its parity is meaningful (a claim can
       // run more than one ring lap ahead of a slot that is still loading)
@@ -652,7 +696,15 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         default: do_rest<D>(rec, ntok, qf, a.scale_log2, st, o, scratch, lane); break;
       }
       __syncwarp();
-      if (ts) acc_comp += gtime() - t_c;
+      jn = __shfl_sync(0xffffffffu, jn, 0);
+      if (ts) {
+        const uint64_t dt = gtime() - t_c;
+        acc_comp += dt;
+        if (lane == 0) {
+          atomicAdd(reinterpret_cast<unsigned long long *>(ts + 56 + kind), (unsigned long long)dt);
+          atomicAdd(reinterpret_cast<unsigned long long *>(ts + 61 + kind), 1ull);
+        }
+      }
       if (lane == 0) {
         const int nd = atomicAdd(stage_done + es, 1) + 1;
         if (nd == *reinterpret_cast<volatile int *>(stage_n + es)) {
@@ -660,79 +712,108 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
           mbar_arrive(&empty[es]);
         }
       }
+      j = jn;
     }
-    if (n_u) for (int pp = 0; pp < 5; pp++) sg_base += pl.nst[pp];
-    seq_base += n_u;
     if (ts && tid == 0) ts[3] = gtime();
     const uint64_t t_e0 = ts ? gtime() : 0;
 
     // ---------------- unit epilogue: merge tree over the warps ----------------
     named_bar_sync(1, NCW * 32);
+    const uint64_t t_e1 = ts ? gtime() : 0;
+    uint64_t t_e2 = 0, t_e3 = 0;
     if (tid == 0) claim[uidx & 1] = 0;            // reused by the unit after next
     uidx++;
     {
-      // 15 -> 8 -> 4 -> 2 -> 1 (warp w >= half hands its state to warp w - half)
-      for (int cnt = NCW; cnt > 1;) {
-        const int half = (cnt + 1) / 2;
-        if (warp >= half && warp < cnt) store_state<KT>(st, o, ep + (warp - half) * SM::EPW, lane);
-        named_bar_sync(1, NCW * 32);
-        if (warp < cnt - half) merge_state<KT>(st, o, ep + warp * SM::EPW, lane);
-        named_bar_sync(1, NCW * 32);
-        cnt = half;
+      // every warp parks its state (l, vb reduced over the 8 lanes of a head pair)
+      for (int off = 4; off <= 16; off <<= 1) {
+        st.l[0] += __shfl_xor_sync(0xffffffffu, st.l[0], off);
+        st.l[1] += __shfl_xor_sync(0xffffffffu, st.l[1], off);
+        st.vb[0] += __shfl_xor_sync(0xffffffffu, st.vb[0], off);
+        st.vb[1] += __shfl_xor_sync(0xffffffffu, st.vb[1], off);
       }
-      const int cf = owner_of(us, G, T);
-      const int cl = ue > us ? owner_of(ue - 1, G, T) : cf;
-      float *slot = a.ws_part + (int64_t)(c + u) * a.grp * (D + 2);
-      if (warp == 0) {
-        // reduce lane partials of l and vb over the 8 lanes sharing a head pair
-        for (int off = 4; off <= 16; off <<= 1) {
-          st.l[0] += __shfl_xor_sync(0xffffffffu, st.l[0], off);
-          st.l[1] += __shfl_xor_sync(0xffffffffu, st.l[1], off);
-          st.vb[0] += __shfl_xor_sync(0xffffffffu, st.vb[0], off);
-          st.vb[1] += __shfl_xor_sync(0xffffffffu, st.vb[1], off);
-        }
-        // CTA partial: (m, l, o + vb) for heads j = 2q, 2q+1 < grp
+      float *mine = ep + warp * SM::EPW;           // [8][D] o, then m[8], l[8], vb[8]
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const int j = 2 * q + e;
-          if (j < a.grp) {
-            float *sp = slot + j * (D + 2);
-            if (g == 0) { sp[0] = st.m[e]; sp[1] = st.l[e]; }
-#pragma unroll
-            for (int mt = 0; mt < KT; mt++) {
-              sp[2 + 16 * mt + g] = o[mt][e] + st.vb[e];
-              sp[2 + 16 * mt + g + 8] = o[mt][2 + e] + st.vb[e];
-            }
-          }
-        }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) {
-          const int old = atomicAdd(a.ws_cnt + u, 1);
-          *s_flag = (old == cl - cf);
-        }
-        __syncwarp();
+      for (int mt = 0; mt < KT; mt++) {
+        mine[(2 * q) * D + 16 * mt + g] = o[mt][0];
+        mine[(2 * q + 1) * D + 16 * mt + g] = o[mt][1];
+        mine[(2 * q) * D + 16 * mt + g + 8] = o[mt][2];
+        mine[(2 * q + 1) * D + 16 * mt + g + 8] = o[mt][3];
+      }
+      if (g == 0) {
+        mine[8 * D + 2 * q] = st.m[0]; mine[8 * D + 2 * q + 1] = st.m[1];
+        mine[8 * D + 8 + 2 * q] = st.l[0]; mine[8 * D + 8 + 2 * q + 1] = st.l[1];
+        mine[8 * D + 16 + 2 * q] = st.vb[0]; mine[8 * D + 16 + 2 * q + 1] = st.vb[1];
       }
       named_bar_sync(1, NCW * 32);
+      // per head: M, L and the warp weights f[w] (thread j < grp); weights overwrite m
+      float *Mh = reinterpret_cast<float *>(sm + SM::scratch_off);   // [8] M, [8] L (scratch is free now)
+      if (tid < a.grp) {
+        const int j = tid;
+        float M = -INFINITY;
+        for (int w = 0; w < NCW; w++) M = fmaxf(M, ep[w * SM::EPW + 8 * D + j]);
+        float L = 0.f;
+        for (int w = 0; w < NCW; w++) {
+          float *pw = ep + w * SM::EPW + 8 * D;
+          const float f = (M == -INFINITY) ? 0.f : exp2f(pw[j] - M);
+          L += f * pw[8 + j];
+          pw[j] = f;
+        }
+        Mh[j] = M;
+        Mh[8 + j] = L;
+      }
+      named_bar_sync(1, NCW * 32);
+      t_e2 = ts ? gtime() : 0;
+      float *slot = a.ws_part + (int64_t)(c + u) * a.grp * (D + 2);
+      // CTA partial (m, l, o + vb) [grp][D + 2], coalesced over channels
+      for (int idx = tid; idx < a.grp * D; idx += NCW * 32) {
+        const int j = idx / D, cc = idx % D;
+        float O = 0.f;
+#pragma unroll 5
+        for (int w = 0; w < NCW; w++) {
+          const float *pw = ep + w * SM::EPW;
+          O += pw[8 * D + j] * (pw[j * D + cc] + pw[8 * D + 16 + j]);
+        }
+        slot[j * (D + 2) + 2 + cc] = O;
+        if (cc == 0) { slot[j * (D + 2)] = Mh[j]; slot[j * (D + 2) + 1] = Mh[8 + j]; }
+      }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      named_bar_sync(1, NCW * 32);
+      if (tid == 0) {
+        const int old = atomicAdd(a.ws_cnt + u, 1);
+        *s_flag = (old == cl - cf);
+      }
+      named_bar_sync(1, NCW * 32);
+      t_e3 = ts ? gtime() : 0;
       if (*s_flag) {
         // last CTA of the unit: log-sum-exp merge of the unit's CTA partials.
         // (m, l) of every partial -> per-partial weights in shared memory (reusing
         // the merge-tree buffer), then each thread sums its output columns.
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         const int np = cl - cf + 1;
         float *wgt = ep;                              // [np][8] weights, then [8] M, [8] L
         float *Ms = ep + (size_t)np * 8, *Ls = Ms + 8;
+        // (m, l) of all partials in one parallel round trip
+        for (int t = tid; t < np * 8; t += NCW * 32) {
+          const int c2 = t >> 3, j = t & 7;
+          float mv = -INFINITY, lv = 0.f;
+          if (j < a.grp) {
+            const float *sp = a.ws_part + (int64_t)(cf + c2 + u) * a.grp * (D + 2) + j * (D + 2);
+            mv = __ldcg(sp);
+            lv = __ldcg(sp + 1);
+          }
+          wgt[t] = mv;
+          Ls[8 + t] = lv;                               // scratch: l of partial c2, head j
+        }
+        named_bar_sync(1, NCW * 32);
         if (tid < a.grp) {
           const int j = tid;
           float M = -INFINITY;
-          for (int c2 = 0; c2 < np; c2++)
-            M = fmaxf(M, __ldcg(a.ws_part + (int64_t)(cf + c2 + u) * a.grp * (D + 2) + j * (D + 2)));
+          for (int c2 = 0; c2 < np; c2++) M = fmaxf(M, wgt[c2 * 8 + j]);
           float L = 0.f;
           for (int c2 = 0; c2 < np; c2++) {
-            const float *sp = a.ws_part + (int64_t)(cf + c2 + u) * a.grp * (D + 2) + j * (D + 2);
-            const float f = (M == -INFINITY) ? 0.f : exp2f(__ldcg(sp) - M);
+            const float f = (M == -INFINITY) ? 0.f : exp2f(wgt[c2 * 8 + j] - M);
             wgt[c2 * 8 + j] = f;
-            L += f * __ldcg(sp + 1);
+            L += f * Ls[8 + c2 * 8 + j];
           }
           Ms[j] = M;
           Ls[j] = L;
@@ -767,7 +848,12 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       }
       named_bar_sync(1, NCW * 32);
     }
-    if (ts && tid == 0) { ts[4] = gtime(); ts[5] = (uint64_t)seq_base; }
+    if (tid == 0) atomicAdd(units_done, 1);
+    if (ts && tid == 0) {
+      const uint64_t t_e4 = gtime();
+      ts[68] += t_e1 - t_e0; ts[69] += t_e2 - t_e1; ts[70] += t_e3 - t_e2; ts[71] += t_e4 - t_e3;
+    }
+    if (ts && tid == 0) { ts[4] = gtime(); ts[5] += (uint64_t)n_u; }
     if (ts) t_ep += gtime() - t_e0;
   }
   if (ts && lane == 0) {

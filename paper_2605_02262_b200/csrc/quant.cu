@@ -50,6 +50,18 @@ struct QuantArgs {
   uint8_t *packed;
 };
 
+// 16-byte unit ui of a code tile, word e -> (lane, word in the lane's chunk) (D-1:
+// chunks of >= 16 bytes are interleaved in 16-byte groups, 8-byte chunks are linear)
+WQ_DEV void unit_lane_word(int ui, int e, int chunk_words, int &L, int &wl) {
+  if (chunk_words >= 4) {
+    L = ui & 31;
+    wl = 4 * (ui >> 5) + e;
+  } else {
+    L = 2 * ui + (e >> 1);
+    wl = e & 1;
+  }
+}
+
 // Q17 on one element: clamp(rint(fl(fl(x - mn) * r)), 0, qmax)
 WQ_DEV uint32_t q17_code(float x, float mn, float r, int qmax) {
   float prod = __fmul_rn(__fsub_rn(x, mn), r);
@@ -113,18 +125,18 @@ __global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
   if (bits == 16) {
     // FP16 window: values re-laid in fragment order (pairs of adjacent columns).
     // word index u over K tiles then V tiles: tile i, lane L, pair P = word in lane chunk
-    constexpr int WORDS = S * D / 2;                         // per tensor
+    constexpr int UPT = 32 * D / 16;                         // 16-byte units per tile
+    constexpr int UNITS = (S / 16) * UPT;                    // per tensor
     uint4 *dst = reinterpret_cast<uint4 *>(rec);
-    for (int u4 = tid; u4 < 2 * WORDS / 4; u4 += QT) {
+    for (int u4 = tid; u4 < 2 * UNITS; u4 += QT) {
+      const int isv = u4 >= UNITS;
+      const int uu = isv ? u4 - UNITS : u4;
+      const int tile = uu / UPT, ui = uu % UPT;
       uint32_t wv[4];
 #pragma unroll
       for (int e = 0; e < 4; e++) {
-        int word = u4 * 4 + e;
-        int isv = word >= WORDS;
-        int wi = isv ? word - WORDS : word;
-        int tile = wi / (16 * D / 2);
-        int inw = wi % (16 * D / 2);
-        int L = inw / (D / 4), P = inw % (D / 4);
+        int L, P;
+        unit_lane_word(ui, e, D / 4, L, P);
         int g = L >> 2, q = L & 3, m = P >> 2, r = P & 3;
         if (!isv) {
           int row = tile * 16 + g + 8 * (r & 1), col = 16 * m + 2 * q + 8 * (r >> 1);
@@ -214,20 +226,19 @@ __global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
 
   // ---- codes in fragment order, 16 bytes (4 words) per thread-iteration ----
   const int ppw = 16 / bits;                  // pairs per word
-  const int words_per_lane = D * bits / 64;   // (D/4 pairs) / ppw
-  const int words_per_tile = 32 * words_per_lane;
-  const int words_per_tensor = (S / 16) * words_per_tile;
+  const int chunk_words = D * bits / 64;      // (D/4 pairs) / ppw
+  const int upt = 2 * D * bits / 16;          // 16-byte units per tile
+  const int units = (S / 16) * upt;           // per tensor
   uint4 *dst = reinterpret_cast<uint4 *>(rec);
-  for (int u4 = tid; u4 < 2 * words_per_tensor / 4; u4 += QT) {
+  for (int u4 = tid; u4 < 2 * units; u4 += QT) {
+    const int isv = u4 >= units;
+    const int uu = isv ? u4 - units : u4;
+    const int tile = uu / upt, ui = uu % upt;
     uint32_t wv[4];
 #pragma unroll
     for (int e4 = 0; e4 < 4; e4++) {
-      int word = u4 * 4 + e4;
-      int isv = word >= words_per_tensor;
-      int wi = isv ? word - words_per_tensor : word;
-      int tile = wi / words_per_tile;
-      int inw = wi % words_per_tile;
-      int L = inw / words_per_lane, wl = inw % words_per_lane;
+      int L, wl;
+      unit_lane_word(ui, e4, chunk_words, L, wl);
       int g = L >> 2, q = L & 3;
       uint32_t acc = 0;
       for (int j = 0; j < ppw; j++) {

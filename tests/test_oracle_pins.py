@@ -573,3 +573,15 @@ def test_merge_identity_and_split(orc):
                                     want_partial=True)
         parts.append(p)
     assert np.max(np.abs(orc.merge(np.stack(parts)) - full)) < 1e-12
+
+
+def test_code_layout_interleaved_groups(orc):
+    """D-1 interleaving: d=128, b=4 -> 32-byte lane chunks stored as 16-byte groups
+    across lanes.  K element (t=0, c=32): m=2, r=0, lane 0 -> pair P=8, word 2
+    (4 pairs/word), so group 0, byte 0*512 + 0*16 + 2*4 = 8.  K element (t=1, c=64):
+    g=1 -> lane 4, m=4 -> P=16 -> word 4 -> group 1: byte 512 + 4*16 + 0 = 576."""
+    assert orc.code_pos(0, 128, 4, 0, 32) == (8, 0)
+    assert orc.code_pos(0, 128, 4, 1, 64) == (576, 0)
+    # 8-byte chunks (d=64, b=2) stay lane-linear: K (t=1, c=18): g=1, m=1, q=1, r=0
+    # -> lane 5, P=4 -> word 0, slot 4 -> byte 5*8 = 40, bit 8
+    assert orc.code_pos(0, 64, 2, 1, 18) == (40, 8)

@@ -24,10 +24,14 @@ for it in range(3):
     print("event us", e0.elapsed_time(e1) * 1e3)
 nsm = torch.cuda.get_device_properties(0).multi_processor_count
 tsb = ws[-nsm * 576:].view(torch.int64).view(nsm, 72).cpu().numpy()
-wt = tsb[:, 8:68].reshape(nsm, 15, 4) / 1e3
+NW = 11
+wt = tsb[:, 8:8 + 4 * NW].reshape(nsm, NW, 4) / 1e3
+kt = tsb[:, 56:61].sum(0) / 1e3; kc = tsb[:, 61:66].sum(0)
+print("per-kind compute us per item (2,4,8,16,rest):", np.round(kt / np.maximum(kc, 1), 3), "counts", kc)
+epi = tsb[:, 68:72] / 1e3
 slow = np.argsort(-(tsb[:, 4] - tsb[:, 0]))[:4]
 for cidx in list(slow) + [int(np.argsort(tsb[:, 4] - tsb[:, 0])[0])]:
-    print("CTA", cidx, "dur us", (tsb[cidx, 4] - tsb[cidx, 0]) / 1e3, "items", tsb[cidx, 5], "per-warp (tag, full, comp, ep):", np.round(wt[cidx, :, :], 1).tolist()[:4])
+    print("CTA", cidx, "dur us", (tsb[cidx, 4] - tsb[cidx, 0]) / 1e3, "items", tsb[cidx, 5], "per-warp (tag, full, comp, ep):", np.round(wt[cidx, :, :], 1).tolist()[:2], "epi (barrier, tree, ticket, merge):", np.round(epi[cidx], 1))
 print("mean over warps/CTAs:", np.round(wt.mean((0, 1)), 2), "max:", np.round(wt.max((0, 1)), 2))
 t0 = tsb[:, 0].min()
 r = (tsb[:, :5] - t0) / 1e3
