@@ -198,7 +198,7 @@ wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t s
  * online softmax with a log-sum-exp merge (Q24).
  * q: fp16 [B][Hq][d] contiguous.  packed/offs/seg_off_l: as produced above.
  * k_rest, v_rest: fp16, element (b, h, t, c) at x[b*rest_strides[0] + h*rest_strides[1] + t*d + c];
- *   rest_len: i32 [B] (device), each in [0, R_max].
+ *   rest_len: i32 [B] (device), each in [0, R_max] (values outside are clamped).
  * out: fp16 [B][Hq][d] (may be NULL).  partial: fp32 [B][Hq][d+2] =
  *   (m, l, o[d]) with m = max logit, l = sum exp(logit - m), o = sum exp(logit - m) v
  *   (unnormalized; m = -inf, l = 0 for an empty cache), may be NULL.

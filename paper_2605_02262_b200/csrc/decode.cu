@@ -75,6 +75,7 @@ WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
   }
   g.nslots = g.so[4];
   g.rl = a.rest_len ? a.rest_len[g.b] : 0;
+  g.rl = g.rl < 0 ? 0 : (g.rl > a.R_max ? a.R_max : g.rl);     // defensive: rest_len <= R_max
   g.ntiles = (g.rl + 15) / 16;
 }
 // Fixed per-unit costs: the unit epilogue (warp merge tree + CTA partial + ticket)

@@ -62,64 +62,84 @@ WQ_DEV void unit_lane_word(int ui, int e, int chunk_words, int &L, int &wl) {
   }
 }
 
-// Q17 on one element: clamp(rint(fl(fl(x - mn) * r)), 0, qmax)
-WQ_DEV uint32_t q17_code(float x, float mn, float r, int qmax) {
+// Q17 on one element: clamp(rint(fl(fl(x - mn) * r)), 0, qmax).  prod >= +0 (x >= mn,
+// r > 0); clamping the float to qmax before rounding gives the same integer as
+// clamping after it, and adding 1.5*2^23 rounds to nearest-even exactly like
+// cvt.rni for |prod| < 2^22 -- the code is then the low mantissa bits.
+WQ_DEV uint32_t q17_code(float x, float mn, float r, float qmaxf) {
   float prod = __fmul_rn(__fsub_rn(x, mn), r);
-  int c = __float2int_rn(prod);
-  c = c < 0 ? 0 : c;
-  c = c > qmax ? qmax : c;
-  return (uint32_t)c;
+  prod = fminf(prod, qmaxf);
+  const float big = __fadd_rn(prod, 12582912.0f);
+  return __float_as_uint(big) & 0xFFu;
 }
 
-template <int D, int S>
-__global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  __half *Ks = reinterpret_cast<__half *>(sm);              // [S][D]
-  __half *Vs = Ks + S * D;                                   // [S][D]
-  float *kmn = reinterpret_cast<float *>(Vs + S * D);        // [D]
-  float *kr = kmn + D;                                       // [D]
-  float *vmn = kr + D;                                       // [S]
-  float *vr = vmn + S;                                       // [S]
-  __half2 *red = reinterpret_cast<__half2 *>(vr + S);        // [QT] x (min2, max2)
-  uint8_t *params = reinterpret_cast<uint8_t *>(red + 2 * QT);  // [4D + 4S]
-  __shared__ uint64_t bar;
-
-  const int slot = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int32_t *so = a.seg_off + 5 * b;
-  if (slot >= so[4]) return;
-  int cls = 0;
-  while (slot >= so[cls + 1]) cls++;
-  const int bits = class_bits(cls);
-  int64_t roff = a.offs[(int64_t)b * a.H + h];
-  for (int k = 0; k < cls; k++) roff += (int64_t)(so[k + 1] - so[k]) * record_bytes(class_bits(k), D, S);
-  roff += (int64_t)(slot - so[cls]) * record_bytes(bits, D, S);
-  uint8_t *rec = a.packed + roff;
-  const int w = a.perm[(int64_t)b * a.perm_stride + slot];
-  const __half *K0 = a.k + b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
-  const __half *V0 = a.v + b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
-  const int tid = threadIdx.x;
-
-  // ---- stage the window (TMA bulk copies) ----
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    constexpr uint32_t ROW = D * 2;
-    mbar_arrive_expect_tx(&bar, 2u * S * ROW);
-    uint64_t pol = policy_evict_first();
-    if (a.st == D) {
-      bulk_g2s_evict_first(Ks, K0, S * ROW, &bar, pol);
-      bulk_g2s_evict_first(Vs, V0, S * ROW, &bar, pol);
-    } else {
-      for (int t = 0; t < S; t++) {
-        bulk_g2s_evict_first(Ks + t * D, K0 + t * a.st, ROW, &bar, pol);
-        bulk_g2s_evict_first(Vs + t * D, V0 + t * a.st, ROW, &bar, pol);
+// Codes of one window in D-1 fragment order: 16-byte units, thread-strided.  For
+// each unit the lane L and its chunk words follow D-1 (unit_lane_word); every pair
+// is two Q17 codes of adjacent columns (K) / adjacent tokens (V).
+template <int D, int S, int BITS>
+WQ_DEV void pack_codes(const __half *Ks, const __half *Vs, const float2 *kp2, const float2 *vp2,
+                       uint4 *dst, int tid) {
+  constexpr int PPW = 16 / BITS;
+  constexpr int CW = D * BITS / 64;           // chunk words per lane
+  constexpr int UPT = 2 * D * BITS / 16;      // 16-byte units per tile
+  constexpr int UNITS = (S / 16) * UPT;       // per tensor
+  constexpr float QMAX = (float)((1 << BITS) - 1);
+  constexpr uint32_t MASK = (1u << BITS) - 1u;
+  // K: rows = tokens, cols = channels
+  for (int u = tid; u < UNITS; u += QT) {
+    const int tile = u / UPT, ui = u % UPT;
+    uint32_t wv[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      int L, wl;
+      unit_lane_word(ui, e, CW, L, wl);
+      const int g = L >> 2, q = L & 3;
+      const __half *kb = Ks + (tile * 16 + g) * D + 2 * q;
+      uint32_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < PPW; j++) {
+        const int P = wl * PPW + j, m = P >> 2, r = P & 3;
+        const int col = 16 * m + 8 * (r >> 1);
+        const float2 x = __half22float2(*reinterpret_cast<const __half2 *>(kb + 8 * (r & 1) * D + col));
+        const float4 pr = *reinterpret_cast<const float4 *>(kp2 + col + 2 * q);
+        const uint32_t c0 = q17_code(x.x, pr.x, pr.y, QMAX) & MASK;
+        const uint32_t c1 = q17_code(x.y, pr.z, pr.w, QMAX) & MASK;
+        acc |= (c0 << (BITS * j)) | (c1 << (16 + BITS * j));
       }
+      wv[e] = acc;
     }
+    dst[u] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
   }
-  mbar_wait(&bar, 0);
+  // V: rows = channels, cols = tokens
+  uint4 *vdst = dst + UNITS;
+  for (int u = tid; u < UNITS; u += QT) {
+    const int tile = u / UPT, ui = u % UPT;
+    uint32_t wv[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      int L, wl;
+      unit_lane_word(ui, e, CW, L, wl);
+      const int g = L >> 2, q = L & 3;
+      uint32_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < PPW; j++) {
+        const int P = wl * PPW + j, m = P >> 2, r = P & 3;
+        const int ch = 16 * m + g + 8 * (r & 1), t = tile * 16 + 2 * q + 8 * (r >> 1);
+        const float4 pr = *reinterpret_cast<const float4 *>(vp2 + t);     // {mn, r} of t, t+1
+        const uint32_t c0 = q17_code(__half2float(Vs[t * D + ch]), pr.x, pr.y, QMAX) & MASK;
+        const uint32_t c1 = q17_code(__half2float(Vs[(t + 1) * D + ch]), pr.z, pr.w, QMAX) & MASK;
+        acc |= (c0 << (BITS * j)) | (c1 << (16 + BITS * j));
+      }
+      wv[e] = acc;
+    }
+    vdst[u] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
+}
+
+// Quantize + pack one staged window (K, V rows in shared memory) into rec.
+template <int D, int S>
+WQ_DEV void quant_window(const __half *Ks, const __half *Vs, float2 *kp2, float2 *vp2, __half2 *red,
+                         uint8_t *params, uint8_t *rec, int bits, int tid) {
 
   const int64_t code_bytes = (int64_t)S * D * bits / 8;      // one of K or V
   if (bits == 16) {
@@ -182,8 +202,7 @@ __global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
         float mx = __half2float(e ? __high2half(mx2) : __low2half(mx2));
         __half s16 = __float2half_ru(__fdiv_rn(__fsub_rn(mx, mn), qmaxf));
         if (__half2float(s16) < 5.9604644775390625e-08f) s16 = __ushort_as_half(0x0001);
-        kmn[c] = mn;
-        kr[c] = __frcp_rn(__half2float(s16));
+        kp2[c] = make_float2(mn, __frcp_rn(__half2float(s16)));
         int m = c / 16, q = (c % 8) / 2, hh = (c % 16) / 8;
         __half *grp = reinterpret_cast<__half *>(params + (q * (D / 16) + m) * 16);
         grp[2 * hh + e] = s16;
@@ -214,8 +233,7 @@ __global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
       float mnf = __half2float(mn), mxf = __half2float(mx);
       __half s16 = __float2half_ru(__fdiv_rn(__fsub_rn(mxf, mnf), qmaxf));
       if (__half2float(s16) < 5.9604644775390625e-08f) s16 = __ushort_as_half(0x0001);
-      vmn[t] = mnf;
-      vr[t] = __frcp_rn(__half2float(s16));
+      vp2[t] = make_float2(mnf, __frcp_rn(__half2float(s16)));
       int i = t / 16, col = t % 16, q = (col % 8) / 2, hh = col / 8, e = col % 2;
       __half *grp = reinterpret_cast<__half *>(params + 4 * D + (4 * i + q) * 16);
       grp[2 * hh + e] = s16;
@@ -224,41 +242,12 @@ __global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
   }
   __syncthreads();
 
-  // ---- codes in fragment order, 16 bytes (4 words) per thread-iteration ----
-  const int ppw = 16 / bits;                  // pairs per word
-  const int chunk_words = D * bits / 64;      // (D/4 pairs) / ppw
-  const int upt = 2 * D * bits / 16;          // 16-byte units per tile
-  const int units = (S / 16) * upt;           // per tensor
+  // ---- codes in fragment order (templated per width: unrolled, constant shifts) ----
   uint4 *dst = reinterpret_cast<uint4 *>(rec);
-  for (int u4 = tid; u4 < 2 * units; u4 += QT) {
-    const int isv = u4 >= units;
-    const int uu = isv ? u4 - units : u4;
-    const int tile = uu / upt, ui = uu % upt;
-    uint32_t wv[4];
-#pragma unroll
-    for (int e4 = 0; e4 < 4; e4++) {
-      int L, wl;
-      unit_lane_word(ui, e4, chunk_words, L, wl);
-      int g = L >> 2, q = L & 3;
-      uint32_t acc = 0;
-      for (int j = 0; j < ppw; j++) {
-        int P = wl * ppw + j, m = P >> 2, r = P & 3;
-        uint32_t c0, c1;
-        if (!isv) {
-          int row = tile * 16 + g + 8 * (r & 1), col = 16 * m + 2 * q + 8 * (r >> 1);
-          __half2 x = *reinterpret_cast<const __half2 *>(Ks + row * D + col);
-          c0 = q17_code(__low2float(x), kmn[col], kr[col], qmax);
-          c1 = q17_code(__high2float(x), kmn[col + 1], kr[col + 1], qmax);
-        } else {
-          int ch = 16 * m + g + 8 * (r & 1), t = tile * 16 + 2 * q + 8 * (r >> 1);
-          c0 = q17_code(__half2float(Vs[t * D + ch]), vmn[t], vr[t], qmax);
-          c1 = q17_code(__half2float(Vs[(t + 1) * D + ch]), vmn[t + 1], vr[t + 1], qmax);
-        }
-        acc |= (c0 << (bits * j)) | (c1 << (16 + bits * j));
-      }
-      wv[e4] = acc;
-    }
-    dst[u4] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  switch (bits) {
+    case 2: pack_codes<D, S, 2>(Ks, Vs, kp2, vp2, dst, tid); break;
+    case 4: pack_codes<D, S, 4>(Ks, Vs, kp2, vp2, dst, tid); break;
+    default: pack_codes<D, S, 8>(Ks, Vs, kp2, vp2, dst, tid); break;
   }
   // ---- params (K then V) after the codes ----
   uint4 *pdst = reinterpret_cast<uint4 *>(rec + 2 * code_bytes);
@@ -266,19 +255,106 @@ __global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
   for (int i = tid; i < (4 * D + 4 * S) / 16; i += QT) pdst[i] = psrc[i];
 }
 
+// Persistent kernel: each CTA walks windows blockIdx.x, +gridDim.x, ... of the
+// flattened (request, kv head, slot) space with an NSTG-deep TMA ring, so the
+// next windows stream in while the current one is quantized.
 template <int D, int S>
-static size_t quant_smem() {
-  return (size_t)2 * S * D * 2 + (2 * D + 2 * S) * 4 + 2 * QT * 4 + 4 * D + 4 * S;
+struct QuantSmem {
+  static constexpr int WIN = 4 * S * D;                     // K + V bytes of one window
+  static constexpr int NSTG = WIN >= 65536 ? 2 : 3;
+  static constexpr size_t ring = (size_t)NSTG * WIN;
+  static constexpr size_t total = ring + (2 * D + 2 * S) * 8 + 2 * QT * 4 + 4 * D + 4 * S + 64;
+};
+
+template <int D, int S>
+__global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
+  using QS = QuantSmem<D, S>;
+  constexpr int NSTG = QS::NSTG;
+  extern __shared__ __align__(128) uint8_t sm[];
+  float2 *kp2 = reinterpret_cast<float2 *>(sm + QS::ring);  // [D] {mn, 1/s} per channel
+  float2 *vp2 = kp2 + D;                                     // [S] {mn, 1/s} per token
+  __half2 *red = reinterpret_cast<__half2 *>(vp2 + S);       // [QT] x (min2, max2)
+  uint8_t *params = reinterpret_cast<uint8_t *>(red + 2 * QT);  // [4D + 4S]
+  __shared__ uint64_t bar[NSTG];
+  const int tid = threadIdx.x;
+  const int total = a.B * a.H * a.perm_stride;
+
+  // window k of this CTA -> (b, h, slot); valid if slot < seg_off[b][4]
+  auto locate = [&](int k, int &b, int &h, int &slot) -> bool {
+    const int idx = blockIdx.x + k * gridDim.x;
+    if (idx >= total) return false;
+    slot = idx % a.perm_stride;
+    const int bh = idx / a.perm_stride;
+    h = bh % a.H;
+    b = bh / a.H;
+    return true;
+  };
+  auto issue = [&](int k) {                       // thread 0: TMA of window k into its stage
+    int b, h, slot;
+    if (!locate(k, b, h, slot)) return;
+    if (slot >= a.seg_off[5 * b + 4]) {           // no window: complete the phase anyway
+      mbar_arrive(&bar[k % NSTG]);
+      return;
+    }
+    const int w = a.perm[(int64_t)b * a.perm_stride + slot];
+    const __half *K0 = a.k + b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
+    const __half *V0 = a.v + b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
+    __half *Ks = reinterpret_cast<__half *>(sm + (size_t)(k % NSTG) * QS::WIN);
+    __half *Vs = Ks + S * D;
+    uint64_t *bb = &bar[k % NSTG];
+    constexpr uint32_t ROW = D * 2;
+    mbar_arrive_expect_tx(bb, 2u * S * ROW);
+    const uint64_t pol = policy_evict_first();
+    if (a.st == D) {
+      bulk_g2s_evict_first(Ks, K0, S * ROW, bb, pol);
+      bulk_g2s_evict_first(Vs, V0, S * ROW, bb, pol);
+    } else {
+      for (int t = 0; t < S; t++) {
+        bulk_g2s_evict_first(Ks + t * D, K0 + t * a.st, ROW, bb, pol);
+        bulk_g2s_evict_first(Vs + t * D, V0 + t * a.st, ROW, bb, pol);
+      }
+    }
+  };
+  if (tid == 0) {
+    for (int i = 0; i < NSTG; i++) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+    for (int k = 0; k < NSTG - 1; k++) issue(k);
+  }
+  __syncthreads();
+  for (int k = 0;; k++) {
+    int b, h, slot;
+    if (!locate(k, b, h, slot)) break;
+    if (tid == 0) issue(k + NSTG - 1);            // its stage was released by the last barrier
+    const int32_t *so = a.seg_off + 5 * b;
+    if (slot < so[4]) {
+      int cls = 0;
+      while (slot >= so[cls + 1]) cls++;
+      const int bits = class_bits(cls);
+      int64_t roff = a.offs[(int64_t)b * a.H + h];
+      for (int kk = 0; kk < cls; kk++) roff += (int64_t)(so[kk + 1] - so[kk]) * record_bytes(class_bits(kk), D, S);
+      roff += (int64_t)(slot - so[cls]) * record_bytes(bits, D, S);
+      mbar_wait(&bar[k % NSTG], (uint32_t)(k / NSTG) & 1u);
+      const __half *Ks = reinterpret_cast<const __half *>(sm + (size_t)(k % NSTG) * QS::WIN);
+      quant_window<D, S>(Ks, Ks + S * D, kp2, vp2, red, params, a.packed + roff, bits, tid);
+    }
+    __syncthreads();
+  }
 }
 
 template <int D, int S>
-static cudaError_t launch_quant_t(const QuantArgs &a, int max_slots, cudaStream_t st) {
-  size_t smem = quant_smem<D, S>();
-  cudaError_t e = cudaFuncSetAttribute(k_quant<D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+static cudaError_t launch_quant_t(const QuantArgs &a, cudaStream_t st) {
+  using QS = QuantSmem<D, S>;
+  const size_t smem = QS::total;
+  cudaError_t e = cudaFuncSetAttribute(k_quant<D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(max_slots, a.H, a.B);
-  k_quant<D, S><<<grid, QT, smem, st>>>(a);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quant<D, S>, QT, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t total = (int64_t)a.B * a.H * a.perm_stride;
+  int64_t grid = (int64_t)device_sm_count() * per_sm;
+  if (grid > total) grid = total;
+  if (grid < 1) grid = 1;
+  k_quant<D, S><<<(unsigned)grid, QT, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -301,6 +377,7 @@ __global__ void k_shard_slots(const int32_t *__restrict__ perm, const int32_t *_
   if (threadIdx.x < 5) seg_r[5 * b + threadIdx.x] = start[threadIdx.x];
 }
 
+
 cudaError_t launch_shard_slots(const int32_t *perm, const int32_t *seg, int B, int W, int G, int r,
                                int32_t *perm_r, int32_t *seg_r, cudaStream_t st) {
   k_shard_slots<<<B, 256, 0, st>>>(perm, seg, W, G, r, perm_r, seg_r);
@@ -319,9 +396,8 @@ cudaError_t launch_quant(const __half *k, const __half *v, const int64_t strides
                          cudaStream_t st) {
   QuantArgs a{k, v, strides[0], strides[1], strides[2], vis_off, B, H, d, S, perm, perm_stride,
               seg_off, offs, packed};
-  int ms = perm_stride;
 #define WQ_Q(DD, SS) \
-  if (d == DD && S == SS) return launch_quant_t<DD, SS>(a, ms, st);
+  if (d == DD && S == SS) return launch_quant_t<DD, SS>(a, st);
   WQ_Q(64, 16) WQ_Q(64, 32) WQ_Q(64, 64) WQ_Q(64, 128)
   WQ_Q(128, 16) WQ_Q(128, 32) WQ_Q(128, 64) WQ_Q(128, 128)
 #undef WQ_Q
