@@ -241,7 +241,7 @@ def decode_attention(q, packed, offs, seg_off_l, perm_l, g: Geom, k_rest, v_rest
     q, k_rest, v_rest = _u16(q), _u16(k_rest), _u16(v_rest)
     B, H, R, d = k_rest.shape
     rs = np.array([H * R * d, R * d], np.int64)
-    rest_len = np.ascontiguousarray(rest_len, np.int32)
+    rest_len = np.clip(np.ascontiguousarray(rest_len, np.int32), 0, R)   # contract: clamped to R_max
     perm_l = np.ascontiguousarray(perm_l, np.int32)
     seg_off_l = np.ascontiguousarray(seg_off_l, np.int32)
     out = np.zeros((g.B, g.Hq, g.d), np.float64)
