@@ -9,7 +9,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "lib", "libwq.so")
+# Experiment builds: WQ_VARIANT=<name> WQ_NVCC_DEFS="-DX=1 ..." build and load lib/<name>/libwq.so
+# (the same sources with extra defines); unset, the product library lib/libwq.so.
+VARIANT = os.environ.get("WQ_VARIANT", "")
+EXTRA_DEFS = os.environ.get("WQ_NVCC_DEFS", "").split()
+LIBDIR = os.path.join(HERE, "lib", VARIANT) if VARIANT else os.path.join(HERE, "lib")
+LIB = os.path.join(LIBDIR, "libwq.so")
 SOURCES = ["abi.cu", "scores.cu", "assign.cu", "quant.cu", "decode.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -37,13 +42,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    objdir = os.path.join(HERE, "lib", "obj")
+    objdir = os.path.join(LIBDIR, "obj")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, f'-DWQ_BUILD_ID="{_build_id()}"', "-I", os.path.join(ROOT, "include"),
+        cmd = [NVCC, *ARCH, *FLAGS, f'-DWQ_BUILD_ID="{_build_id()}"', *EXTRA_DEFS, "-I", os.path.join(ROOT, "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
@@ -57,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
     os.replace(tmp, LIB)
-    with open(os.path.join(HERE, "lib", "ptxas.log"), "w") as f:
+    with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))

@@ -38,17 +38,41 @@ constexpr int NCW = WQ_DEC_NCW;                 // consumer warps
 constexpr int DT = (NCW + 1) * 32;      // threads per CTA
 constexpr int MAX_UNITS = 1024;         // B * H
 constexpr int64_t MIN_CTA_BYTES = 49152;
+#ifndef WQ_DEC_QLO
+#define WQ_DEC_QLO 1                     // carry q*s as fp16 hi + lo (0: hi only, experiment)
+#endif
 #ifndef WQ_DEC_STAGE
 #define WQ_DEC_STAGE 32768
 #endif
+constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trace
 constexpr float LAZY_TH = 8.0f;         // log2 headroom of the lazy softmax rescale
 constexpr int KIND_REST = 4;
 
-// Geometry of one unit (request b, kv head h).  Work is partitioned across CTAs in
-// COST space, not bytes: every item costs its bytes plus a per-item compute term
-// (a window's dequant + MMA work is nearly independent of its width), so CTAs that
-// get many narrow windows get fewer of them.  kappa ~ bytes the HBM delivers to
-// one SM while it computes one window (0.75 B per element of a quantized window).
+// Compile-time item sizes and costs of a (D, S) instantiation.  Work is partitioned
+// across CTAs in COST space, not bytes: every item costs its bytes plus a per-item
+// compute term (a window's dequant + MMA work is nearly independent of its width),
+// so CTAs that get many narrow windows get fewer of them.
+template <int D, int S>
+struct ItemGeo {
+  // record bytes of class k (0..2 = 2/4/8-bit, 3 = FP16), D-1 contract
+  static constexpr int64_t rb(int k) {
+    return k == 3 ? 4LL * S * D : (int64_t)S * D * (2 << k) / 4 + 4LL * D + 4LL * S;
+  }
+  static constexpr int REST_SZ = 64 * D;               // FP16 rest tile: 16 K rows + 16 V rows
+  static constexpr int sz(int k) { return k == 4 ? REST_SZ : (int)rb(k); }
+  // An SM streams ~49 KB/us of HBM while its NCW consumer warps compute; an item
+  // costs max(its bytes, the bytes the SM could stream during its compute).
+  // Compute-equivalents from measured per-warp item times (tools/dbg_decode_time.py):
+  // quantized window ~1.56*S*D, FP16 window ~0.95*S*D, 16-token rest tile ~35*D.
+  static constexpr int64_t cpe(int k) {
+    return k == 4 ? 35LL * D : (k == 3 ? 95LL * S * D / 100 : 156LL * S * D / 100);
+  }
+  static constexpr int64_t cost(int k) {               // k = 4: one 16-token rest tile
+    return (k == 4 ? (int64_t)REST_SZ : rb(k)) > cpe(k) ? (k == 4 ? (int64_t)REST_SZ : rb(k)) : cpe(k);
+  }
+};
+
+// Geometry of one unit (request b, kv head h).
 struct UnitGeo {
   int b, h, nslots, rl, ntiles;
   int so[5];
@@ -56,113 +80,67 @@ struct UnitGeo {
   int64_t cc[5];                        // cost start of each class segment; cc[4] = windows' cost
 };
 
-WQ_DEV int64_t item_cost(int k, int d, int S) {   // k = 0..3 class, 4 = rest tile
-  if (k == 4) return 64LL * d + 176LL * d;
-  return record_bytes(class_bits(k), d, S) + (k == 3 ? 6LL * S * d : 12LL * S * d);
-}
-
+template <int D, int S>
 WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
+  using IG = ItemGeo<D, S>;
   g.b = u / a.H;
-  g.h = u % a.H;
+  g.h = u - g.b * a.H;
   const int32_t *so = a.seg_off + 5 * g.b;
+#pragma unroll
   for (int k = 0; k < 5; k++) g.so[k] = so[k];
   g.cs[0] = 0;
   g.cc[0] = 0;
+#pragma unroll
   for (int k = 0; k < 4; k++) {
     const int64_t n = g.so[k + 1] - g.so[k];
-    g.cs[k + 1] = g.cs[k] + n * record_bytes(class_bits(k), a.d, a.S);
-    g.cc[k + 1] = g.cc[k] + n * item_cost(k, a.d, a.S);
+    g.cs[k + 1] = g.cs[k] + n * IG::rb(k);
+    g.cc[k + 1] = g.cc[k] + n * IG::cost(k);
   }
   g.nslots = g.so[4];
   g.rl = a.rest_len ? a.rest_len[g.b] : 0;
-  g.rl = g.rl < 0 ? 0 : (g.rl > a.R_max ? a.R_max : g.rl);     // defensive: rest_len <= R_max
+  g.rl = g.rl < 0 ? 0 : (g.rl > a.R_max ? a.R_max : g.rl);     // contract: rest_len clamped to R_max
   g.ntiles = (g.rl + 15) / 16;
 }
-// Fixed per-unit costs: the unit epilogue (warp merge tree + CTA partial + ticket)
-// is charged at the unit's start and the cross-CTA log-sum-exp merge at its end,
-// so a CTA that crosses a unit boundary or finishes a unit gets fewer windows.
-constexpr int64_t COST_UNIT_HEAD = 0;
-constexpr int64_t COST_UNIT_TAIL = 0;
-WQ_DEV int64_t unit_cost(const DecodeArgs &a, const UnitGeo &g) {
-  return COST_UNIT_HEAD + g.cc[4] + (int64_t)g.ntiles * item_cost(4, a.d, a.S) + COST_UNIT_TAIL;
+template <int D, int S>
+WQ_DEV int64_t unit_cost(const UnitGeo &g) {
+  return g.cc[4] + (int64_t)g.ntiles * ItemGeo<D, S>::cost(4);
 }
 
 // first item whose start (in cost units, relative to the unit) is >= x
-WQ_DEV int first_item(const DecodeArgs &a, const UnitGeo &g, int64_t x) {
-  x -= COST_UNIT_HEAD;
+template <int D, int S>
+WQ_DEV int first_item(const UnitGeo &g, int64_t x) {
+  using IG = ItemGeo<D, S>;
   if (x <= 0) return 0;
+#pragma unroll
   for (int k = 0; k < 4; k++) {
     if (x <= g.cc[k]) return g.so[k];
-    if (x < g.cc[k + 1]) {
-      const int64_t c = item_cost(k, a.d, a.S);
-      return g.so[k] + (int)((x - g.cc[k] + c - 1) / c);
-    }
+    if (x < g.cc[k + 1]) return g.so[k] + (int)((x - g.cc[k] + IG::cost(k) - 1) / IG::cost(k));
   }
   if (x <= g.cc[4]) return g.nslots;
-  const int64_t tc = item_cost(4, a.d, a.S);
-  const int64_t t = (x - g.cc[4] + tc - 1) / tc;
+  const int64_t t = (x - g.cc[4] + IG::cost(4) - 1) / IG::cost(4);
   return g.nslots + (int)(t < g.ntiles ? t : g.ntiles);
 }
 
 // Stage plan of one unit's item range [i0, i1): five "pieces" (the width-class
-// segments 2|4|8|16 and the FP16 rest tiles), each cut into stages of cap
-// equal-size items.  Producer and consumers evaluate the same arithmetic, so no
-// per-item descriptors are exchanged.
+// segments 2|4|8|16 and the FP16 rest tiles), each cut into stages of CAP(p)
+// equal-size items.  Producer and consumers walk the same plan.
 struct UnitPlan {
-  int lo[5], hi[5], cap[5], nst[5];
-  int sz[5];
+  int lo[5], hi[5], nst[5];
 };
-// The unit the consumers work on, published in shared memory by warp 0 (keeps
-// the plan out of the per-thread registers of the window loop).
-struct UnitSm {
-  int u, n_u, sg_base, rl, nslots, tag;
-  int len[5], nst[5], cap[5], lo[5], sz[5];
-  float rcap[5];                        // 1 / cap (exact integer division for idx < 2^20)
-  int c0, c1;                           // CTAs sharing this unit
-};
-
-template <int STAGE>
-WQ_DEV void plan_unit(const DecodeArgs &a, const UnitGeo &g, int i0, int i1, UnitPlan &pl) {
+template <int D, int S, int STAGE>
+WQ_DEV void plan_unit(const UnitGeo &g, int i0, int i1, UnitPlan &pl) {
+  using IG = ItemGeo<D, S>;
+#pragma unroll
   for (int p = 0; p < 5; p++) {
     const int a0 = p < 4 ? g.so[p] : g.nslots;
     const int a1 = p < 4 ? g.so[p + 1] : g.nslots + g.ntiles;
     const int lo = i0 > a0 ? i0 : a0;
     const int hi = i1 < a1 ? i1 : a1;
-    const int sz = p < 4 ? (int)record_bytes(class_bits(p), a.d, a.S) : 32 * (2 * a.d + 16);
+    const int cap = STAGE / IG::sz(p);
     pl.lo[p] = lo;
     pl.hi[p] = hi > lo ? hi : lo;
-    pl.sz[p] = sz;
-    pl.cap[p] = STAGE / sz;
-    pl.nst[p] = (pl.hi[p] - pl.lo[p] + pl.cap[p] - 1) / pl.cap[p];
+    pl.nst[p] = (pl.hi[p] - pl.lo[p] + cap - 1) / cap;
   }
-}
-
-WQ_DEV int64_t cta_lo(int c, int G, int64_t T) { return (int64_t)c * T / G; }
-
-// CTAs [c0, c1) that share unit u.  With at least as many units as CTAs, whole
-// units go to the CTA owning their cost midpoint (no cross-CTA merge); with fewer
-// units, every unit gets 1 + its cost share of the remaining CTAs, so no CTA
-// ever spans two split units (one epilogue per CTA).
-WQ_DEV void unit_ctas(int u, int U, int G, int64_t T, const int64_t *ustart, int &c0, int &c1) {
-  if (T <= 0) { c0 = 0; c1 = 1; return; }
-  if (U >= G) {
-    const int64_t mid = ustart[u] + (ustart[u + 1] - ustart[u]) / 2;
-    c0 = (int)((mid * G) / T);
-    if (c0 >= G) c0 = G - 1;
-    c1 = c0 + 1;
-  } else {
-    const int64_t extra = G - U;
-    c0 = u + (int)((ustart[u] * extra + T / 2) / T);
-    c1 = (u + 1 < U) ? (u + 1) + (int)((ustart[u + 1] * extra + T / 2) / T) : G;
-  }
-}
-WQ_DEV int owner_of(int64_t x, int G, int64_t T) {
-  if (T <= 0) return 0;
-  int c = (int)((x * G) / T);
-  if (c >= G) c = G - 1;
-  while (c + 1 < G && cta_lo(c + 1, G, T) <= x) c++;
-  while (c > 0 && cta_lo(c, G, T) > x) c--;
-  return c;
 }
 
 struct WarpState {
@@ -317,7 +295,7 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
       for (int i = 0; i < 4; i++) { ah[t][i] = 0.f; al[t][i] = 0.f; }
 #pragma unroll
     for (int kt = 0; kt < KT; kt++) {
-      uint32_t h0, h1, l0, l1;
+      uint32_t h0 = 0, h1 = 0, l0 = 0, l1 = 0;
       if constexpr (BITS < 16) {
         const uint4 pr = lds128(kp + (q * KT + kt) * 16);   // {s01, s89, mn01, mn89}
         if (c0 == 0) {
@@ -326,9 +304,11 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
           else mma16816(b0, am, qf[kt][0], qf[kt][1], b0);
         }
         h0 = hmul2u(qf[kt][0], pr.x);
-        l0 = h2u(__hfma2(u2h(qf[kt][0]), u2h(pr.x), __hneg2(u2h(h0))));
         h1 = hmul2u(qf[kt][1], pr.y);
-        l1 = h2u(__hfma2(u2h(qf[kt][1]), u2h(pr.y), __hneg2(u2h(h1))));
+        if constexpr (WQ_DEC_QLO) {
+          l0 = h2u(__hfma2(u2h(qf[kt][0]), u2h(pr.x), __hneg2(u2h(h0))));
+          l1 = h2u(__hfma2(u2h(qf[kt][1]), u2h(pr.y), __hneg2(u2h(h1))));
+        }
       }
 #pragma unroll
       for (int t = 0; t < CH; t++) {
@@ -336,8 +316,13 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
 #pragma unroll
         for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS>(wk[t], 4 * kt + r);
         if constexpr (BITS < 16) {
-          mma16816(ah[t], a, h0, h1, ah[t]);
-          mma16816(al[t], a, l0, l1, al[t]);
+          if constexpr (WQ_DEC_QLO) {
+            mma16816(ah[t], a, h0, h1, ah[t]);
+            mma16816(al[t], a, l0, l1, al[t]);
+          } else {
+            if (kt & 1) mma16816(al[t], a, h0, h1, al[t]);
+            else mma16816(ah[t], a, h0, h1, ah[t]);
+          }
         } else {
           if (kt & 1) mma16816(al[t], a, qf[kt][0], qf[kt][1], al[t]);
           else mma16816(ah[t], a, qf[kt][0], qf[kt][1], ah[t]);
@@ -377,14 +362,15 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
   }
 }
 
-// FP16 rest tile: K rows [16][D] at base, V rows [16][D] after them, rows padded to 2D+16 bytes
+// FP16 rest tile: K rows [16][D] at Kb, V rows [16][D] at Vb (unpadded rows as the
+// bulk copies land them; rows past ntok hold stale bytes and are masked)
 template <int D>
-WQ_DEV void do_rest(const uint8_t *base, int ntok, const uint32_t (&qf)[D / 16][2], float scale2,
+WQ_DEV void do_rest(const uint8_t *Kb, const uint8_t *Vb, int ntok, const uint32_t (&qf)[D / 16][2], float scale2,
                     WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane) {
   constexpr int KT = D / 16;
-  constexpr int RPH = D + 8;                       // padded row stride (halves)
-  const __half *Ks = reinterpret_cast<const __half *>(base);
-  const __half *Vs = Ks + 16 * RPH;
+  constexpr int RPH = D;                           // row stride (halves)
+  const __half *Ks = reinterpret_cast<const __half *>(Kb);
+  const __half *Vs = reinterpret_cast<const __half *>(Vb);
   const int g = lane >> 2, q = lane & 3, mi = lane >> 3, rr = lane & 7;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -418,45 +404,48 @@ WQ_DEV void do_rest(const uint8_t *base, int ntok, const uint32_t (&qf)[D / 16][
 // -------------------------------------------------------------------------------------
 // the kernel
 // -------------------------------------------------------------------------------------
+// A CTA's work is a list of "entries" (unit u, items [i0, i1) of it).  The producer
+// lane publishes each entry's stage plan in a small shared ring and streams its
+// stages; consumers walk the same stages in order and take the items of every
+// stage round-robin (item k of the entry -> warp k % NCW): a static schedule, so
+// the only synchronisation per stage is one full-barrier wait and one
+// empty-barrier arrive per warp (empty counts NCW arrivals).
+struct Entry {
+  int u, n_u, c0, c1, rl, nslots, tag;
+  int lo[5], len[5], nst[5];
+};
+// This CTA's share, planned in the prologue by warp 0 (lane-parallel): units
+// [ua, ub) whole, or one unit split over CTAs [c0, c1) of which this CTA takes
+// items [i0, i1).
+struct CtaPlan {
+  int ua, ub, split, c0, c1, i0, i1;
+};
+
 template <int D, int S>
 struct DecodeSmem {
-  // a stage must hold the largest item (an FP16 window: 4*S*D bytes); small stages
-  // release shared memory item-group by item-group, a deep ring gives lookahead.
+  // a stage must hold the largest item (an FP16 window: 4*S*D bytes)
   static constexpr int STAGE = (4 * S * D > WQ_DEC_STAGE) ? 4 * S * D : WQ_DEC_STAGE;
   static constexpr int RING = WQ_DEC_RING;
   static constexpr int NST = (RING / STAGE) < 2 ? 2 : RING / STAGE;
   static constexpr int KT = D / 16;
   static constexpr int SCRATCH = 2 * 16 * 16;            // P' rows of one 2-tile chunk per warp
-  // epilogue: every warp's o as [8 heads][D] + (m, l, vb)[8]; 1200+ floats reused by
-  // the cross-CTA merge of the last CTA
-  static constexpr int EPW = 8 * D + 24;
-  static constexpr int EP_SLOTS = NCW;
+  static constexpr int EPW = 8 * D + 24;                 // per warp: o [8][D], m[8], l[8], vb[8]
+  static constexpr int NUS = 4;                          // entry ring published by the producer
   static constexpr size_t ring = (size_t)NST * STAGE;
   static constexpr size_t scratch_off = ring;
   static constexpr size_t ep_off = scratch_off + (size_t)NCW * SCRATCH;
-  static constexpr size_t units_off = ep_off + (size_t)EP_SLOTS * EPW * 4;
-  static constexpr size_t cnt_off = units_off + (size_t)(MAX_UNITS + 1) * 8;
-  static constexpr size_t usm_off = (cnt_off + (size_t)(3 * NST + 4) * 4 + 15) / 16 * 16;
-  static constexpr int NUS = 4;                          // unit-plan ring published by the producer
-  static constexpr size_t bar_off = usm_off + NUS * sizeof(UnitSm);
-  static constexpr size_t total = bar_off + 2 * NST * 8 + 16;
+  static constexpr size_t units_off = ep_off + (size_t)NCW * EPW * 4;
+  static constexpr size_t ent_off = units_off + (size_t)(MAX_UNITS + 1) * 8;
+  static constexpr size_t plan_off = ent_off + NUS * sizeof(Entry);
+  static constexpr size_t misc_off = plan_off + sizeof(CtaPlan);
+  static constexpr size_t bar_off = (misc_off + 16 + 15) / 16 * 16;
+  static constexpr size_t total = bar_off + 2 * NST * 8;
 };
 
-WQ_DEV uint64_t gtime() {      // profiling clock: SM cycles scaled to ~ns at 1.965 GHz
-  return (uint64_t)((double)clock64() * (1.0 / 1.965));
-}
-
-WQ_DEV void mbar_wait_sleep(uint64_t *b, uint32_t parity) {
-  uint32_t done = 0;
-  for (;;) {
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-    if (done) return;
-    __nanosleep(64);
-  }
+WQ_DEV uint64_t gtime() {      // profiling clock (debug & 8 only): global ns timer
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 template <int D, int S>
@@ -468,271 +457,264 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint8_t *ring = sm;
   int64_t *ustart = reinterpret_cast<int64_t *>(sm + SM::units_off);
-  int *stage_n = reinterpret_cast<int *>(sm + SM::cnt_off);      // items per stage fill
-  int *stage_done = stage_n + NST;                                // completed items per stage
-  int *stage_fill = stage_done + NST;                             // fill number a slot holds
-  int *claim = stage_fill + NST;                                  // [2] per-unit claim counters
-  int *s_flag = claim + 2;
+  Entry *ent = reinterpret_cast<Entry *>(sm + SM::ent_off);
+  int *s_flag = reinterpret_cast<int *>(sm + SM::misc_off);
   int *units_done = s_flag + 1;
-  UnitSm *usm = reinterpret_cast<UnitSm *>(sm + SM::usm_off);
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + SM::bar_off);
   uint64_t *empty = full + NST;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int U = a.B * a.H;
-  uint64_t *ts = a.ws_ts ? a.ws_ts + (size_t)blockIdx.x * 72 : nullptr;
+  uint64_t *ts = a.ws_ts ? a.ws_ts + (size_t)blockIdx.x * TS_PER_CTA : nullptr;
   if (ts && tid == 0) ts[0] = gtime();
 
-  // ---- unit byte prefix (warp 0) ----
+  // ---- prologue (warp 0): unit cost prefix, then this CTA's share ----
+  CtaPlan *cp = reinterpret_cast<CtaPlan *>(sm + SM::plan_off);
   if (warp == 0) {
     int64_t carry = 0;
     for (int base = 0; base < U; base += 32) {
-      int u = base + lane;
+      const int u = base + lane;
       int64_t v = 0;
       if (u < U) {
         UnitGeo gg;
-        unit_geo(a, u, gg);
-        v = unit_cost(a, gg);
+        unit_geo<D, S>(a, u, gg);
+        v = unit_cost<D, S>(gg);
       }
       int64_t x = v;
+#pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
       if (u < U) ustart[u] = carry + x - v;
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
     if (lane == 0) ustart[U] = carry;
+    __syncwarp();
+    const int64_t T = carry;
+    int G = (int)(T / MIN_CTA_BYTES);
+    G = G < 1 ? 1 : (G > (int)gridDim.x ? (int)gridDim.x : G);
+    const int c = blockIdx.x;
+    if (U >= G || T <= 0) {
+      // whole units to the CTA owning their cost midpoint: a contiguous unit range
+      int ua = 0, ub = 0;
+      for (int base = 0; base < U; base += 32) {
+        const int u = base + lane;
+        int own = G;
+        if (u < U) {
+          const int64_t mid = ustart[u] + (ustart[u + 1] - ustart[u]) / 2;
+          own = T > 0 ? (int)((mid * G) / T) : 0;
+          own = own >= G ? G - 1 : own;
+        }
+        ua += __popc(__ballot_sync(0xffffffffu, own < c));
+        ub += __popc(__ballot_sync(0xffffffffu, own <= c));
+      }
+      if (lane == 0) { cp->ua = ua; cp->ub = ub; cp->split = 0; cp->c0 = c; cp->c1 = c + 1; }
+    } else {
+      // every unit gets 1 + its cost share of the G - U extra CTAs: unit u owns
+      // CTAs [c0(u), c0(u+1)), c0(U) = G
+      const int64_t extra = G - U;
+      int cnt = 0;
+      for (int base = 0; base < U; base += 32) {
+        const int u = base + lane;
+        const int c0u = u < U ? u + (int)((ustart[u] * extra + T / 2) / T) : G;
+        cnt += __popc(__ballot_sync(0xffffffffu, u < U && c0u <= c));
+      }
+      const int u = cnt - 1;                      // c0(0) = 0 <= c: u >= 0
+      if (lane == 0) {
+        const int c0 = u + (int)((ustart[u] * extra + T / 2) / T);
+        const int c1 = (u + 1 < U) ? (u + 1) + (int)((ustart[u + 1] * extra + T / 2) / T) : G;
+        cp->ua = u; cp->ub = u + 1; cp->split = c1 - c0 > 1; cp->c0 = c0; cp->c1 = c1;
+      }
+    }
+    if (lane == 0) *s_flag = G;
   }
-  if (tid == 0) {
+  if (tid == 32) {
     for (int s = 0; s < NST; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-      stage_n[s] = 0;
-      stage_done[s] = 0;
-      stage_fill[s] = -1;
+      mbar_init(&empty[s], NCW);
     }
-    claim[0] = claim[1] = 0;
     *units_done = 0;
-    for (int i = 0; i < SM::NUS; i++) usm[i].tag = -1;
+    for (int i = 0; i < SM::NUS; i++) ent[i].tag = -1;
     fence_mbar_init();
   }
   __syncthreads();
-  const int64_t T = ustart[U];
-  int G = (int)(T / MIN_CTA_BYTES);
-  G = G < 1 ? 1 : (G > (int)gridDim.x ? (int)gridDim.x : G);
+  const int G = *s_flag;
   const int c = blockIdx.x;
   if (c >= G) return;
-  if (ts && tid == 0) ts[1] = gtime();
+  if (a.debug & 32) return;                       // debug: launch + prologue only
+  if (ts && tid == 0) { ts[1] = gtime(); ts[70] = clock64(); }
 
   if (warp == NCW) {
     // =========================== producer ===========================
-    // One elected lane walks the stage plan: per stage, wait until the ring slot
-    // is free, arm the tx bytes and issue one bulk copy (a run of equal-size
-    // records) or two per FP16 rest tile.
     if (lane == 0) {
+      using IG = ItemGeo<D, S>;
       const uint64_t pol = policy_evict_first();
       const bool nocopy = (a.debug & 2) != 0;
-      int sg = 0;                                  // global stage number of this CTA
-      int uix = 0;                                 // index of the unit among this CTA's units
-      // publish a unit plan for the consumers (ring of NUS slots, tag written last)
-      auto publish = [&](int u, int n_u, const UnitGeo *gg, const UnitPlan *pl, int c0, int c1) {
+      const CtaPlan P = *cp;
+      int sg = 0;                                  // stage number of this CTA
+      int uix = 0;                                 // entry number of this CTA
+      auto publish = [&](int u, int n_u, const UnitGeo *gg, const UnitPlan *pl) {
         while (*reinterpret_cast<volatile int *>(units_done) < uix - (SM::NUS - 1)) {
         }
-        UnitSm &d = usm[uix % SM::NUS];
+        Entry &d = ent[uix % SM::NUS];
         d.u = u;
         d.n_u = n_u;
-        d.sg_base = sg;
-        d.c0 = c0;
-        d.c1 = c1;
+        d.c0 = P.split ? P.c0 : c;
+        d.c1 = P.split ? P.c1 : c + 1;
         d.rl = gg ? gg->rl : 0;
         d.nslots = gg ? gg->nslots : 0;
+#pragma unroll
         for (int pp = 0; pp < 5; pp++) {
+          d.lo[pp] = pl ? pl->lo[pp] : 0;
           d.len[pp] = pl ? pl->hi[pp] - pl->lo[pp] : 0;
           d.nst[pp] = pl ? pl->nst[pp] : 0;
-          d.cap[pp] = pl ? pl->cap[pp] : 1;
-          d.rcap[pp] = 1.0f / (float)d.cap[pp];
-          d.lo[pp] = pl ? pl->lo[pp] : 0;
-          d.sz[pp] = pl ? pl->sz[pp] : 0;
         }
         __threadfence_block();
         *reinterpret_cast<volatile int *>(&d.tag) = uix;
         uix++;
       };
-      for (int u = 0; u < U; u++) {
-        int c0, c1;
-        unit_ctas(u, U, G, T, ustart, c0, c1);
-        if (c < c0 || c >= c1) continue;
-        const int64_t us = ustart[u], ue = ustart[u + 1];
-        if (ue <= us) {
-          publish(u, 0, nullptr, nullptr, c0, c1);
-          continue;
-        }
+      for (int u = P.ua; u < P.ub; u++) {
+        const int64_t img_off = a.offs[u];         // issued with unit_geo's loads
         UnitGeo gg;
-        unit_geo(a, u, gg);
-        const int nitems = gg.nslots + gg.ntiles;
-        const int64_t ucost = ue - us, k = c - c0, n = c1 - c0;
-        const int i0 = first_item(a, gg, k * ucost / n);
-        const int i1 = (k == n - 1) ? nitems : first_item(a, gg, (k + 1) * ucost / n);
+        unit_geo<D, S>(a, u, gg);
+        int i0 = 0, i1 = gg.nslots + gg.ntiles;
+        if (P.split) {
+          const int64_t ucost = ustart[u + 1] - ustart[u], k = c - P.c0, n = P.c1 - P.c0;
+          i0 = first_item<D, S>(gg, k * ucost / n);
+          if (k < n - 1) i1 = first_item<D, S>(gg, (k + 1) * ucost / n);
+        }
         UnitPlan pl;
-        plan_unit<STAGE>(a, gg, i0, i1, pl);
-        publish(u, i1 - i0, &gg, &pl, c0, c1);
-        const uint8_t *img = a.packed + a.offs[u];
+        plan_unit<D, S, STAGE>(gg, i0, i1, pl);
+        bool published = false;
+        const uint8_t *img = a.packed + img_off;
         const __half *kr = a.k_rest + gg.b * a.rs_b + gg.h * a.rs_h;
         const __half *vr = a.v_rest + gg.b * a.rs_b + gg.h * a.rs_h;
+#pragma unroll
         for (int p = 0; p < 5; p++) {
+          const int cap = STAGE / IG::sz(p);
           for (int t = 0; t < pl.nst[p]; t++, sg++) {
             const int slot = sg % NST;
             const uint32_t fill = (uint32_t)(sg / NST);
-            const int f0 = pl.lo[p] + t * pl.cap[p];
-            const int f1 = min(pl.hi[p], f0 + pl.cap[p]);
+            const int f0 = pl.lo[p] + t * cap;
+            const int f1 = min(pl.hi[p], f0 + cap);
             mbar_wait(&empty[slot], (fill & 1) ^ 1);
-            stage_n[slot] = f1 - f0;
-            *reinterpret_cast<volatile int *>(stage_fill + slot) = (int)fill;
+            if (ts && sg < 64) ts[72 + sg] = clock64();
             uint8_t *dst = ring + (size_t)slot * STAGE;
             if (nocopy) {
               mbar_arrive(&full[slot]);
             } else if (p < 4) {
-              const uint32_t nb = (uint32_t)(f1 - f0) * pl.sz[p];
+              const uint32_t nb = (uint32_t)(f1 - f0) * IG::sz(p);
               mbar_arrive_expect_tx(&full[slot], nb);
-              bulk_g2s_evict_first(dst, img + gg.cs[p] + (int64_t)(f0 - gg.so[p]) * pl.sz[p], nb, &full[slot], pol);
+              bulk_g2s_evict_first(dst, img + gg.cs[p] + (int64_t)(f0 - gg.so[p]) * IG::sz(p), nb, &full[slot], pol);
             } else {
-              uint32_t tx = 0;
-              for (int i = f0; i < f1; i++) tx += (uint32_t)min(16, gg.rl - 16 * (i - gg.nslots)) * 4u * D;
-              mbar_arrive_expect_tx(&full[slot], tx);
-              // FP16 rest rows land in padded rows (stride 2D+16 B) so the ldmatrix
-              // reads of do_rest are bank-conflict free
-              constexpr int RP = 2 * D + 16;
-              for (int i = f0; i < f1; i++) {
-                const int t0 = 16 * (i - gg.nslots);
-                const int nt = min(16, gg.rl - t0);
-                uint8_t *d2 = dst + (size_t)(i - f0) * pl.sz[4];
-                for (int r = 0; r < nt; r++) {
-                  bulk_g2s_evict_first(d2 + r * RP, kr + (int64_t)(t0 + r) * D, 2 * D, &full[slot], pol);
-                  bulk_g2s_evict_first(d2 + (16 + r) * RP, vr + (int64_t)(t0 + r) * D, 2 * D, &full[slot], pol);
-                }
-              }
+              // rest tiles [f0, f1) = rows [r0, r1): one bulk copy for K, one for V
+              const int r0 = 16 * (f0 - gg.nslots);
+              const int r1 = min(gg.rl, 16 * (f1 - gg.nslots));
+              const uint32_t nb = (uint32_t)(r1 - r0) * 2u * D;
+              mbar_arrive_expect_tx(&full[slot], 2 * nb);
+              bulk_g2s_evict_first(dst, kr + (int64_t)r0 * D, nb, &full[slot], pol);
+              bulk_g2s_evict_first(dst + cap * 32 * D, vr + (int64_t)r0 * D, nb, &full[slot], pol);
             }
+            if (!published) { publish(u, i1 - i0, &gg, &pl); published = true; }
           }
         }
+        if (!published) publish(u, i1 - i0, &gg, &pl);
       }
-      publish(-1, 0, nullptr, nullptr, 0, 1);     // terminator
+      publish(-1, 0, nullptr, nullptr);           // terminator
       if (ts) ts[2] = gtime();
     }
     return;
   }
 
   // =========================== consumers ===========================
-  // Units in the same order as the producer; items of a unit are claimed
-  // dynamically (shared-memory ticket), so faster warps take more windows.
   uint8_t *scratch = sm + SM::scratch_off + warp * SM::SCRATCH;
   float *ep = reinterpret_cast<float *>(sm + SM::ep_off);
   const int g = lane >> 2, q = lane & 3;
+  const int grp = a.grp;
   uint32_t qf[KT][2];
   float o[KT][4];
   WarpState st;
-  int uidx = 0;
-  uint64_t acc_tag = 0, acc_full = 0, acc_comp = 0, t_ep = 0;
+  int uidx = 0, sg = 0;
+  uint64_t acc_wait = 0, acc_comp = 0, t_ep = 0;
   for (;;) {
-    const UnitSm &U_ = usm[uidx % SM::NUS];
-    while (*reinterpret_cast<const volatile int *>(&U_.tag) != uidx) {
+    const Entry &E = ent[uidx % SM::NUS];
+    while (*reinterpret_cast<const volatile int *>(&E.tag) != uidx) {
     }
     __threadfence_block();
-    const int u = *reinterpret_cast<const volatile int *>(&U_.u);
+    const int u = *reinterpret_cast<const volatile int *>(&E.u);
     if (u < 0) break;
-    const int n_u = U_.n_u;
-    const int sg_base = U_.sg_base;
-    const int cf = U_.c0, cl = U_.c1 - 1;
+    const int c0 = E.c0, c1 = E.c1, rl = E.rl, nslots = E.nslots;
     const int b = u / a.H, h = u % a.H;
     {
-      const __half *qrow = a.q + ((int64_t)b * a.Hq + h * a.grp + g) * D;
+      const __half *qrow = a.q + ((int64_t)b * a.Hq + h * grp + g) * D;
 #pragma unroll
       for (int kt = 0; kt < KT; kt++) {
-        qf[kt][0] = g < a.grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q) : 0u;
-        qf[kt][1] = g < a.grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q + 8) : 0u;
+        qf[kt][0] = g < grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q) : 0u;
+        qf[kt][1] = g < grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q + 8) : 0u;
       }
     }
 #pragma unroll
     for (int mt = 0; mt < KT; mt++) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
     st.m[0] = st.m[1] = -INFINITY;
     st.l[0] = st.l[1] = st.vb[0] = st.vb[1] = 0.f;
-    int *cl_ctr = claim + (uidx & 1);
-    int j = 0;
-    if (lane == 0) j = atomicAdd(cl_ctr, 1);
-    j = __shfl_sync(0xffffffffu, j, 0);
-    for (;;) {
-      uint64_t t_a = ts ? gtime() : 0;
-      if (j >= n_u) break;
-      // claim the next item now; its ticket is only needed after this window
-      int jn = 0;
-      if (lane == 0) jn = atomicAdd(cl_ctr, 1);
-      // locate item j of the unit in the stage plan (shared-memory plan)
-      int p = 0, sbase = sg_base, idx = j;
-      while (idx >= U_.len[p]) { idx -= U_.len[p]; sbase += U_.nst[p]; p++; }
-      const int cap = U_.cap[p];
-      const int qs = (int)(((float)idx + 0.5f) * U_.rcap[p]);   // idx / cap
-      const int sgi = sbase + qs;
-      const int es = sgi % NST;
-      const int fill = sgi / NST;
-      const uint32_t par = (uint32_t)fill & 1u;
-      const int kind = p;
-      const int ii = U_.lo[p] + idx;
-      const int ntok = p == 4 ? min(16, U_.rl - 16 * (ii - U_.nslots)) : 0;
-      const uint8_t *rec = ring + (size_t)es * STAGE + (size_t)(idx - qs * cap) * U_.sz[p];
-      uint64_t t_b = ts ? gtime() : 0;
-      // the slot must be on this fill before its parity is meaningful (a claim can
-      // run more than one ring lap ahead of a slot that is still loading)
-      while (*reinterpret_cast<volatile int *>(stage_fill + es) < fill) {
-      }
-      mbar_wait(&full[es], par);
-      uint64_t t_c = ts ? gtime() : 0;
-      if (ts) { acc_tag += t_b - t_a; acc_full += t_c - t_b; }
-      if (a.debug & 1) {
-        st.l[0] += (float)lds32(rec + 16 * lane);
-      } else switch (kind) {
-        case 0: do_window<D, S, 2>(rec, qf, a.scale_log2, st, o, scratch, lane); break;
-        case 1: do_window<D, S, 4>(rec, qf, a.scale_log2, st, o, scratch, lane); break;
-        case 2: do_window<D, S, 8>(rec, qf, a.scale_log2, st, o, scratch, lane); break;
-        case 3: do_window<D, S, 16>(rec, qf, a.scale_log2, st, o, scratch, lane); break;
-        default: do_rest<D>(rec, ntok, qf, a.scale_log2, st, o, scratch, lane); break;
-      }
-      __syncwarp();
-      jn = __shfl_sync(0xffffffffu, jn, 0);
-      if (ts) {
-        const uint64_t dt = gtime() - t_c;
-        acc_comp += dt;
-        if (lane == 0) {
-          atomicAdd(reinterpret_cast<unsigned long long *>(ts + 56 + kind), (unsigned long long)dt);
-          atomicAdd(reinterpret_cast<unsigned long long *>(ts + 61 + kind), 1ull);
+
+    int nxt = warp;                                // next entry item of this warp
+    int kbase = 0;                                 // entry item index of the stage's first item
+#pragma unroll
+    for (int p = 0; p < 5; p++) {
+      using IG = ItemGeo<D, S>;
+      constexpr int SZ_[5] = {IG::sz(0), IG::sz(1), IG::sz(2), IG::sz(3), IG::sz(4)};
+      const int sz = SZ_[p];
+      const int cap = STAGE / sz;
+      const int len = E.len[p], nst = E.nst[p], lo = E.lo[p];
+      for (int t = 0; t < nst; t++, sg++) {
+        const int slot = sg % NST;
+        const int n = min(cap, len - t * cap);
+        const uint64_t t0 = ts ? gtime() : 0;
+        mbar_wait(&full[slot], (uint32_t)(sg / NST) & 1u);
+        const uint64_t t1 = ts ? gtime() : 0;
+        if (ts && sg < 64 && lane == 0 && warp == 0) ts[136 + sg] = clock64();
+        const uint8_t *sbase = ring + (size_t)slot * STAGE;
+        for (; nxt < kbase + n; nxt += NCW) {
+          const int k = nxt - kbase;
+          const uint8_t *rec = sbase + (size_t)k * sz;
+          if (a.debug & 1) {
+            st.l[0] += (float)lds32(rec + 16 * lane);
+          } else if (p == 0) {
+            do_window<D, S, 2>(rec, qf, a.scale_log2, st, o, scratch, lane);
+          } else if (p == 1) {
+            do_window<D, S, 4>(rec, qf, a.scale_log2, st, o, scratch, lane);
+          } else if (p == 2) {
+            do_window<D, S, 8>(rec, qf, a.scale_log2, st, o, scratch, lane);
+          } else if (p == 3) {
+            do_window<D, S, 16>(rec, qf, a.scale_log2, st, o, scratch, lane);
+          } else {
+            const int ii = lo + t * cap + k;
+            do_rest<D>(sbase + (size_t)k * 32 * D, sbase + (size_t)(cap + k) * 32 * D, min(16, rl - 16 * (ii - nslots)),
+                       qf, a.scale_log2, st, o, scratch, lane);
+          }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        kbase += n;
+        if (ts) { acc_wait += t1 - t0; acc_comp += gtime() - t1; }
       }
-      if (lane == 0) {
-        const int nd = atomicAdd(stage_done + es, 1) + 1;
-        if (nd == *reinterpret_cast<volatile int *>(stage_n + es)) {
-          stage_done[es] = 0;
-          mbar_arrive(&empty[es]);
-        }
-      }
-      j = jn;
     }
     if (ts && tid == 0) ts[3] = gtime();
     const uint64_t t_e0 = ts ? gtime() : 0;
 
-    // ---------------- unit epilogue: merge tree over the warps ----------------
-    named_bar_sync(1, NCW * 32);
-    const uint64_t t_e1 = ts ? gtime() : 0;
-    uint64_t t_e2 = 0, t_e3 = 0;
-    if (tid == 0) claim[uidx & 1] = 0;            // reused by the unit after next
-    uidx++;
-    {
-      // every warp parks its state (l, vb reduced over the 8 lanes of a head pair)
-      for (int off = 4; off <= 16; off <<= 1) {
-        st.l[0] += __shfl_xor_sync(0xffffffffu, st.l[0], off);
-        st.l[1] += __shfl_xor_sync(0xffffffffu, st.l[1], off);
-        st.vb[0] += __shfl_xor_sync(0xffffffffu, st.vb[0], off);
-        st.vb[1] += __shfl_xor_sync(0xffffffffu, st.vb[1], off);
-      }
-      float *mine = ep + warp * SM::EPW;           // [8][D] o, then m[8], l[8], vb[8]
+    // ---------------- entry epilogue ----------------
+    // (1) every warp parks (m, l, vb) per head and its o as [8 heads][D]
+#pragma unroll
+    for (int off = 4; off <= 16; off <<= 1) {
+      st.l[0] += __shfl_xor_sync(0xffffffffu, st.l[0], off);
+      st.l[1] += __shfl_xor_sync(0xffffffffu, st.l[1], off);
+      st.vb[0] += __shfl_xor_sync(0xffffffffu, st.vb[0], off);
+      st.vb[1] += __shfl_xor_sync(0xffffffffu, st.vb[1], off);
+    }
+    if (!(a.debug & 16)) {
+      float *mine = ep + warp * SM::EPW;
 #pragma unroll
       for (int mt = 0; mt < KT; mt++) {
         mine[(2 * q) * D + 16 * mt + g] = o[mt][0];
@@ -745,121 +727,116 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         mine[8 * D + 8 + 2 * q] = st.l[0]; mine[8 * D + 8 + 2 * q + 1] = st.l[1];
         mine[8 * D + 16 + 2 * q] = st.vb[0]; mine[8 * D + 16 + 2 * q + 1] = st.vb[1];
       }
-      named_bar_sync(1, NCW * 32);
-      // per head: M, L and the warp weights f[w] (thread j < grp); weights overwrite m
-      float *Mh = reinterpret_cast<float *>(sm + SM::scratch_off);   // [8] M, [8] L (scratch is free now)
-      if (tid < a.grp) {
-        const int j = tid;
-        float M = -INFINITY;
-        for (int w = 0; w < NCW; w++) M = fmaxf(M, ep[w * SM::EPW + 8 * D + j]);
-        float L = 0.f;
-        for (int w = 0; w < NCW; w++) {
-          float *pw = ep + w * SM::EPW + 8 * D;
-          const float f = (M == -INFINITY) ? 0.f : exp2f(pw[j] - M);
-          L += f * pw[8 + j];
-          pw[j] = f;
-        }
-        Mh[j] = M;
-        Mh[8 + j] = L;
-      }
-      named_bar_sync(1, NCW * 32);
-      t_e2 = ts ? gtime() : 0;
-      float *slot = a.ws_part + (int64_t)(c + u) * a.grp * (D + 2);
-      // CTA partial (m, l, o + vb) [grp][D + 2], coalesced over channels
-      for (int idx = tid; idx < a.grp * D; idx += NCW * 32) {
-        const int j = idx / D, cc = idx % D;
-        float O = 0.f;
-#pragma unroll 5
+    }
+    named_bar_sync(1, NCW * 32);
+    uidx++;
+    if (a.debug & 16) {                           // debug: no epilogue
+      if (tid == 0) atomicAdd(units_done, 1);
+      continue;
+    }
+    // (2) CTA merge: thread per output (head j, channel cc); M, L recomputed per
+    // element from the NCW parked states (broadcast reads, no extra barrier)
+    const bool split = (c1 - c0) > 1;
+    float *wslot = a.ws_part + (int64_t)(c + u) * grp * (D + 2);
+    for (int idx = tid; idx < grp * D; idx += NCW * 32) {
+      const int j = idx / D, cc = idx - j * D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < NCW; w++) M = fmaxf(M, ep[w * SM::EPW + 8 * D + j]);
+      float L = 0.f, O = 0.f;
+      if (M != -INFINITY) {
+#pragma unroll
         for (int w = 0; w < NCW; w++) {
           const float *pw = ep + w * SM::EPW;
-          O += pw[8 * D + j] * (pw[j * D + cc] + pw[8 * D + 16 + j]);
+          const float f = exp2f(pw[8 * D + j] - M);
+          L = fmaf(f, pw[8 * D + 8 + j], L);
+          O = fmaf(f, pw[j * D + cc] + pw[8 * D + 16 + j], O);
         }
-        slot[j * (D + 2) + 2 + cc] = O;
-        if (cc == 0) { slot[j * (D + 2)] = Mh[j]; slot[j * (D + 2) + 1] = Mh[8 + j]; }
       }
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (split) {
+        if (cc == 0) { wslot[j * (D + 2)] = M; wslot[j * (D + 2) + 1] = L; }
+        wslot[j * (D + 2) + 2 + cc] = O;
+      } else {
+        const int64_t row = (int64_t)b * a.Hq + h * grp + j;
+        if (a.out) a.out[row * D + cc] = __float2half_rn(L > 0.f ? O / L : 0.f);
+        if (a.partial) {
+          float *pp = a.partial + row * (D + 2);
+          if (cc == 0) { pp[0] = M * 0.69314718055994530942f; pp[1] = L; }
+          pp[2 + cc] = O;
+        }
+      }
+    }
+    const uint64_t t_e1 = ts ? gtime() : 0;
+    if (split) {
+      // (3) ticket: the last CTA of the unit merges all CTA partials by log-sum-exp
       named_bar_sync(1, NCW * 32);
       if (tid == 0) {
+        __threadfence();
         const int old = atomicAdd(a.ws_cnt + u, 1);
-        *s_flag = (old == cl - cf);
+        *s_flag = (old == c1 - c0 - 1);
       }
       named_bar_sync(1, NCW * 32);
-      t_e3 = ts ? gtime() : 0;
+      if (ts && tid == 0) { ts[6] = *s_flag; ts[7] = c - c0; }
       if (*s_flag) {
-        // last CTA of the unit: log-sum-exp merge of the unit's CTA partials.
-        // (m, l) of every partial -> per-partial weights in shared memory (reusing
-        // the merge-tree buffer), then each thread sums its output columns.
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        const int np = cl - cf + 1;
-        float *wgt = ep;                              // [np][8] weights, then [8] M, [8] L
-        float *Ms = ep + (size_t)np * 8, *Ls = Ms + 8;
-        // (m, l) of all partials in one parallel round trip
-        for (int t = tid; t < np * 8; t += NCW * 32) {
-          const int c2 = t >> 3, j = t & 7;
-          float mv = -INFINITY, lv = 0.f;
-          if (j < a.grp) {
-            const float *sp = a.ws_part + (int64_t)(cf + c2 + u) * a.grp * (D + 2) + j * (D + 2);
-            mv = __ldcg(sp);
-            lv = __ldcg(sp + 1);
+        __threadfence();
+        // every output element: the np partials' (m, l, o) in one batch of
+        // independent loads, then the log-sum-exp combination in registers
+        const int np = c1 - c0;
+        const int64_t stride = (int64_t)grp * (D + 2);
+        const float *pb = a.ws_part + (int64_t)(c0 + u) * stride;
+        constexpr int CHP = 16;                   // partials per load batch
+        for (int idx = tid; idx < grp * D; idx += NCW * 32) {
+          const int j = idx / D, cc = idx - j * D;
+          const float *hb = pb + j * (D + 2);
+          float M = -INFINITY, L = 0.f, O = 0.f;
+          for (int b0 = 0; b0 < np; b0 += CHP) {
+            float mv[CHP], lv[CHP], ov[CHP];
+#pragma unroll
+            for (int i = 0; i < CHP; i++) {
+              const bool ok = b0 + i < np;
+              mv[i] = ok ? __ldcg(hb + (b0 + i) * stride) : -INFINITY;
+              lv[i] = ok ? __ldcg(hb + (b0 + i) * stride + 1) : 0.f;
+              ov[i] = ok ? __ldcg(hb + (b0 + i) * stride + 2 + cc) : 0.f;
+            }
+            float Mn = M;
+#pragma unroll
+            for (int i = 0; i < CHP; i++) Mn = fmaxf(Mn, lv[i] > 0.f ? mv[i] : -INFINITY);
+            if (Mn != -INFINITY) {
+              const float r = exp2f(M - Mn);
+              L *= r;
+              O *= r;
+#pragma unroll
+              for (int i = 0; i < CHP; i++) {
+                const float f = lv[i] > 0.f ? exp2f(mv[i] - Mn) : 0.f;
+                L = fmaf(f, lv[i], L);
+                O = fmaf(f, ov[i], O);
+              }
+              M = Mn;
+            }
           }
-          wgt[t] = mv;
-          Ls[8 + t] = lv;                               // scratch: l of partial c2, head j
-        }
-        named_bar_sync(1, NCW * 32);
-        if (tid < a.grp) {
-          const int j = tid;
-          float M = -INFINITY;
-          for (int c2 = 0; c2 < np; c2++) M = fmaxf(M, wgt[c2 * 8 + j]);
-          float L = 0.f;
-          for (int c2 = 0; c2 < np; c2++) {
-            const float f = (M == -INFINITY) ? 0.f : exp2f(wgt[c2 * 8 + j] - M);
-            wgt[c2 * 8 + j] = f;
-            L += f * Ls[8 + c2 * 8 + j];
-          }
-          Ms[j] = M;
-          Ls[j] = L;
-        }
-        named_bar_sync(1, NCW * 32);
-        for (int idx = tid; idx < a.grp * D; idx += NCW * 32) {
-          const int j = idx / D, cc = idx % D;
-          float O = 0.f;
-          const float *base = a.ws_part + (int64_t)(cf + u) * a.grp * (D + 2) + j * (D + 2) + 2 + cc;
-          const int64_t stride = (int64_t)a.grp * (D + 2);
-          int c2 = 0;
-          for (; c2 + 4 <= np; c2 += 4) {
-            const float o0 = __ldcg(base + (c2 + 0) * stride), o1 = __ldcg(base + (c2 + 1) * stride);
-            const float o2 = __ldcg(base + (c2 + 2) * stride), o3 = __ldcg(base + (c2 + 3) * stride);
-            O += wgt[(c2 + 0) * 8 + j] * o0 + wgt[(c2 + 1) * 8 + j] * o1 + wgt[(c2 + 2) * 8 + j] * o2 +
-                 wgt[(c2 + 3) * 8 + j] * o3;
-          }
-          for (; c2 < np; c2++) O += wgt[c2 * 8 + j] * __ldcg(base + c2 * stride);
-          const float L = Ls[j];
-          const int64_t row = (int64_t)b * a.Hq + h * a.grp + j;
+          const int64_t row = (int64_t)b * a.Hq + h * grp + j;
           if (a.out) a.out[row * D + cc] = __float2half_rn(L > 0.f ? O / L : 0.f);
           if (a.partial) {
             float *pp = a.partial + row * (D + 2);
-            if (cc == 0) {
-              pp[0] = Ms[j] * 0.69314718055994530942f;   // log2 domain -> natural
-              pp[1] = L;
-            }
+            if (cc == 0) { pp[0] = M * 0.69314718055994530942f; pp[1] = L; }
             pp[2 + cc] = O;
           }
         }
         if (tid == 0) a.ws_cnt[u] = 0;
       }
-      named_bar_sync(1, NCW * 32);
     }
-    if (tid == 0) atomicAdd(units_done, 1);
     if (ts && tid == 0) {
-      const uint64_t t_e4 = gtime();
-      ts[68] += t_e1 - t_e0; ts[69] += t_e2 - t_e1; ts[70] += t_e3 - t_e2; ts[71] += t_e4 - t_e3;
+      const uint64_t t_e2 = gtime();
+      ts[68] += t_e1 - t_e0; ts[69] += t_e2 - t_e1;
+      ts[4] = t_e2; ts[5] += (uint64_t)E.n_u;
     }
-    if (ts && tid == 0) { ts[4] = gtime(); ts[5] += (uint64_t)n_u; }
+    named_bar_sync(1, NCW * 32);                  // ep is reused by the next entry
+    if (tid == 0) atomicAdd(units_done, 1);
     if (ts) t_ep += gtime() - t_e0;
   }
   if (ts && lane == 0) {
     uint64_t *wt = ts + 8 + warp * 4;
-    wt[0] = acc_tag; wt[1] = acc_full; wt[2] = acc_comp; wt[3] = t_ep;
+    wt[0] = acc_wait; wt[1] = acc_comp; wt[2] = t_ep; wt[3] = 0;
   }
 }
 
@@ -888,7 +865,7 @@ size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms) {
   size_t part = (size_t)(num_sms + B * H) * grp * (d + 2) * sizeof(float);
   part = (part + 255) / 256 * 256;
   size_t cnt = ((size_t)B * H * sizeof(int32_t) + 255) / 256 * 256;
-  return part + cnt + (size_t)num_sms * 72 * sizeof(uint64_t);
+  return part + cnt + (size_t)num_sms * TS_PER_CTA * sizeof(uint64_t);
 }
 
 template <int D, int S>

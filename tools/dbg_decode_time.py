@@ -1,42 +1,57 @@
-"""Per-CTA globaltimer stamps of one C5-shaped decode layer (WQ_DECODE_DEBUG has bit 8)."""
+"""Per-CTA globaltimer stamps of C5-shaped decode launches (WQ_DECODE_DEBUG bit 8 plus
+optional mode bits from DBG, e.g. DBG=19 for the no-copy/no-math/no-epilogue skeleton)."""
 import math, sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2605_02262_b200 import configs, synth, wq
+import oracle
 cfg = configs.CONFIGS["C5"]; m = cfg.model
 dev = "cuda"
-vis, txt = synth.embeddings(cfg.B, cfg.M, 32, m.D, cfg.S, cfg.seed, dev)
+vis, txt = synth.embeddings(cfg.B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, dev)
 g = wq.geom(cfg.B, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
-thr = wq.wq_thresholds([0.5], 2.0, 4)
+thr = oracle.thresholds(cfg.sensitivities(), cfg.alpha, len(cfg.widths))
 sc = wq.wq_window_scores(vis, txt, cfg.S)
-bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
-K, V, kr, vr, rest_len = synth.layer_tensors(cfg, 0, dev)
-q = synth.queries(cfg.B, m.Hq, m.H, m.d, cfg.seed, 0, device=dev)
-offs = wq.wq_layer_layout(g, seg[0])
+bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, cfg.layers, g, wq.AssignOpts(cfg.budget, 1, 0))
+l = cfg.layers - 1
+K, V, kr, vr, rest_len = synth.layer_tensors(cfg, l, dev)
+q = synth.queries(cfg.B, m.Hq, m.H, m.d, cfg.seed, l, device=dev)
+offs = wq.wq_layer_layout(g, seg[l])
 packed = torch.zeros(int(offs[-1].item()) + 16, dtype=torch.uint8, device=dev)
-wq.wq_reorder_quantize_pack(K, V, 0, g, perm[0], seg[0], offs, packed)
+wq.wq_reorder_quantize_pack(K, V, 0, g, perm[l], seg[l], offs, packed)
 ws = torch.zeros(wq.wq_decode_workspace(g), dtype=torch.uint8, device=dev)
 out = torch.empty((cfg.B, m.Hq, m.d), dtype=torch.float16, device=dev)
-for it in range(3):
-    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    e0.record(); wq.wq_decode_attention(q, packed, offs, seg[0], g, kr, vr, rest_len, 1 / math.sqrt(128), out=out, workspace=ws); e1.record()
-    torch.cuda.synchronize()
-    print("event us", e0.elapsed_time(e1) * 1e3)
 nsm = torch.cuda.get_device_properties(0).multi_processor_count
-tsb = ws[-nsm * 576:].view(torch.int64).view(nsm, 72).cpu().numpy()
-NW = 11
-wt = tsb[:, 8:8 + 4 * NW].reshape(nsm, NW, 4) / 1e3
-kt = tsb[:, 56:61].sum(0) / 1e3; kc = tsb[:, 61:66].sum(0)
-print("per-kind compute us per item (2,4,8,16,rest):", np.round(kt / np.maximum(kc, 1), 3), "counts", kc)
-epi = tsb[:, 68:72] / 1e3
-slow = np.argsort(-(tsb[:, 4] - tsb[:, 0]))[:4]
-for cidx in list(slow) + [int(np.argsort(tsb[:, 4] - tsb[:, 0])[0])]:
-    print("CTA", cidx, "dur us", (tsb[cidx, 4] - tsb[cidx, 0]) / 1e3, "items", tsb[cidx, 5], "per-warp (tag, full, comp, ep):", np.round(wt[cidx, :, :], 1).tolist()[:2], "epi (barrier, tree, ticket, merge):", np.round(epi[cidx], 1))
-print("mean over warps/CTAs:", np.round(wt.mean((0, 1)), 2), "max:", np.round(wt.max((0, 1)), 2))
-t0 = tsb[:, 0].min()
-r = (tsb[:, :5] - t0) / 1e3
-tsb = tsb[:, :8]
-print("per-CTA us: start, prologue, producer_done, consumers_done(last unit), epilogue_done; items")
-for i in list(range(0, nsm, 16)) + [nsm - 1]:
-    print(i, np.round(r[i], 2), tsb[i, 5])
-print("max:", np.round(r.max(0), 2), "median:", np.round(np.median(r, 0), 2))
+NW = int(os.environ.get("NW", "11"))
+TS = 200
+TSB = TS * 8
+for mode in [int(x) for x in os.environ.get("DBG", "0,19").split(",")]:
+    os.environ["WQ_DECODE_DEBUG"] = str(8 | mode)
+    for it in range(4):
+        ws[-nsm * TSB:].zero_()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record(); wq.wq_decode_attention(q, packed, offs, seg[l].contiguous(), g, kr, vr, rest_len, 1 / math.sqrt(128), out=out, workspace=ws); e1.record()
+        torch.cuda.synchronize()
+    print(f"=== mode {mode}: event us {e0.elapsed_time(e1) * 1e3:.1f}")
+    tsb = ws[-nsm * TSB:].view(torch.int64).view(nsm, TS).cpu().numpy().astype(np.float64)
+    t0 = tsb[:, 0].min()
+    st = (tsb[:, :5] - t0) / 1e3
+    st[tsb[:, :5] == 0] = np.nan
+    wt = tsb[:, 8:8 + 4 * NW].reshape(nsm, NW, 4) / 1e3
+    print("per-CTA us (start, prologue done, producer done, consumers done, end) min/median/max:")
+    for k, nm in enumerate(["start", "prologue", "producer", "loop_end", "end"]):
+        print(f"  {nm:9s} {np.nanmin(st[:, k]):7.2f} {np.nanmedian(st[:, k]):7.2f} {np.nanmax(st[:, k]):7.2f}")
+    print("per-warp us (full-wait, compute, epilogue) mean/max:", np.round(wt[:, :, :3].mean((0, 1)), 2), np.round(wt[:, :, :3].max((0, 1)), 2))
+    print("epilogue CTA merge / ticket+merge us mean/max:", np.round(tsb[:, 68:70].mean(0) / 1e3, 2), np.round(tsb[:, 68:70].max(0) / 1e3, 2))
+    print("items per CTA min/max:", tsb[:, 5].min(), tsb[:, 5].max())
+    dur = (tsb[:, 4] - tsb[:, 0]) / 1e3
+    order = np.argsort(-dur)
+    print("slowest CTAs: (cta, end us, loop_end us, producer us, last?, k, items)")
+    for cta in order[:10]:
+        print("   ", cta, round(st[cta, 4], 2), round(st[cta, 3], 2), round(st[cta, 2], 2), int(tsb[cta, 6]), int(tsb[cta, 7]), int(tsb[cta, 5]))
+    for cta in (0, 77):
+        ref = tsb[cta, 70]
+        pi = tsb[cta, 72:136]; fd = tsb[cta, 136:200]
+        n = int((pi > 0).sum())
+        print(f"CTA {cta} stage trace (cycles after prologue): producer issue / warp0 full-done")
+        print("   ", [int(x - ref) if x > 0 else -1 for x in pi[:n]])
+        print("   ", [int(x - ref) if x > 0 else -1 for x in fd[:n]])
