@@ -41,6 +41,9 @@ constexpr int64_t MIN_CTA_BYTES = 49152;
 #ifndef WQ_DEC_QLO
 #define WQ_DEC_QLO 1                     // carry q*s as fp16 hi + lo (0: hi only, experiment)
 #endif
+#ifndef WQ_DEC_KSCALE
+#define WQ_DEC_KSCALE 0                  // K side: A = s*code (fp16, one rounding), B = q (experiment)
+#endif
 #ifndef WQ_DEC_STAGE
 #define WQ_DEC_STAGE 32768
 #endif
@@ -60,15 +63,13 @@ struct ItemGeo {
   }
   static constexpr int REST_SZ = 64 * D;               // FP16 rest tile: 16 K rows + 16 V rows
   static constexpr int sz(int k) { return k == 4 ? REST_SZ : (int)rb(k); }
-  // An SM streams ~49 KB/us of HBM while its NCW consumer warps compute; an item
-  // costs max(its bytes, the bytes the SM could stream during its compute).
-  // Compute-equivalents from measured per-warp item times (tools/dbg_decode_time.py):
-  // quantized window ~1.56*S*D, FP16 window ~0.95*S*D, 16-token rest tile ~35*D.
-  static constexpr int64_t cpe(int k) {
-    return k == 4 ? 35LL * D : (k == 3 ? 95LL * S * D / 100 : 156LL * S * D / 100);
-  }
-  static constexpr int64_t cost(int k) {               // k = 4: one 16-token rest tile
-    return (k == 4 ? (int64_t)REST_SZ : rb(k)) > cpe(k) ? (k == 4 ? (int64_t)REST_SZ : rb(k)) : cpe(k);
+  // Cost of an item ~ its time on one SM inside a full decode launch (the CTA
+  // partition balances cost).  Measured per-class CTA-level item times on C5
+  // (tools/dbg_decode_time.py least-squares fit): 2-bit 0.135 us, 4-bit 0.152,
+  // 8-bit 0.177, FP16 0.287 (byte-bound), 16-token rest tile ~ half an FP16 window;
+  // expressed in units of S*D so other window sizes scale.
+  static constexpr int64_t cost(int k) {
+    return k == 4 ? 53LL * D : (int64_t)(k == 0 ? 156 : k == 1 ? 175 : k == 2 ? 204 : 331) * S * D / 100;
   }
 };
 
@@ -106,19 +107,21 @@ WQ_DEV int64_t unit_cost(const UnitGeo &g) {
   return g.cc[4] + (int64_t)g.ntiles * ItemGeo<D, S>::cost(4);
 }
 
-// first item whose start (in cost units, relative to the unit) is >= x
+// first item whose start (in cost units, relative to the unit) is >= x.  Planning
+// arithmetic runs in double (no 64-bit integer division on the producer's path);
+// every CTA evaluates the same expressions, so neighbouring CTAs agree on the cut.
 template <int D, int S>
-WQ_DEV int first_item(const UnitGeo &g, int64_t x) {
+WQ_DEV int first_item(const UnitGeo &g, double x) {
   using IG = ItemGeo<D, S>;
-  if (x <= 0) return 0;
+  if (x <= 0.0) return 0;
 #pragma unroll
   for (int k = 0; k < 4; k++) {
-    if (x <= g.cc[k]) return g.so[k];
-    if (x < g.cc[k + 1]) return g.so[k] + (int)((x - g.cc[k] + IG::cost(k) - 1) / IG::cost(k));
+    if (x <= (double)g.cc[k]) return g.so[k];
+    if (x < (double)g.cc[k + 1]) return g.so[k] + (int)ceil((x - (double)g.cc[k]) / (double)IG::cost(k));
   }
-  if (x <= g.cc[4]) return g.nslots;
-  const int64_t t = (x - g.cc[4] + IG::cost(4) - 1) / IG::cost(4);
-  return g.nslots + (int)(t < g.ntiles ? t : g.ntiles);
+  if (x <= (double)g.cc[4]) return g.nslots;
+  const int t = (int)ceil((x - (double)g.cc[4]) / (double)IG::cost(4));
+  return g.nslots + (t < g.ntiles ? t : g.ntiles);
 }
 
 // Stage plan of one unit's item range [i0, i1): five "pieces" (the width-class
@@ -178,6 +181,36 @@ WQ_DEV uint32_t deq_pair(const uint32_t *wd, int P) {
       case 5: return dq_pair<2, 5>(w, w8);
       case 6: return dq_pair<2, 6>(w, w8);
       default: return dq_pair<2, 7>(w, w8);
+    }
+  }
+}
+
+// s * code of pair P (scales s: the pair's two channels), K side of WQ_DEC_KSCALE
+template <int BITS>
+WQ_DEV uint32_t deq_pair_s(const uint32_t *wd, int P, uint32_t s) {
+  constexpr int PPW = 16 / BITS;
+  const uint32_t w = wd[P / PPW];
+  if constexpr (BITS == 8) {
+    return hmul2u(deq_pair<8>(wd, P), s);
+  } else if constexpr (BITS == 4) {
+    const uint32_t w8 = w >> 8;
+    switch (P % 4) {
+      case 0: return dq_pair_scaled<4, 0>(w, w8, s);
+      case 1: return dq_pair_scaled<4, 1>(w, w8, s);
+      case 2: return dq_pair_scaled<4, 2>(w, w8, s);
+      default: return dq_pair_scaled<4, 3>(w, w8, s);
+    }
+  } else {
+    const uint32_t w8 = w >> 8;
+    switch (P % 8) {
+      case 0: return dq_pair_scaled<2, 0>(w, w8, s);
+      case 1: return dq_pair_scaled<2, 1>(w, w8, s);
+      case 2: return dq_pair_scaled<2, 2>(w, w8, s);
+      case 3: return dq_pair_scaled<2, 3>(w, w8, s);
+      case 4: return dq_pair_scaled<2, 4>(w, w8, s);
+      case 5: return dq_pair_scaled<2, 5>(w, w8, s);
+      case 6: return dq_pair_scaled<2, 6>(w, w8, s);
+      default: return dq_pair_scaled<2, 7>(w, w8, s);
     }
   }
 }
@@ -296,6 +329,23 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
 #pragma unroll
     for (int kt = 0; kt < KT; kt++) {
       uint32_t h0 = 0, h1 = 0, l0 = 0, l1 = 0;
+      if constexpr (BITS < 16 && WQ_DEC_KSCALE) {
+        const uint4 pr = lds128(kp + (q * KT + kt) * 16);   // {s01, s89, mn01, mn89}
+        if (c0 == 0) {
+          const uint32_t am[4] = {pr.z, pr.z, pr.w, pr.w};
+          if (kt & 1) mma16816(b1, am, qf[kt][0], qf[kt][1], b1);
+          else mma16816(b0, am, qf[kt][0], qf[kt][1], b0);
+        }
+#pragma unroll
+        for (int t = 0; t < CH; t++) {
+          uint32_t a[4];
+#pragma unroll
+          for (int r = 0; r < 4; r++) a[r] = deq_pair_s<BITS>(wk[t], 4 * kt + r, (r < 2) ? pr.x : pr.y);
+          if (kt & 1) mma16816(al[t], a, qf[kt][0], qf[kt][1], al[t]);
+          else mma16816(ah[t], a, qf[kt][0], qf[kt][1], ah[t]);
+        }
+        continue;
+      }
       if constexpr (BITS < 16) {
         const uint4 pr = lds128(kp + (q * KT + kt) * 16);   // {s01, s89, mn01, mn89}
         if (c0 == 0) {
@@ -419,6 +469,9 @@ struct Entry {
 // items [i0, i1).
 struct CtaPlan {
   int ua, ub, split, c0, c1, i0, i1;
+  int geo_ok;                           // geo/img_off of unit ua valid (handed over by warp 0)
+  int64_t img_off;
+  UnitGeo geo;
 };
 
 template <int D, int S>
@@ -472,11 +525,13 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   CtaPlan *cp = reinterpret_cast<CtaPlan *>(sm + SM::plan_off);
   if (warp == 0) {
     int64_t carry = 0;
+    UnitGeo gg;                                   // this lane's unit of the last chunk
+    int64_t ioff = 0;
     for (int base = 0; base < U; base += 32) {
       const int u = base + lane;
       int64_t v = 0;
       if (u < U) {
-        UnitGeo gg;
+        ioff = a.offs[u];
         unit_geo<D, S>(a, u, gg);
         v = unit_cost<D, S>(gg);
       }
@@ -503,7 +558,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         int own = G;
         if (u < U) {
           const int64_t mid = ustart[u] + (ustart[u + 1] - ustart[u]) / 2;
-          own = T > 0 ? (int)((mid * G) / T) : 0;
+          own = T > 0 ? (int)((double)mid * G / (double)T) : 0;
           own = own >= G ? G - 1 : own;
         }
         ua += __popc(__ballot_sync(0xffffffffu, own < c));
@@ -517,15 +572,25 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       int cnt = 0;
       for (int base = 0; base < U; base += 32) {
         const int u = base + lane;
-        const int c0u = u < U ? u + (int)((ustart[u] * extra + T / 2) / T) : G;
+        const int c0u = u < U ? u + (int)rint((double)ustart[u] * extra / (double)T) : G;
         cnt += __popc(__ballot_sync(0xffffffffu, u < U && c0u <= c));
       }
       const int u = cnt - 1;                      // c0(0) = 0 <= c: u >= 0
       if (lane == 0) {
-        const int c0 = u + (int)((ustart[u] * extra + T / 2) / T);
-        const int c1 = (u + 1 < U) ? (u + 1) + (int)((ustart[u + 1] * extra + T / 2) / T) : G;
+        const int c0 = u + (int)rint((double)ustart[u] * extra / (double)T);
+        const int c1 = (u + 1 < U) ? (u + 1) + (int)rint((double)ustart[u + 1] * extra / (double)T) : G;
         cp->ua = u; cp->ub = u + 1; cp->split = c1 - c0 > 1; cp->c0 = c0; cp->c1 = c1;
       }
+    }
+    __syncwarp();
+    const int ua = cp->ua;
+    const int last_base = ((U - 1) / 32) * 32;
+    if (lane == 0) cp->geo_ok = 0;
+    __syncwarp();
+    if (ua < U && ua >= last_base && lane == ua - last_base) {
+      cp->geo = gg;
+      cp->img_off = ioff;
+      cp->geo_ok = 1;
     }
     if (lane == 0) *s_flag = G;
   }
@@ -552,6 +617,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       const uint64_t pol = policy_evict_first();
       const bool nocopy = (a.debug & 2) != 0;
       const CtaPlan P = *cp;
+      if (ts) ts[62] = gtime();
       int sg = 0;                                  // stage number of this CTA
       int uix = 0;                                 // entry number of this CTA
       auto publish = [&](int u, int n_u, const UnitGeo *gg, const UnitPlan *pl) {
@@ -572,17 +638,25 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         }
         __threadfence_block();
         *reinterpret_cast<volatile int *>(&d.tag) = uix;
+        if (ts && uix == 0) ts[60] = gtime();
         uix++;
       };
       for (int u = P.ua; u < P.ub; u++) {
-        const int64_t img_off = a.offs[u];         // issued with unit_geo's loads
+        int64_t img_off;
         UnitGeo gg;
-        unit_geo<D, S>(a, u, gg);
+        if (u == P.ua && P.geo_ok) {
+          gg = P.geo;                              // from the prologue: no global round trip
+          img_off = P.img_off;
+        } else {
+          img_off = a.offs[u];
+          unit_geo<D, S>(a, u, gg);
+        }
         int i0 = 0, i1 = gg.nslots + gg.ntiles;
         if (P.split) {
-          const int64_t ucost = ustart[u + 1] - ustart[u], k = c - P.c0, n = P.c1 - P.c0;
-          i0 = first_item<D, S>(gg, k * ucost / n);
-          if (k < n - 1) i1 = first_item<D, S>(gg, (k + 1) * ucost / n);
+          const double ucost = (double)(ustart[u + 1] - ustart[u]);
+          const int k = c - P.c0, n = P.c1 - P.c0;
+          i0 = first_item<D, S>(gg, ucost * k / n);
+          if (k < n - 1) i1 = first_item<D, S>(gg, ucost * (k + 1) / n);
         }
         UnitPlan pl;
         plan_unit<D, S, STAGE>(gg, i0, i1, pl);
@@ -636,7 +710,19 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   float o[KT][4];
   WarpState st;
   int uidx = 0, sg = 0;
-  uint64_t acc_wait = 0, acc_comp = 0, t_ep = 0;
+  uint64_t acc_wait = 0, acc_comp = 0, t_ep = 0, t_loop = 0;
+  // q fragments of a unit (B operand, heads x channels)
+  auto load_q = [&](int uq) {
+    const int bq = uq / a.H, hq = uq - bq * a.H;
+    const __half *qrow = a.q + ((int64_t)bq * a.Hq + hq * grp + g) * D;
+#pragma unroll
+    for (int kt = 0; kt < KT; kt++) {
+      qf[kt][0] = g < grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q) : 0u;
+      qf[kt][1] = g < grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q + 8) : 0u;
+    }
+  };
+  int qu = cp->ua;                                // prefetch q of the first unit while the
+  if (qu < U) load_q(qu);                         // producer plans and issues the first copy
   for (;;) {
     const Entry &E = ent[uidx % SM::NUS];
     while (*reinterpret_cast<const volatile int *>(&E.tag) != uidx) {
@@ -646,19 +732,17 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
     if (u < 0) break;
     const int c0 = E.c0, c1 = E.c1, rl = E.rl, nslots = E.nslots;
     const int b = u / a.H, h = u % a.H;
-    {
-      const __half *qrow = a.q + ((int64_t)b * a.Hq + h * grp + g) * D;
-#pragma unroll
-      for (int kt = 0; kt < KT; kt++) {
-        qf[kt][0] = g < grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q) : 0u;
-        qf[kt][1] = g < grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q + 8) : 0u;
-      }
-    }
+    if (u != qu) { load_q(u); qu = u; }
 #pragma unroll
     for (int mt = 0; mt < KT; mt++) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
     st.m[0] = st.m[1] = -INFINITY;
     st.l[0] = st.l[1] = st.vb[0] = st.vb[1] = 0.f;
 
+    const uint64_t t_ls = ts ? clock64() : 0;
+    if (ts && tid == 0 && uidx == 0) {
+      ts[61] = gtime();
+      for (int pp = 0; pp < 5; pp++) ts[63 + pp] = (uint64_t)E.len[pp];
+    }
     int nxt = warp;                                // next entry item of this warp
     int kbase = 0;                                 // entry item index of the stage's first item
 #pragma unroll
@@ -671,9 +755,9 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       for (int t = 0; t < nst; t++, sg++) {
         const int slot = sg % NST;
         const int n = min(cap, len - t * cap);
-        const uint64_t t0 = ts ? gtime() : 0;
+        const uint64_t t0 = ts ? clock64() : 0;
         mbar_wait(&full[slot], (uint32_t)(sg / NST) & 1u);
-        const uint64_t t1 = ts ? gtime() : 0;
+        const uint64_t t1 = ts ? clock64() : 0;
         if (ts && sg < 64 && lane == 0 && warp == 0) ts[136 + sg] = clock64();
         const uint8_t *sbase = ring + (size_t)slot * STAGE;
         for (; nxt < kbase + n; nxt += NCW) {
@@ -698,11 +782,12 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         kbase += n;
-        if (ts) { acc_wait += t1 - t0; acc_comp += gtime() - t1; }
+        if (ts) { acc_wait += t1 - t0; acc_comp += clock64() - t1; }
       }
     }
     if (ts && tid == 0) ts[3] = gtime();
-    const uint64_t t_e0 = ts ? gtime() : 0;
+    const uint64_t t_e0 = ts ? clock64() : 0;
+    if (ts) t_loop += t_e0 - t_ls;
 
     // ---------------- entry epilogue ----------------
     // (1) every warp parks (m, l, vb) per head and its o as [8 heads][D]
@@ -734,25 +819,37 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       if (tid == 0) atomicAdd(units_done, 1);
       continue;
     }
-    // (2) CTA merge: thread per output (head j, channel cc); M, L recomputed per
-    // element from the NCW parked states (broadcast reads, no extra barrier)
+    // (2) CTA merge: per head j, M = max_w m_w, weights f_w = 2^(m_w - M) (written over
+    // m_w), L = sum f_w l_w, VB = sum f_w vb_w; then per output (j, cc):
+    // O = VB + sum_w f_w o_w[j][cc]
     const bool split = (c1 - c0) > 1;
     float *wslot = a.ws_part + (int64_t)(c + u) * grp * (D + 2);
-    for (int idx = tid; idx < grp * D; idx += NCW * 32) {
-      const int j = idx / D, cc = idx - j * D;
+    float *hML = reinterpret_cast<float *>(sm + SM::scratch_off);      // [8] M, [8] L, [8] VB
+    if (tid < grp) {
+      const int j = tid;
       float M = -INFINITY;
 #pragma unroll
       for (int w = 0; w < NCW; w++) M = fmaxf(M, ep[w * SM::EPW + 8 * D + j]);
-      float L = 0.f, O = 0.f;
-      if (M != -INFINITY) {
+      float L = 0.f, VB = 0.f;
 #pragma unroll
-        for (int w = 0; w < NCW; w++) {
-          const float *pw = ep + w * SM::EPW;
-          const float f = exp2f(pw[8 * D + j] - M);
-          L = fmaf(f, pw[8 * D + 8 + j], L);
-          O = fmaf(f, pw[j * D + cc] + pw[8 * D + 16 + j], O);
-        }
+      for (int w = 0; w < NCW; w++) {
+        float *pw = ep + w * SM::EPW + 8 * D;
+        const float f = (M == -INFINITY) ? 0.f : exp2f(pw[j] - M);
+        pw[j] = f;
+        L = fmaf(f, pw[8 + j], L);
+        VB = fmaf(f, pw[16 + j], VB);
       }
+      hML[j] = M;
+      hML[8 + j] = L;
+      hML[16 + j] = VB;
+    }
+    named_bar_sync(1, NCW * 32);
+    for (int idx = tid; idx < grp * D; idx += NCW * 32) {
+      const int j = idx / D, cc = idx - j * D;
+      float O = hML[16 + j];
+#pragma unroll
+      for (int w = 0; w < NCW; w++) O = fmaf(ep[w * SM::EPW + 8 * D + j], ep[w * SM::EPW + j * D + cc], O);
+      const float M = hML[j], L = hML[8 + j];
       if (split) {
         if (cc == 0) { wslot[j * (D + 2)] = M; wslot[j * (D + 2) + 1] = L; }
         wslot[j * (D + 2) + 2 + cc] = O;
@@ -766,7 +863,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         }
       }
     }
-    const uint64_t t_e1 = ts ? gtime() : 0;
+    const uint64_t t_e1 = ts ? clock64() : 0;
     if (split) {
       // (3) ticket: the last CTA of the unit merges all CTA partials by log-sum-exp
       named_bar_sync(1, NCW * 32);
@@ -784,59 +881,77 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         const int np = c1 - c0;
         const int64_t stride = (int64_t)grp * (D + 2);
         const float *pb = a.ws_part + (int64_t)(c0 + u) * stride;
-        constexpr int CHP = 16;                   // partials per load batch
-        for (int idx = tid; idx < grp * D; idx += NCW * 32) {
-          const int j = idx / D, cc = idx - j * D;
-          const float *hb = pb + j * (D + 2);
-          float M = -INFINITY, L = 0.f, O = 0.f;
-          for (int b0 = 0; b0 < np; b0 += CHP) {
-            float mv[CHP], lv[CHP], ov[CHP];
+        constexpr int EPT_ = (8 * D + NCW * 32 - 1) / (NCW * 32);
+        float mM[EPT_], mL[EPT_], mO[EPT_];
+#pragma unroll
+        for (int e = 0; e < EPT_; e++) { mM[e] = -INFINITY; mL[e] = 0.f; mO[e] = 0.f; }
+        constexpr int CHP = 10;                   // partials per load batch
+        constexpr int EPT = (8 * D + NCW * 32 - 1) / (NCW * 32);   // elements per thread (max)
+        for (int b0 = 0; b0 < np || b0 == 0; b0 += CHP) {
+          // (the common case np <= CHP is one pass with every load of the thread in flight)
+          float mv[EPT][CHP], lv[EPT][CHP], ov[EPT][CHP];
+#pragma unroll
+          for (int e = 0; e < EPT; e++) {
+            const int idx = tid + e * NCW * 32;
+            const int j = idx / D, cc = idx - j * D;
+            const bool ie = idx < grp * D;
+            const float *hb = pb + j * (D + 2);
 #pragma unroll
             for (int i = 0; i < CHP; i++) {
-              const bool ok = b0 + i < np;
-              mv[i] = ok ? __ldcg(hb + (b0 + i) * stride) : -INFINITY;
-              lv[i] = ok ? __ldcg(hb + (b0 + i) * stride + 1) : 0.f;
-              ov[i] = ok ? __ldcg(hb + (b0 + i) * stride + 2 + cc) : 0.f;
-            }
-            float Mn = M;
-#pragma unroll
-            for (int i = 0; i < CHP; i++) Mn = fmaxf(Mn, lv[i] > 0.f ? mv[i] : -INFINITY);
-            if (Mn != -INFINITY) {
-              const float r = exp2f(M - Mn);
-              L *= r;
-              O *= r;
-#pragma unroll
-              for (int i = 0; i < CHP; i++) {
-                const float f = lv[i] > 0.f ? exp2f(mv[i] - Mn) : 0.f;
-                L = fmaf(f, lv[i], L);
-                O = fmaf(f, ov[i], O);
-              }
-              M = Mn;
+              const bool ok = ie && b0 + i < np;
+              mv[e][i] = ok ? __ldcg(hb + (b0 + i) * stride) : -INFINITY;
+              lv[e][i] = ok ? __ldcg(hb + (b0 + i) * stride + 1) : 0.f;
+              ov[e][i] = ok ? __ldcg(hb + (b0 + i) * stride + 2 + cc) : 0.f;
             }
           }
+#pragma unroll
+          for (int e = 0; e < EPT; e++) {
+            float Mn = mM[e];
+#pragma unroll
+            for (int i = 0; i < CHP; i++) Mn = fmaxf(Mn, lv[e][i] > 0.f ? mv[e][i] : -INFINITY);
+            if (Mn != -INFINITY) {
+              const float r = exp2f(mM[e] - Mn);
+              mL[e] *= r;
+              mO[e] *= r;
+#pragma unroll
+              for (int i = 0; i < CHP; i++) {
+                const float f = lv[e][i] > 0.f ? exp2f(mv[e][i] - Mn) : 0.f;
+                mL[e] = fmaf(f, lv[e][i], mL[e]);
+                mO[e] = fmaf(f, ov[e][i], mO[e]);
+              }
+              mM[e] = Mn;
+            }
+          }
+          if (b0 + CHP >= np) break;
+        }
+#pragma unroll
+        for (int e = 0; e < EPT; e++) {
+          const int idx = tid + e * NCW * 32;
+          if (idx >= grp * D) continue;
+          const int j = idx / D, cc = idx - j * D;
           const int64_t row = (int64_t)b * a.Hq + h * grp + j;
-          if (a.out) a.out[row * D + cc] = __float2half_rn(L > 0.f ? O / L : 0.f);
+          if (a.out) a.out[row * D + cc] = __float2half_rn(mL[e] > 0.f ? mO[e] / mL[e] : 0.f);
           if (a.partial) {
             float *pp = a.partial + row * (D + 2);
-            if (cc == 0) { pp[0] = M * 0.69314718055994530942f; pp[1] = L; }
-            pp[2 + cc] = O;
+            if (cc == 0) { pp[0] = mM[e] * 0.69314718055994530942f; pp[1] = mL[e]; }
+            pp[2 + cc] = mO[e];
           }
         }
         if (tid == 0) a.ws_cnt[u] = 0;
       }
     }
     if (ts && tid == 0) {
-      const uint64_t t_e2 = gtime();
+      const uint64_t t_e2 = clock64();
       ts[68] += t_e1 - t_e0; ts[69] += t_e2 - t_e1;
-      ts[4] = t_e2; ts[5] += (uint64_t)E.n_u;
+      ts[4] = gtime(); ts[5] += (uint64_t)E.n_u;
     }
     named_bar_sync(1, NCW * 32);                  // ep is reused by the next entry
     if (tid == 0) atomicAdd(units_done, 1);
-    if (ts) t_ep += gtime() - t_e0;
+    if (ts) t_ep += clock64() - t_e0;
   }
   if (ts && lane == 0) {
     uint64_t *wt = ts + 8 + warp * 4;
-    wt[0] = acc_wait; wt[1] = acc_comp; wt[2] = t_ep; wt[3] = 0;
+    wt[0] = acc_wait; wt[1] = acc_comp; wt[2] = t_ep; wt[3] = t_loop;
   }
 }
 

@@ -36,18 +36,29 @@ for mode in [int(x) for x in os.environ.get("DBG", "0,19").split(",")]:
     t0 = tsb[:, 0].min()
     st = (tsb[:, :5] - t0) / 1e3
     st[tsb[:, :5] == 0] = np.nan
-    wt = tsb[:, 8:8 + 4 * NW].reshape(nsm, NW, 4) / 1e3
+    wt = tsb[:, 8:8 + 4 * NW].reshape(nsm, NW, 4) / 1965.0   # SM cycles -> us
     print("per-CTA us (start, prologue done, producer done, consumers done, end) min/median/max:")
     for k, nm in enumerate(["start", "prologue", "producer", "loop_end", "end"]):
         print(f"  {nm:9s} {np.nanmin(st[:, k]):7.2f} {np.nanmedian(st[:, k]):7.2f} {np.nanmax(st[:, k]):7.2f}")
-    print("per-warp us (full-wait, compute, epilogue) mean/max:", np.round(wt[:, :, :3].mean((0, 1)), 2), np.round(wt[:, :, :3].max((0, 1)), 2))
-    print("epilogue CTA merge / ticket+merge us mean/max:", np.round(tsb[:, 68:70].mean(0) / 1e3, 2), np.round(tsb[:, 68:70].max(0) / 1e3, 2))
+    print("per-warp us (full-wait, compute, epilogue, loop total) mean/max:", np.round(wt[:, :, :4].mean((0, 1)), 2), np.round(wt[:, :, :4].max((0, 1)), 2))
+    print("epilogue CTA merge / ticket+merge us mean/max:", np.round(tsb[:, 68:70].mean(0) / 1965.0, 2), np.round(tsb[:, 68:70].max(0) / 1965.0, 2))
     print("items per CTA min/max:", tsb[:, 5].min(), tsb[:, 5].max())
+    for k, nm in ((62, "producer start"), (60, "first publish"), (61, "warp0 loop start")):
+        v = (tsb[:, k] - t0) / 1e3
+        print(f"  {nm:18s} min/median/max us: {v.min():.2f} {np.median(v):.2f} {v.max():.2f}")
     dur = (tsb[:, 4] - tsb[:, 0]) / 1e3
     order = np.argsort(-dur)
-    print("slowest CTAs: (cta, end us, loop_end us, producer us, last?, k, items)")
-    for cta in order[:10]:
-        print("   ", cta, round(st[cta, 4], 2), round(st[cta, 3], 2), round(st[cta, 2], 2), int(tsb[cta, 6]), int(tsb[cta, 7]), int(tsb[cta, 5]))
+    print("CTAs by loop end: (cta, end us, loop_end us, producer us, last?, k, items, class counts 2/4/8/16/rest)")
+    lo = np.argsort(-st[:, 3])
+    for cta in list(lo[:8]) + list(lo[-4:]):
+        print("   ", cta, round(st[cta, 4], 2), round(st[cta, 3], 2), round(st[cta, 2], 2), int(tsb[cta, 6]), int(tsb[cta, 7]), int(tsb[cta, 5]), tsb[cta, 63:68].astype(int).tolist())
+    # least-squares per-class item time (CTA-level us per item): loop duration ~ sum n_k t_k + c
+    n = tsb[:, 63:68]
+    dur_loop = st[:, 3] - (tsb[:, 61] - t0) / 1e3
+    A = np.concatenate([n, np.ones((nsm, 1))], 1)
+    ok = np.isfinite(dur_loop)
+    sol, *_ = np.linalg.lstsq(A[ok], dur_loop[ok], rcond=None)
+    print("fit us/item (2,4,8,16,rest) + const:", np.round(sol, 4), " resid rms", round(float(np.sqrt(np.mean((A[ok] @ sol - dur_loop[ok]) ** 2))), 3))
     for cta in (0, 77):
         ref = tsb[cta, 70]
         pi = tsb[cta, 72:136]; fd = tsb[cta, 136:200]
