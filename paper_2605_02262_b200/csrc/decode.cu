@@ -44,6 +44,9 @@ constexpr int64_t MIN_CTA_BYTES = 49152;
 #ifndef WQ_DEC_KSCALE
 #define WQ_DEC_KSCALE 0                  // K side: A = s*code (fp16, one rounding), B = q (experiment)
 #endif
+#ifndef WQ_DEC_PROFILE
+#define WQ_DEC_PROFILE 0                 // per-CTA timestamps into the workspace (debug & 8)
+#endif
 #ifndef WQ_DEC_STAGE
 #define WQ_DEC_STAGE 32768
 #endif
@@ -304,7 +307,7 @@ WQ_DEV void softmax_tiles(float (&s)[NT][4], WarpState &st, float (&o)[KT][4],
 // (HMUL2 + exact-residual HFMA2) and the bias q.mn accumulates on the tensor core;
 // each tile keeps independent hi/lo accumulators (short dependency chains).
 template <int D, int S, int BITS>
-WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float scale2,
+WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
                       WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane) {
   constexpr int NTT = S / 16;
   constexpr int CH = (BITS == 16 || NTT < 2) ? 1 : 2;
@@ -328,21 +331,22 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
       for (int i = 0; i < 4; i++) { ah[t][i] = 0.f; al[t][i] = 0.f; }
 #pragma unroll
     for (int kt = 0; kt < KT; kt++) {
+      const uint2 qk = lds64(qs + (kt * 32 + lane) * 8);   // q fragment (B operand) of k-tile kt
       uint32_t h0 = 0, h1 = 0, l0 = 0, l1 = 0;
       if constexpr (BITS < 16 && WQ_DEC_KSCALE) {
         const uint4 pr = lds128(kp + (q * KT + kt) * 16);   // {s01, s89, mn01, mn89}
         if (c0 == 0) {
           const uint32_t am[4] = {pr.z, pr.z, pr.w, pr.w};
-          if (kt & 1) mma16816(b1, am, qf[kt][0], qf[kt][1], b1);
-          else mma16816(b0, am, qf[kt][0], qf[kt][1], b0);
+          if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
+          else mma16816(b0, am, qk.x, qk.y, b0);
         }
 #pragma unroll
         for (int t = 0; t < CH; t++) {
           uint32_t a[4];
 #pragma unroll
           for (int r = 0; r < 4; r++) a[r] = deq_pair_s<BITS>(wk[t], 4 * kt + r, (r < 2) ? pr.x : pr.y);
-          if (kt & 1) mma16816(al[t], a, qf[kt][0], qf[kt][1], al[t]);
-          else mma16816(ah[t], a, qf[kt][0], qf[kt][1], ah[t]);
+          if (kt & 1) mma16816(al[t], a, qk.x, qk.y, al[t]);
+          else mma16816(ah[t], a, qk.x, qk.y, ah[t]);
         }
         continue;
       }
@@ -350,14 +354,14 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
         const uint4 pr = lds128(kp + (q * KT + kt) * 16);   // {s01, s89, mn01, mn89}
         if (c0 == 0) {
           const uint32_t am[4] = {pr.z, pr.z, pr.w, pr.w};
-          if (kt & 1) mma16816(b1, am, qf[kt][0], qf[kt][1], b1);
-          else mma16816(b0, am, qf[kt][0], qf[kt][1], b0);
+          if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
+          else mma16816(b0, am, qk.x, qk.y, b0);
         }
-        h0 = hmul2u(qf[kt][0], pr.x);
-        h1 = hmul2u(qf[kt][1], pr.y);
+        h0 = hmul2u(qk.x, pr.x);
+        h1 = hmul2u(qk.y, pr.y);
         if constexpr (WQ_DEC_QLO) {
-          l0 = h2u(__hfma2(u2h(qf[kt][0]), u2h(pr.x), __hneg2(u2h(h0))));
-          l1 = h2u(__hfma2(u2h(qf[kt][1]), u2h(pr.y), __hneg2(u2h(h1))));
+          l0 = h2u(__hfma2(u2h(qk.x), u2h(pr.x), __hneg2(u2h(h0))));
+          l1 = h2u(__hfma2(u2h(qk.y), u2h(pr.y), __hneg2(u2h(h1))));
         }
       }
 #pragma unroll
@@ -374,8 +378,8 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
             else mma16816(ah[t], a, h0, h1, ah[t]);
           }
         } else {
-          if (kt & 1) mma16816(al[t], a, qf[kt][0], qf[kt][1], al[t]);
-          else mma16816(ah[t], a, qf[kt][0], qf[kt][1], ah[t]);
+          if (kt & 1) mma16816(al[t], a, qk.x, qk.y, al[t]);
+          else mma16816(ah[t], a, qk.x, qk.y, ah[t]);
         }
       }
     }
@@ -415,7 +419,7 @@ WQ_DEV void do_window(const uint8_t *rec, const uint32_t (&qf)[D / 16][2], float
 // FP16 rest tile: K rows [16][D] at Kb, V rows [16][D] at Vb (unpadded rows as the
 // bulk copies land them; rows past ntok hold stale bytes and are masked)
 template <int D>
-WQ_DEV void do_rest(const uint8_t *Kb, const uint8_t *Vb, int ntok, const uint32_t (&qf)[D / 16][2], float scale2,
+WQ_DEV void do_rest(const uint8_t *Kb, const uint8_t *Vb, int ntok, const uint8_t *qs, float scale2,
                     WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane) {
   constexpr int KT = D / 16;
   constexpr int RPH = D;                           // row stride (halves)
@@ -425,9 +429,10 @@ WQ_DEV void do_rest(const uint8_t *Kb, const uint8_t *Vb, int ntok, const uint32
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int kt = 0; kt < KT; kt++) {
+    const uint2 qk = lds64(qs + (kt * 32 + lane) * 8);
     uint32_t a[4];
     ldsm_x4(a, Ks + ((mi & 1) * 8 + rr) * RPH + 16 * kt + (mi >> 1) * 8);
-    mma16816(acc, a, qf[kt][0], qf[kt][1], acc);
+    mma16816(acc, a, qk.x, qk.y, acc);
   }
   float sc[1][4];
   sc[0][0] = g < ntok ? acc[0] * scale2 : -INFINITY;
@@ -486,7 +491,8 @@ struct DecodeSmem {
   static constexpr int NUS = 4;                          // entry ring published by the producer
   static constexpr size_t ring = (size_t)NST * STAGE;
   static constexpr size_t scratch_off = ring;
-  static constexpr size_t ep_off = scratch_off + (size_t)NCW * SCRATCH;
+  static constexpr size_t q_off = scratch_off + (size_t)NCW * SCRATCH;     // q fragments [KT][32][2]
+  static constexpr size_t ep_off = q_off + (size_t)KT * 32 * 8;
   static constexpr size_t units_off = ep_off + (size_t)NCW * EPW * 4;
   static constexpr size_t ent_off = units_off + (size_t)(MAX_UNITS + 1) * 8;
   static constexpr size_t plan_off = ent_off + NUS * sizeof(Entry);
@@ -518,7 +524,8 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int U = a.B * a.H;
-  uint64_t *ts = a.ws_ts ? a.ws_ts + (size_t)blockIdx.x * TS_PER_CTA : nullptr;
+  // timestamps only in profiling builds (WQ_DEC_PROFILE=1, tools/dbg_decode_time.py)
+  uint64_t *ts = (WQ_DEC_PROFILE && a.ws_ts) ? a.ws_ts + (size_t)blockIdx.x * TS_PER_CTA : nullptr;
   if (ts && tid == 0) ts[0] = gtime();
 
   // ---- prologue (warp 0): unit cost prefix, then this CTA's share ----
@@ -706,7 +713,8 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   float *ep = reinterpret_cast<float *>(sm + SM::ep_off);
   const int g = lane >> 2, q = lane & 3;
   const int grp = a.grp;
-  uint32_t qf[KT][2];
+  uint8_t *qs = sm + SM::q_off;
+  uint32_t qf[KT][2];                             // warp 0: q of the next unit, staged to qs
   float o[KT][4];
   WarpState st;
   int uidx = 0, sg = 0;
@@ -721,8 +729,15 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       qf[kt][1] = g < grp ? *reinterpret_cast<const uint32_t *>(qrow + 16 * kt + 2 * q + 8) : 0u;
     }
   };
-  int qu = cp->ua;                                // prefetch q of the first unit while the
-  if (qu < U) load_q(qu);                         // producer plans and issues the first copy
+  // warp 0 stages q of the first unit (cp->ua) while the producer plans and issues
+  // the first copy; later entries restage at their start
+  auto stage_q = [&](int uq) {
+    load_q(uq);
+#pragma unroll
+    for (int kt = 0; kt < KT; kt++)
+      *reinterpret_cast<uint2 *>(qs + (kt * 32 + lane) * 8) = make_uint2(qf[kt][0], qf[kt][1]);
+  };
+  if (warp == 0 && cp->ua < U) stage_q(cp->ua);
   for (;;) {
     const Entry &E = ent[uidx % SM::NUS];
     while (*reinterpret_cast<const volatile int *>(&E.tag) != uidx) {
@@ -732,7 +747,8 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
     if (u < 0) break;
     const int c0 = E.c0, c1 = E.c1, rl = E.rl, nslots = E.nslots;
     const int b = u / a.H, h = u % a.H;
-    if (u != qu) { load_q(u); qu = u; }
+    if (warp == 0 && uidx > 0) stage_q(u);        // (entries after the first: unit ua + uidx)
+    named_bar_sync(2, NCW * 32);
 #pragma unroll
     for (int mt = 0; mt < KT; mt++) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
     st.m[0] = st.m[1] = -INFINITY;
@@ -766,17 +782,17 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
           if (a.debug & 1) {
             st.l[0] += (float)lds32(rec + 16 * lane);
           } else if (p == 0) {
-            do_window<D, S, 2>(rec, qf, a.scale_log2, st, o, scratch, lane);
+            do_window<D, S, 2>(rec, qs, a.scale_log2, st, o, scratch, lane);
           } else if (p == 1) {
-            do_window<D, S, 4>(rec, qf, a.scale_log2, st, o, scratch, lane);
+            do_window<D, S, 4>(rec, qs, a.scale_log2, st, o, scratch, lane);
           } else if (p == 2) {
-            do_window<D, S, 8>(rec, qf, a.scale_log2, st, o, scratch, lane);
+            do_window<D, S, 8>(rec, qs, a.scale_log2, st, o, scratch, lane);
           } else if (p == 3) {
-            do_window<D, S, 16>(rec, qf, a.scale_log2, st, o, scratch, lane);
+            do_window<D, S, 16>(rec, qs, a.scale_log2, st, o, scratch, lane);
           } else {
             const int ii = lo + t * cap + k;
             do_rest<D>(sbase + (size_t)k * 32 * D, sbase + (size_t)(cap + k) * 32 * D, min(16, rl - 16 * (ii - nslots)),
-                       qf, a.scale_log2, st, o, scratch, lane);
+                       qs, a.scale_log2, st, o, scratch, lane);
           }
         }
         __syncwarp();
@@ -885,7 +901,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         float mM[EPT_], mL[EPT_], mO[EPT_];
 #pragma unroll
         for (int e = 0; e < EPT_; e++) { mM[e] = -INFINITY; mL[e] = 0.f; mO[e] = 0.f; }
-        constexpr int CHP = 10;                   // partials per load batch
+        constexpr int CHP = 4;                    // partials per load batch
         constexpr int EPT = (8 * D + NCW * 32 - 1) / (NCW * 32);   // elements per thread (max)
         for (int b0 = 0; b0 < np || b0 == 0; b0 += CHP) {
           // (the common case np <= CHP is one pass with every load of the thread in flight)

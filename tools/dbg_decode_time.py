@@ -1,6 +1,7 @@
 """Per-CTA globaltimer stamps of C5-shaped decode launches (WQ_DECODE_DEBUG bit 8 plus
 optional mode bits from DBG, e.g. DBG=19 for the no-copy/no-math/no-epilogue skeleton)."""
 import math, sys, os
+os.environ.setdefault("WQ_VARIANT", "prof")   # timestamps need a WQ_DEC_PROFILE=1 build
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2605_02262_b200 import configs, synth, wq
