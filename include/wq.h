@@ -98,11 +98,13 @@ typedef struct {
  *
  * K params (per channel c over the window's S tokens, Q19): 4 x d/16 groups
  * of 16 bytes, group (q, m) at byte (q*(d/16) + m)*16 holds fp16
- *   { s(c0), s(c0+1), s(c0+8), s(c0+9), mn(c0), mn(c0+1), mn(c0+8), mn(c0+9) },
- *   c0 = 16*m + 2*q.
+ *   { mn(c0), mn(c0+1), s(c0), s(c0+1), mn(c0+8), mn(c0+9), s(c0+8), s(c0+9) },
+ *   c0 = 16*m + 2*q  (one 16-byte load is directly the mma A fragment of the
+ *   zero-point term: rows g hold mn, rows g+8 are ignored).
  * V params (per token t over the d channels, Q19): S/16 x 4 groups of 16 B,
- * group (i, q) at byte (4*i + q)*16 holds the same pattern for tokens
- *   t0 = 16*i + 2*q of the window.
+ * group (i, q) at byte (4*i + q)*16 holds fp16
+ *   { s(t0), s(t0+1), s(t0+8), s(t0+9), mn(t0), mn(t0+1), mn(t0+8), mn(t0+9) },
+ *   t0 = 16*i + 2*q (token index within the window).
  *
  * Quantizer (Eq.14-16, reading Q17/Q18/Q21).  Per group x[0..n),
  * q_max = 2^b - 1, all arithmetic IEEE fp32 with one rounding per operation:

@@ -77,6 +77,7 @@ def lib():
                 "wqo_layer_layout": (None, [C.POINTER(Geom), P, P]),
                 "wqo_quantize_group": (None, [P, I32, I64, I32, P, P, P]),
                 "wqo_code_pos": (None, [I32, I32, I32, I32, I32, P, P]),
+                "wqo_param_pos": (C.c_int64, [I32, I32, I32, I32]),
                 "wqo_reorder_quantize_pack": (None, [P, P, P, I32, C.POINTER(Geom), P, I32, P, P, P]),
                 "wqo_dequant_record": (None, [P, I32, I32, I32, P, P]),
                 "wqo_decode_attention": (None, [P, P, P, P, P, I32, C.POINTER(Geom), P, P, P, P,
@@ -203,6 +204,11 @@ def quantize_group(x: np.ndarray, bits: int):
     codes = np.zeros(len(x), np.uint8)
     lib().wqo_quantize_group(_p(x), len(x), 1, bits, _p(s), _p(mn), _p(codes))
     return int(s[0]), int(mn[0]), codes
+
+
+def param_pos(is_v, d, i, is_min):
+    """Byte offset of K channel / V token i's scale (is_min=0) or zero point inside the params."""
+    return int(lib().wqo_param_pos(is_v, d, i, is_min))
 
 
 def code_pos(is_v, d, b, t, c):

@@ -387,11 +387,14 @@ static uint16_t get_u16(const uint8_t *p) { return (uint16_t)(p[0] | (p[1] << 8)
 /* byte offset of the (s, mn) of K channel c / V token t inside the params */
 static int64_t kparam_off(int d, int c, int is_min) {
   int m = c / 16, q = (c % 8) / 2, h = (c % 16) / 8, e = c % 2;
-  return ((int64_t)q * (d / 16) + m) * 16 + 2 * ((is_min ? 4 : 0) + 2 * h + e);
+  return ((int64_t)q * (d / 16) + m) * 16 + 2 * (4 * h + (is_min ? 0 : 2) + e);
 }
 static int64_t vparam_off(int t, int is_min) {
   int i = t / 16, col = t % 16, q = (col % 8) / 2, h = col / 8, e = col % 2;
   return ((int64_t)4 * i + q) * 16 + 2 * ((is_min ? 4 : 0) + 2 * h + e);
+}
+int64_t wqo_param_pos(int32_t is_v, int32_t d, int32_t i, int32_t is_min) {
+  return is_v ? vparam_off(i, is_min) : kparam_off(d, i, is_min);
 }
 
 static int64_t slot_offset(const wqo_geom *g, const int32_t *so, int slot, int *bits_out) {

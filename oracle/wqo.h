@@ -66,6 +66,9 @@ void wqo_quantize_group(const uint16_t *x, int32_t n, int64_t stride, int32_t bi
 
 /* Position of element (row, col) of a code tile (D-1): byte offset of its
  * 32-bit word inside the tile and its bit offset inside that word. */
+/* Byte offset of the fp16 scale (is_min = 0) or zero point (is_min = 1) of K
+ * channel i (is_v = 0) or V token i (is_v = 1) inside a record's params (D-1). */
+int64_t wqo_param_pos(int32_t is_v, int32_t d, int32_t i, int32_t is_min);
 void wqo_code_pos(int32_t is_v, int32_t d, int32_t b, int32_t t, int32_t c,
                   int64_t *byte_off, int32_t *bit);
 

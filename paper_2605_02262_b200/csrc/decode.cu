@@ -18,8 +18,9 @@
 //    D-1 fragment order straight into MMA A registers and turned into exact fp16
 //    integers with one LOP3 + one HSUB2 per pair (magic-exponent trick).  Online
 //    softmax per window in the exp2 domain with a lazy rescale (max may run 2^8
-//    ahead).  V side: o[c][j] += sum_t vcode[t][c] * p'_j[t], p' = p*s_t, the
-//    per-token zero point contributing sum_t p_t*mn_t to every channel.
+//    ahead).  V side: o[c][j] += sum_t (vcode[t][c] - 2^(b-1)) * p'_j[t], p' = p*s_t
+//    (centered codes halve the fp16 rounding of p' in the result), the per-token
+//    zero point mn_t + s_t*2^(b-1) contributing sum_t p_t*(mn_t + s_t 2^(b-1)) in fp32.
 //  * Unit epilogue: warps merged in shared memory, the CTA partial (m, l, o) goes
 //    to the workspace, and the last CTA of the unit (atomic ticket) merges all
 //    partials by log-sum-exp and writes out / partial (Q24).
@@ -40,9 +41,6 @@ constexpr int MAX_UNITS = 1024;         // B * H
 constexpr int64_t MIN_CTA_BYTES = 49152;
 #ifndef WQ_DEC_QLO
 #define WQ_DEC_QLO 1                     // carry q*s as fp16 hi + lo (0: hi only, experiment)
-#endif
-#ifndef WQ_DEC_KSCALE
-#define WQ_DEC_KSCALE 0                  // K side: A = s*code (fp16, one rounding), B = q (experiment)
 #endif
 #ifndef WQ_DEC_PROFILE
 #define WQ_DEC_PROFILE 0                 // per-CTA timestamps into the workspace (debug & 8)
@@ -156,64 +154,35 @@ struct WarpState {
 // -------------------------------------------------------------------------------------
 // consumer: one window (BITS in {2,4,8,16}) or one rest tile
 // -------------------------------------------------------------------------------------
-// Exact fp16 value pair of pair-slot P (compile-time after unrolling) of a lane chunk.
-template <int BITS>
+// Exact fp16 value pair of pair-slot P (compile-time after unrolling) of a lane chunk
+// (CENTER: code - 2^(BITS-1), the V side).
+template <int BITS, bool CENTER = false>
 WQ_DEV uint32_t deq_pair(const uint32_t *wd, int P) {
   constexpr int PPW = 16 / BITS;
   const uint32_t w = wd[P / PPW];
   if constexpr (BITS == 16) {
     return w;
   } else if constexpr (BITS == 8) {
-    return (P % 2) == 0 ? dq_pair<8, 0>(w, 0) : dq_pair<8, 1>(w, 0);
+    return (P % 2) == 0 ? dq_pair8<0, CENTER>(w) : dq_pair8<1, CENTER>(w);
   } else if constexpr (BITS == 4) {
     const uint32_t w8 = w >> 8;
     switch (P % 4) {
-      case 0: return dq_pair<4, 0>(w, w8);
-      case 1: return dq_pair<4, 1>(w, w8);
-      case 2: return dq_pair<4, 2>(w, w8);
-      default: return dq_pair<4, 3>(w, w8);
+      case 0: return dq_pair<4, 0, CENTER>(w, w8);
+      case 1: return dq_pair<4, 1, CENTER>(w, w8);
+      case 2: return dq_pair<4, 2, CENTER>(w, w8);
+      default: return dq_pair<4, 3, CENTER>(w, w8);
     }
   } else {
     const uint32_t w8 = w >> 8;
     switch (P % 8) {
-      case 0: return dq_pair<2, 0>(w, w8);
-      case 1: return dq_pair<2, 1>(w, w8);
-      case 2: return dq_pair<2, 2>(w, w8);
-      case 3: return dq_pair<2, 3>(w, w8);
-      case 4: return dq_pair<2, 4>(w, w8);
-      case 5: return dq_pair<2, 5>(w, w8);
-      case 6: return dq_pair<2, 6>(w, w8);
-      default: return dq_pair<2, 7>(w, w8);
-    }
-  }
-}
-
-// s * code of pair P (scales s: the pair's two channels), K side of WQ_DEC_KSCALE
-template <int BITS>
-WQ_DEV uint32_t deq_pair_s(const uint32_t *wd, int P, uint32_t s) {
-  constexpr int PPW = 16 / BITS;
-  const uint32_t w = wd[P / PPW];
-  if constexpr (BITS == 8) {
-    return hmul2u(deq_pair<8>(wd, P), s);
-  } else if constexpr (BITS == 4) {
-    const uint32_t w8 = w >> 8;
-    switch (P % 4) {
-      case 0: return dq_pair_scaled<4, 0>(w, w8, s);
-      case 1: return dq_pair_scaled<4, 1>(w, w8, s);
-      case 2: return dq_pair_scaled<4, 2>(w, w8, s);
-      default: return dq_pair_scaled<4, 3>(w, w8, s);
-    }
-  } else {
-    const uint32_t w8 = w >> 8;
-    switch (P % 8) {
-      case 0: return dq_pair_scaled<2, 0>(w, w8, s);
-      case 1: return dq_pair_scaled<2, 1>(w, w8, s);
-      case 2: return dq_pair_scaled<2, 2>(w, w8, s);
-      case 3: return dq_pair_scaled<2, 3>(w, w8, s);
-      case 4: return dq_pair_scaled<2, 4>(w, w8, s);
-      case 5: return dq_pair_scaled<2, 5>(w, w8, s);
-      case 6: return dq_pair_scaled<2, 6>(w, w8, s);
-      default: return dq_pair_scaled<2, 7>(w, w8, s);
+      case 0: return dq_pair<2, 0, CENTER>(w, w8);
+      case 1: return dq_pair<2, 1, CENTER>(w, w8);
+      case 2: return dq_pair<2, 2, CENTER>(w, w8);
+      case 3: return dq_pair<2, 3, CENTER>(w, w8);
+      case 4: return dq_pair<2, 4, CENTER>(w, w8);
+      case 5: return dq_pair<2, 5, CENTER>(w, w8);
+      case 6: return dq_pair<2, 6, CENTER>(w, w8);
+      default: return dq_pair<2, 7, CENTER>(w, w8);
     }
   }
 }
@@ -244,7 +213,7 @@ WQ_DEV void tile_pv(const uint32_t (&wd)[D * BITS / 64], uint32_t pb0, uint32_t 
   for (int mt = 0; mt < KT; mt++) {
     uint32_t a[4];
 #pragma unroll
-    for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS>(wd, 4 * mt + r);
+    for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS, true>(wd, 4 * mt + r);
     mma16816(o[mt], a, pb0, pb1, o[mt]);
   }
 }
@@ -333,35 +302,20 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
     for (int kt = 0; kt < KT; kt++) {
       const uint2 qk = lds64(qs + (kt * 32 + lane) * 8);   // q fragment (B operand) of k-tile kt
       uint32_t h0 = 0, h1 = 0, l0 = 0, l1 = 0;
-      if constexpr (BITS < 16 && WQ_DEC_KSCALE) {
-        const uint4 pr = lds128(kp + (q * KT + kt) * 16);   // {s01, s89, mn01, mn89}
-        if (c0 == 0) {
-          const uint32_t am[4] = {pr.z, pr.z, pr.w, pr.w};
-          if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
-          else mma16816(b0, am, qk.x, qk.y, b0);
-        }
-#pragma unroll
-        for (int t = 0; t < CH; t++) {
-          uint32_t a[4];
-#pragma unroll
-          for (int r = 0; r < 4; r++) a[r] = deq_pair_s<BITS>(wk[t], 4 * kt + r, (r < 2) ? pr.x : pr.y);
-          if (kt & 1) mma16816(al[t], a, qk.x, qk.y, al[t]);
-          else mma16816(ah[t], a, qk.x, qk.y, ah[t]);
-        }
-        continue;
-      }
       if constexpr (BITS < 16) {
-        const uint4 pr = lds128(kp + (q * KT + kt) * 16);   // {s01, s89, mn01, mn89}
+        // {mn01, s01, mn89, s89}: the quad is the zero-point term's A fragment as
+        // loaded (rows g: mn, rows g+8: don't-care -- only d0/d1 of b0/b1 are used)
+        const uint4 pr = lds128(kp + (q * KT + kt) * 16);
         if (c0 == 0) {
-          const uint32_t am[4] = {pr.z, pr.z, pr.w, pr.w};
+          const uint32_t am[4] = {pr.x, pr.y, pr.z, pr.w};
           if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
           else mma16816(b0, am, qk.x, qk.y, b0);
         }
-        h0 = hmul2u(qk.x, pr.x);
-        h1 = hmul2u(qk.y, pr.y);
+        h0 = hmul2u(qk.x, pr.y);
+        h1 = hmul2u(qk.y, pr.w);
         if constexpr (WQ_DEC_QLO) {
-          l0 = h2u(__hfma2(u2h(qk.x), u2h(pr.x), __hneg2(u2h(h0))));
-          l1 = h2u(__hfma2(u2h(qk.y), u2h(pr.y), __hneg2(u2h(h1))));
+          l0 = h2u(__hfma2(u2h(qk.x), u2h(pr.y), __hneg2(u2h(h0))));
+          l1 = h2u(__hfma2(u2h(qk.y), u2h(pr.w), __hneg2(u2h(h1))));
         }
       }
 #pragma unroll
@@ -387,7 +341,7 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
 #pragma unroll
     for (int t = 0; t < CH; t++)
 #pragma unroll
-      for (int i = 0; i < 4; i++) sc[t][i] = ((ah[t][i] + al[t][i]) + (b0[i] + b1[i])) * scale2;
+      for (int i = 0; i < 4; i++) sc[t][i] = ((ah[t][i] + al[t][i]) + (b0[i & 1] + b1[i & 1])) * scale2;
     float vs[CH][2], vm[CH][2];
     if constexpr (BITS < 16) {
       const uint8_t *vp = kp + 4 * D;
@@ -398,8 +352,10 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
         const uint32_t sh = (g & 1) * 16;
         vs[t][0] = __half2float(__ushort_as_half((unsigned short)(pr.x >> sh)));
         vs[t][1] = __half2float(__ushort_as_half((unsigned short)(pr.y >> sh)));
-        vm[t][0] = __half2float(__ushort_as_half((unsigned short)(pr.z >> sh)));
-        vm[t][1] = __half2float(__ushort_as_half((unsigned short)(pr.w >> sh)));
+        // centered V codes (code - 2^(BITS-1)) move s * 2^(BITS-1) into the fp32 zero-point term
+        constexpr float HALF = (float)(1 << (BITS - 1));
+        vm[t][0] = fmaf(vs[t][0], HALF, __half2float(__ushort_as_half((unsigned short)(pr.z >> sh))));
+        vm[t][1] = fmaf(vs[t][1], HALF, __half2float(__ushort_as_half((unsigned short)(pr.w >> sh))));
       }
     }
     softmax_tiles<CH, KT>(sc, st, o, vs, vm, BITS < 16, scratch, lane);

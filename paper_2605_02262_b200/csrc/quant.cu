@@ -205,8 +205,8 @@ WQ_DEV void quant_window(const __half *Ks, const __half *Vs, float2 *kp2, float2
         kp2[c] = make_float2(mn, __frcp_rn(__half2float(s16)));
         int m = c / 16, q = (c % 8) / 2, hh = (c % 16) / 8;
         __half *grp = reinterpret_cast<__half *>(params + (q * (D / 16) + m) * 16);
-        grp[2 * hh + e] = s16;
-        grp[4 + 2 * hh + e] = __float2half_rn(mn);
+        grp[4 * hh + e] = __float2half_rn(mn);      // D-1 K group {mn01, s01, mn89, s89}
+        grp[4 * hh + 2 + e] = s16;
       }
     }
   }

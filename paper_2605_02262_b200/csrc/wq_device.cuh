@@ -148,9 +148,10 @@ WQ_DEV uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t magic) {
 // Exact fp16 values of the two codes of pair slot P in word w (D-1 packing):
 // element e sits at bit 16*e + BITS*j.  A code at bit p of each half is ORed into
 // the mantissa of 2^(10-p)*(1 + .) (exponent field 25 - p), giving 2^(10-p) + code
-// exactly; subtracting 2^(10-p) leaves the code.  Positions p + BITS <= 10 only;
-// higher slots use the word shifted right by 8.
-template <int BITS, int J>
+// exactly; subtracting 2^(10-p) leaves the code (CENTER: subtracting
+// 2^(10-p) + 2^(BITS-1) leaves code - 2^(BITS-1), also exact).  Positions
+// p + BITS <= 10 only; higher slots use the word shifted right by 8.
+template <int BITS, int J, bool CENTER = false>
 WQ_DEV uint32_t dq_pair(uint32_t w, uint32_t w8) {
   constexpr int SLOT_BITS = BITS * J;
   constexpr bool HI = (SLOT_BITS + BITS > 10);
@@ -159,45 +160,18 @@ WQ_DEV uint32_t dq_pair(uint32_t w, uint32_t w8) {
   constexpr uint32_t MASK = MASK1 | (MASK1 << 16);
   constexpr uint32_t MAG1 = (uint32_t)(25 - P) << 10;
   constexpr uint32_t MAG = MAG1 | (MAG1 << 16);
+  constexpr uint32_t SUB1 = MAG1 | (CENTER ? (1u << (BITS - 1)) << P : 0u);
+  constexpr uint32_t SUB = SUB1 | (SUB1 << 16);
   uint32_t x = lop3_and_or(HI ? w8 : w, MASK, MAG);
-#ifdef WQ_DEC_NOSUB
-  return x;                                     // timing experiment only (wrong values)
-#else
-  return h2u(__hsub2(u2h(x), u2h(MAG)));
-#endif
+  return h2u(__hsub2(u2h(x), u2h(SUB)));
 }
-// s * code of pair slot J, rounded once: fma(2^(10-p) + code, s, -2^(10-p) * s);
-// the constant is exact while 2^(10-p) * s stays finite in fp16.
-template <int BITS, int J>
-WQ_DEV uint32_t dq_pair_scaled(uint32_t w, uint32_t w8, uint32_t s) {
-  constexpr int SLOT_BITS = BITS * J;
-  constexpr bool HI = (SLOT_BITS + BITS > 10);
-  constexpr int P = HI ? SLOT_BITS - 8 : SLOT_BITS;
-  constexpr uint32_t MASK1 = ((1u << BITS) - 1u) << P;
-  constexpr uint32_t MASK = MASK1 | (MASK1 << 16);
-  constexpr uint32_t MAG1 = (uint32_t)(25 - P) << 10;
-  constexpr uint32_t MAG = MAG1 | (MAG1 << 16);
-  const uint32_t x = lop3_and_or(HI ? w8 : w, MASK, MAG);
-  const uint32_t c = h2u(__hmul2(u2h(s), u2h(MAG ^ 0x80008000u)));
-  return h2u(__hfma2(u2h(x), u2h(s), u2h(c)));
-}
-template <>
-WQ_DEV uint32_t dq_pair<8, 0>(uint32_t w, uint32_t) {
+// 8-bit codes: bytes 0/2 (J = 0) or 1/3 (J = 1) under the exponent byte 0x64 -> 1024 + code
+template <int J, bool CENTER = false>
+WQ_DEV uint32_t dq_pair8(uint32_t w) {
   uint32_t x;
-  asm("prmt.b32 %0, %1, %2, 0x7250;" : "=r"(x) : "r"(w), "r"(0x64646464u));  // [b0,0x64,b2,0x64]
-#ifdef WQ_DEC_NOSUB
-  return x;
-#endif
-  return h2u(__hsub2(u2h(x), u2h(0x64006400u)));
-}
-template <>
-WQ_DEV uint32_t dq_pair<8, 1>(uint32_t w, uint32_t) {
-  uint32_t x;
-  asm("prmt.b32 %0, %1, %2, 0x7351;" : "=r"(x) : "r"(w), "r"(0x64646464u));  // [b1,0x64,b3,0x64]
-#ifdef WQ_DEC_NOSUB
-  return x;
-#endif
-  return h2u(__hsub2(u2h(x), u2h(0x64006400u)));
+  if constexpr (J == 0) asm("prmt.b32 %0, %1, %2, 0x7250;" : "=r"(x) : "r"(w), "r"(0x64646464u));
+  else asm("prmt.b32 %0, %1, %2, 0x7351;" : "=r"(x) : "r"(w), "r"(0x64646464u));
+  return h2u(__hsub2(u2h(x), u2h(CENTER ? 0x64806480u : 0x64006400u)));
 }
 
 WQ_DEV float warp_max(float v, int xor_from = 1) {

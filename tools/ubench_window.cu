@@ -29,8 +29,10 @@ __global__ void __launch_bounds__(512, 1) kbench(int iters, unsigned long long *
   }
   __syncthreads();
   uint8_t *scratch = sm + 4 * REC + warp * 512;
-  uint32_t qf[KT][2];
-  for (int kt = 0; kt < KT; kt++) { qf[kt][0] = 0x3c003c00u ^ (lane * kt); qf[kt][1] = 0x38003800u; }
+  uint8_t *qs = sm + 4 * REC + 16 * 512;          // q fragment table [KT][32][2]
+  if (warp == 0)
+    for (int kt = 0; kt < KT; kt++)
+      *reinterpret_cast<uint2 *>(qs + (kt * 32 + lane) * 8) = make_uint2(0x3c003c00u ^ (lane * kt), 0x38003800u);
   float o[KT][4] = {};
   WarpState st;
   st.m[0] = st.m[1] = -INFINITY;
@@ -38,7 +40,7 @@ __global__ void __launch_bounds__(512, 1) kbench(int iters, unsigned long long *
   const uint8_t *rec = sm + (warp & 3) * REC;
   __syncthreads();
   const unsigned long long t0 = clock64();
-  for (int it = 0; it < iters; it++) do_window<D, S, BITS>(rec, qf, 0.1275f, st, o, scratch, lane);
+  for (int it = 0; it < iters; it++) do_window<D, S, BITS>(rec, qs, 0.1275f, st, o, scratch, lane);
   __syncwarp();
   const unsigned long long t1 = clock64();
   float acc = st.l[0] + st.vb[1];
@@ -51,7 +53,7 @@ template <int BITS>
 void run(int sms, unsigned long long *dc, float *ds) {
   constexpr int D = 128, S = 32;
   constexpr int REC = BITS == 16 ? 4 * S * D : S * D * BITS / 4 + 4 * D + 4 * S;
-  const size_t smem = 4 * REC + 16 * 512;
+  const size_t smem = 4 * REC + 16 * 512 + 2048;
   cudaFuncSetAttribute(kbench<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int iters = 200;
   for (int nw : {1, 2, 4, 8, 11, 12, 16}) {
