@@ -196,14 +196,18 @@ class Workload:
         for t in range(self.n_gen):
             rl = self.rest_len[t] if self.rank == 0 else self.rest_zero
             for l in range(self.L):
+                # every decode but the first after quantize follows work that does not
+                # write the packed cache / offs / seg_off / rest_len: WQ_DECODE_EARLY
+                # lets it plan and prefetch the cache while that work drains (PDL)
+                flags = 0 if (t == 0 and l == 0) else wq.WQ_DECODE_EARLY
                 if self.world == 1:
                     wq.wq_decode_attention(self.q[t, l], self.packed[l], self.offs[l], self.seg_r[l], self.g,
                                            self.kr[l], self.vr[l], rl, self.sm_scale, out=self.out[t, l],
-                                           workspace=self.dws)
+                                           workspace=self.dws, flags=flags)
                 else:
                     wq.wq_decode_attention(self.q[t, l], self.packed[l], self.offs[l], self.seg_r[l], self.g,
                                            self.kr[l], self.vr[l], rl, self.sm_scale, partial=self.part,
-                                           workspace=self.dws)
+                                           workspace=self.dws, flags=flags)
                     torch.distributed.all_gather_into_tensor(self.gathered, self.part, group=group)
                     wq.wq_merge_partials(self.gathered, self.g, out=self.out[t, l])
 

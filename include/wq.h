@@ -207,6 +207,26 @@ wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t s
  * workspace: wq_decode_workspace(g) bytes, zero-filled once.
  * Errors: WQ_ESHAPE (unsupported d/S, Hq/H > 8), WQ_EINVAL (both outputs NULL). */
 wq_status wq_decode_workspace(const wq_geom *g, size_t *bytes_host);
+
+/* wq_decode_attention_ex flags. */
+enum {
+  /* WQ_DECODE_EARLY: the caller guarantees that packed, offs, seg_off_l and
+   * rest_len are NOT written by the work enqueued immediately before this call
+   * on `stream` (e.g. the previous layer's decode).  The kernel is then launched
+   * as a programmatic dependent of that work (PDL): it plans the split-KV
+   * partition and starts streaming the packed cache into shared memory while
+   * that work drains, and touches q, k_rest/v_rest, out, partial and the
+   * workspace only after it has completed.  Without the guarantee, pass 0. */
+  WQ_DECODE_EARLY = 1
+};
+/* wq_decode_attention with flags (WQ_DECODE_*); flags = 0 is wq_decode_attention. */
+wq_status wq_decode_attention_ex(const void *q, const uint8_t *packed, const int64_t *offs,
+                                 const int32_t *seg_off_l, const wq_geom *g,
+                                 const void *k_rest, const void *v_rest,
+                                 const int64_t rest_strides[2], const int32_t *rest_len,
+                                 int32_t R_max, float sm_scale,
+                                 void *out, float *partial,
+                                 void *workspace, size_t workspace_bytes, uint32_t flags, void *stream);
 wq_status wq_decode_attention(const void *q, const uint8_t *packed, const int64_t *offs,
                               const int32_t *seg_off_l, const wq_geom *g,
                               const void *k_rest, const void *v_rest,

@@ -194,6 +194,16 @@ wq_status wq_decode_attention(const void *q, const uint8_t *packed, const int64_
                               const int64_t rest_strides[2], const int32_t *rest_len, int32_t R_max,
                               float sm_scale, void *out, float *partial, void *workspace,
                               size_t workspace_bytes, void *stream) {
+  return wq_decode_attention_ex(q, packed, offs, seg_off_l, g, k_rest, v_rest, rest_strides, rest_len, R_max,
+                                sm_scale, out, partial, workspace, workspace_bytes, 0u, stream);
+}
+
+wq_status wq_decode_attention_ex(const void *q, const uint8_t *packed, const int64_t *offs,
+                                 const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
+                                 const void *v_rest, const int64_t rest_strides[2], const int32_t *rest_len,
+                                 int32_t R_max, float sm_scale, void *out, float *partial, void *workspace,
+                                 size_t workspace_bytes, uint32_t flags, void *stream) {
+  if (flags & ~(uint32_t)WQ_DECODE_EARLY) return fail(WQ_EINVAL, "unknown decode flags 0x%x", flags);
   wq_status s = check_geom(g, true);
   if (s != WQ_OK) return s;
   if (!q || !packed || !offs || !seg_off_l || !workspace) return fail(WQ_EINVAL, "NULL pointer");
@@ -217,6 +227,7 @@ wq_status wq_decode_attention(const void *q, const uint8_t *packed, const int64_
   a.scale_log2 = sm_scale * 1.4426950408889634f;
   { const char *dbg = getenv("WQ_DECODE_DEBUG"); a.debug = dbg ? atoi(dbg) : 0; }
   a.out = (__half *)out; a.partial = partial;
+  a.flags = flags;
   const int grp = a.grp;
   size_t part = (size_t)(sms + g->B * g->H) * grp * (g->d + 2) * sizeof(float);
   part = (part + 255) / 256 * 256;

@@ -48,6 +48,7 @@ constexpr int64_t MIN_CTA_BYTES = 49152;
 #ifndef WQ_DEC_STAGE
 #define WQ_DEC_STAGE 32768
 #endif
+constexpr uint32_t WQ_DECODE_EARLY_ = 1u;     // = WQ_DECODE_EARLY (include/wq.h)
 constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trace
 constexpr float LAZY_TH = 8.0f;         // log2 headroom of the lazy softmax rescale
 constexpr int KIND_REST = 4;
@@ -569,6 +570,9 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   __syncthreads();
   const int G = *s_flag;
   const int c = blockIdx.x;
+  // the next launch on the stream may start its prologue and cache prefetch as soon
+  // as SMs free up (it waits for this grid before touching q / outputs: PDL)
+  if (tid == 0) griddep_launch_dependents();
   if (c >= G) return;
   if (a.debug & 32) return;                       // debug: launch + prologue only
   if (ts && tid == 0) { ts[1] = gtime(); ts[70] = clock64(); }
@@ -646,6 +650,8 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
               bulk_g2s_evict_first(dst, img + gg.cs[p] + (int64_t)(f0 - gg.so[p]) * IG::sz(p), nb, &full[slot], pol);
             } else {
               // rest tiles [f0, f1) = rows [r0, r1): one bulk copy for K, one for V
+              // (the rest buffers may be written by the preceding work: wait for it)
+              if (a.flags & WQ_DECODE_EARLY_) griddep_wait();
               const int r0 = 16 * (f0 - gg.nslots);
               const int r1 = min(gg.rl, 16 * (f1 - gg.nslots));
               const uint32_t nb = (uint32_t)(r1 - r0) * 2u * D;
@@ -693,6 +699,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
     for (int kt = 0; kt < KT; kt++)
       *reinterpret_cast<uint2 *>(qs + (kt * 32 + lane) * 8) = make_uint2(qf[kt][0], qf[kt][1]);
   };
+  if (warp == 0 && (a.flags & WQ_DECODE_EARLY_)) griddep_wait();   // q / outputs / workspace
   if (warp == 0 && cp->ua < U) stage_q(cp->ua);
   for (;;) {
     const Entry &E = ent[uidx % SM::NUS];
@@ -958,11 +965,26 @@ size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms) {
 template <int D, int S>
 static cudaError_t launch_decode_t(const DecodeArgs &a, int num_sms, cudaStream_t st) {
   using SM = DecodeSmem<D, S>;
-  cudaError_t e = cudaFuncSetAttribute(k_decode<D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)SM::total);
-  if (e != cudaSuccess) return e;
-  k_decode<D, S><<<num_sms, DT, SM::total, st>>>(a);
-  return cudaGetLastError();
+  static bool attr_set = false;                  // per instantiation (per process: one device)
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_decode<D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SM::total);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms);
+  cfg.blockDim = dim3(DT);
+  cfg.dynamicSmemBytes = SM::total;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (a.flags & WQ_DECODE_EARLY_) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, k_decode<D, S>, a);
 }
 
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st) {

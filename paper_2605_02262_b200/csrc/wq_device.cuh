@@ -66,6 +66,11 @@ WQ_DEV uint64_t policy_evict_first() {
   return p;
 }
 
+// Programmatic dependent launch (PDL): wait for the prerequisite grid (no-op when the
+// grid was launched without a programmatic dependency); allow dependents to launch.
+WQ_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+WQ_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 WQ_DEV void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

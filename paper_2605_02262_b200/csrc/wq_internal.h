@@ -45,6 +45,7 @@ struct DecodeArgs {
   int B, H, Hq, grp, d, S;
   float scale_log2;          // sm_scale * log2(e)
   int debug;                 // WQ_DECODE_DEBUG: 1 = stream only (no math), profiling aid
+  uint32_t flags;            // WQ_DECODE_* flags (include/wq.h)
   __half *out;
   float *partial;
   float *ws_part;            // [(G + B*H)][grp][d + 2]

@@ -68,6 +68,7 @@ def load(build_if_missing: bool = True):
         "wq_reorder_quantize_pack": [P, P, P, I32, C.POINTER(Geom), P, I32, P, P, P, P],
         "wq_decode_workspace": [C.POINTER(Geom), P],
         "wq_decode_attention": [P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, P, SZ, P],
+        "wq_decode_attention_ex": [P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, P, SZ, C.c_uint32, P],
         "wq_merge_partials": [P, I32, C.POINTER(Geom), P, P],
         "wq_shard_slots": [P, P, I32, I32, I32, I32, P, P, P],
     }
@@ -86,7 +87,7 @@ def load(build_if_missing: bool = True):
 def exported_symbols():
     return ["wq_thresholds", "wq_window_scores_workspace", "wq_window_scores", "wq_assign_bits",
             "wq_packed_bytes", "wq_layer_layout", "wq_reorder_quantize_pack", "wq_decode_workspace",
-            "wq_decode_attention", "wq_merge_partials", "wq_shard_slots", "wq_last_error", "wq_version"]
+            "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_last_error", "wq_version"]
 
 
 def _check(rc: int):
@@ -200,18 +201,24 @@ def wq_decode_workspace(g: Geom) -> int:
     return n.value
 
 
+WQ_DECODE_EARLY = 1
+
+
 def wq_decode_attention(q: torch.Tensor, packed: torch.Tensor, offs: torch.Tensor, seg_off_l: torch.Tensor,
                         g: Geom, k_rest, v_rest, rest_len, sm_scale: float, out=None, partial=None,
-                        workspace=None, stream=None):
-    """q fp16 [B][Hq][d]; k_rest/v_rest fp16 [B][H][R_max][d] (or None); rest_len i32 [B]."""
+                        workspace=None, stream=None, flags: int = 0):
+    """q fp16 [B][Hq][d]; k_rest/v_rest fp16 [B][H][R_max][d] (or None); rest_len i32 [B].
+    flags: WQ_DECODE_EARLY (see include/wq.h) calls wq_decode_attention_ex."""
     if workspace is None:
         workspace = torch.zeros(wq_decode_workspace(g), dtype=torch.uint8, device=q.device)
     R_max = 0 if k_rest is None else k_rest.shape[2]
     rs = (C.c_int64 * 2)(*(k_rest.stride(0), k_rest.stride(1))) if k_rest is not None else None
-    _check(load().wq_decode_attention(_ptr(q), _ptr(packed), _ptr(offs), _ptr(seg_off_l), C.byref(g),
-                                      _ptr(k_rest), _ptr(v_rest), rs, _ptr(rest_len), R_max, float(sm_scale),
-                                      _ptr(out), _ptr(partial), _ptr(workspace), workspace.numel(),
-                                      _stream(stream)))
+    args = (_ptr(q), _ptr(packed), _ptr(offs), _ptr(seg_off_l), C.byref(g), _ptr(k_rest), _ptr(v_rest), rs,
+            _ptr(rest_len), R_max, float(sm_scale), _ptr(out), _ptr(partial), _ptr(workspace), workspace.numel())
+    if flags:
+        _check(load().wq_decode_attention_ex(*args, int(flags), _stream(stream)))
+    else:
+        _check(load().wq_decode_attention(*args, _stream(stream)))
     return out, partial
 
 

@@ -310,3 +310,32 @@ def test_config_layer_parity(orc, name):
         pk = packed[int(offs[b * m.H].item()):int(offs[(b + 1) * m.H].item())]
         r = _decode_ref(orc, sub, gb, ob, pk, perm[b:b + 1], seg[b:b + 1], sm)[0]
         assert rel_err(out[b:b + 1].float().cpu().numpy(), r) <= ATTN_TOL
+
+
+def test_decode_early_flag_matches(orc):
+    """WQ_DECODE_EARLY (programmatic dependent launch after a previous decode on the
+    stream) gives the same bytes as flags = 0, with both launches writing one output."""
+    outs = []
+    for flags in (0, wq.WQ_DECODE_EARLY):
+        res = []
+        for seed in (301, 302, 303):
+            c = small_case(seed, d=128, S=32, W=12, tail=7, B=2, H=4, Hq=28)
+            g = c["g"]
+            sc = wq.wq_window_scores(c["vis"], c["txt"], 32)
+            thr = orc.thresholds([0.45], 2.0, 4)
+            _, _, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
+            offs = wq.wq_layer_layout(g, seg[0])
+            packed = torch.zeros(int(offs[-1].item()) + 16, dtype=torch.uint8, device="cuda")
+            wq.wq_reorder_quantize_pack(c["K"], c["V"], 0, g, perm[0], seg[0], offs, packed)
+            res.append((c, g, offs, packed, seg[0].contiguous()))
+        torch.cuda.synchronize()
+        out = torch.empty((2, 28, 128), dtype=torch.float16, device="cuda")
+        ws = torch.zeros(wq.wq_decode_workspace(res[0][1]), dtype=torch.uint8, device="cuda")
+        got = []
+        for i, (c, g, offs, packed, seg) in enumerate(res):
+            wq.wq_decode_attention(c["q"], packed, offs, seg, g, c["kr"], c["vr"], c["rest_len"], 0.088,
+                                   out=out, workspace=ws, flags=flags if i > 0 else 0)
+            got.append(out.clone())
+        torch.cuda.synchronize()
+        outs.append(torch.stack(got))
+    assert torch.equal(outs[0], outs[1])

@@ -35,10 +35,14 @@ nbytes = sum(int(x[2][-1].item()) for x in layers) / L
 sm = 1 / math.sqrt(m.d)
 
 
+EARLY = int(os.environ.get("EARLY", "0"))
+
+
 def run(n):
     for i in range(n):
         q, packed, offs, s, kr, vr, rl = layers[i % L]
-        wq.wq_decode_attention(q, packed, offs, s, g, kr, vr, rl, sm, out=out, workspace=ws)
+        wq.wq_decode_attention(q, packed, offs, s, g, kr, vr, rl, sm, out=out, workspace=ws,
+                               flags=wq.WQ_DECODE_EARLY if (EARLY and i > 0) else 0)
 
 
 import time
