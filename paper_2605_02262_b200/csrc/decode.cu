@@ -219,10 +219,19 @@ WQ_DEV void tile_pv(const uint32_t (&wd)[D * BITS / 64], uint32_t pb0, uint32_t 
   }
 }
 
-// Online softmax over NT tiles of scores (already in the log2 domain), writes P'
-// (p * s_t) as fp16 [token][8 heads] rows to the warp scratch.
+WQ_DEV float ex2f(float x) {                 // 2^x, MUFU.EX2 (rel. error ~2^-22, denormals flushed)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Online softmax over NT tiles of raw scores t (logit = t * scale2 in the log2
+// domain), writes P' (p * s_t) as fp16 [token][8 heads] rows to the warp scratch.
+// The running max is lazy: a tile only triggers the cross-lane max reduction (and a
+// rescale) when one of its logits exceeds the current max by LAZY_TH, so most
+// windows skip the shuffles (p <= 2^LAZY_TH keeps fp32 sums and fp16 P' in range).
 template <int NT, int KT>
-WQ_DEV void softmax_tiles(float (&s)[NT][4], WarpState &st, float (&o)[KT][4],
+WQ_DEV void softmax_tiles(const float (&s)[NT][4], float scale2, WarpState &st, float (&o)[KT][4],
                           const float (&vs)[NT][2], const float (&vm)[NT][2], bool has_vparams,
                           uint8_t *scratch, int lane) {
   const int g = lane >> 2, q = lane & 3;
@@ -232,17 +241,22 @@ WQ_DEV void softmax_tiles(float (&s)[NT][4], WarpState &st, float (&o)[KT][4],
     mx0 = fmaxf(mx0, fmaxf(s[nt][0], s[nt][2]));
     mx1 = fmaxf(mx1, fmaxf(s[nt][1], s[nt][3]));
   }
+  mx0 *= scale2;
+  mx1 *= scale2;
+  const bool up0 = mx0 > st.m[0] + LAZY_TH || (st.m[0] == -INFINITY && mx0 > -INFINITY);
+  const bool up1 = mx1 > st.m[1] + LAZY_TH || (st.m[1] == -INFINITY && mx1 > -INFINITY);
+  if (__any_sync(0xffffffffu, up0 || up1)) {
 #pragma unroll
-  for (int off = 4; off <= 16; off <<= 1) {
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
-  }
-  const bool n0 = mx0 > st.m[0] + LAZY_TH || (st.m[0] == -INFINITY && mx0 > -INFINITY);
-  const bool n1 = mx1 > st.m[1] + LAZY_TH || (st.m[1] == -INFINITY && mx1 > -INFINITY);
-  if (__any_sync(0xffffffffu, n0 || n1)) {
+    for (int off = 4; off <= 16; off <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+    }
+    // uniform over the 8 lanes of a head after the reduction
+    const bool n0 = mx0 > st.m[0] + LAZY_TH || (st.m[0] == -INFINITY && mx0 > -INFINITY);
+    const bool n1 = mx1 > st.m[1] + LAZY_TH || (st.m[1] == -INFINITY && mx1 > -INFINITY);
     float a0 = 1.f, a1 = 1.f;
-    if (n0) { a0 = exp2f(st.m[0] - mx0); st.m[0] = mx0; }
-    if (n1) { a1 = exp2f(st.m[1] - mx1); st.m[1] = mx1; }
+    if (n0) { a0 = ex2f(st.m[0] - mx0); st.m[0] = mx0; }
+    if (n1) { a1 = ex2f(st.m[1] - mx1); st.m[1] = mx1; }
     st.l[0] *= a0; st.vb[0] *= a0;
     st.l[1] *= a1; st.vb[1] *= a1;
 #pragma unroll
@@ -254,10 +268,10 @@ WQ_DEV void softmax_tiles(float (&s)[NT][4], WarpState &st, float (&o)[KT][4],
   const float m1 = st.m[1] == -INFINITY ? 0.f : st.m[1];
 #pragma unroll
   for (int nt = 0; nt < NT; nt++) {
-    float p0 = exp2f(s[nt][0] - m0);
-    float p1 = exp2f(s[nt][1] - m1);
-    float p2 = exp2f(s[nt][2] - m0);
-    float p3 = exp2f(s[nt][3] - m1);
+    float p0 = ex2f(fmaf(s[nt][0], scale2, -m0));
+    float p1 = ex2f(fmaf(s[nt][1], scale2, -m1));
+    float p2 = ex2f(fmaf(s[nt][2], scale2, -m0));
+    float p3 = ex2f(fmaf(s[nt][3], scale2, -m1));
     st.l[0] += p0 + p2;
     st.l[1] += p1 + p3;
     if (has_vparams) {
@@ -342,7 +356,7 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
 #pragma unroll
     for (int t = 0; t < CH; t++)
 #pragma unroll
-      for (int i = 0; i < 4; i++) sc[t][i] = ((ah[t][i] + al[t][i]) + (b0[i & 1] + b1[i & 1])) * scale2;
+      for (int i = 0; i < 4; i++) sc[t][i] = (ah[t][i] + al[t][i]) + (b0[i & 1] + b1[i & 1]);
     float vs[CH][2], vm[CH][2];
     if constexpr (BITS < 16) {
       const uint8_t *vp = kp + 4 * D;
@@ -359,7 +373,7 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
         vm[t][1] = fmaf(vs[t][1], HALF, __half2float(__ushort_as_half((unsigned short)(pr.w >> sh))));
       }
     }
-    softmax_tiles<CH, KT>(sc, st, o, vs, vm, BITS < 16, scratch, lane);
+    softmax_tiles<CH, KT>(sc, scale2, st, o, vs, vm, BITS < 16, scratch, lane);
 #pragma unroll
     for (int t = 0; t < CH; t++) {
       uint32_t pb[2];
@@ -392,12 +406,12 @@ WQ_DEV void do_rest(const uint8_t *Kb, const uint8_t *Vb, int ntok, const uint8_
     mma16816(acc, a, qk.x, qk.y, acc);
   }
   float sc[1][4];
-  sc[0][0] = g < ntok ? acc[0] * scale2 : -INFINITY;
-  sc[0][1] = g < ntok ? acc[1] * scale2 : -INFINITY;
-  sc[0][2] = g + 8 < ntok ? acc[2] * scale2 : -INFINITY;
-  sc[0][3] = g + 8 < ntok ? acc[3] * scale2 : -INFINITY;
+  sc[0][0] = g < ntok ? acc[0] : -INFINITY;
+  sc[0][1] = g < ntok ? acc[1] : -INFINITY;
+  sc[0][2] = g + 8 < ntok ? acc[2] : -INFINITY;
+  sc[0][3] = g + 8 < ntok ? acc[3] : -INFINITY;
   float vs[1][2], vm[1][2];
-  softmax_tiles<1, KT>(sc, st, o, vs, vm, false, scratch, lane);
+  softmax_tiles<1, KT>(sc, scale2, st, o, vs, vm, false, scratch, lane);
   uint32_t pb[2];
   ldsm_x2_t(pb, scratch + (lane & 15) * 16);
   // zero masked token columns of V^T (stale shared memory may hold non-finite bits)
