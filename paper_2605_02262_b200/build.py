@@ -8,7 +8,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-CSRC = os.path.join(HERE, "csrc")
+CSRC = os.environ.get("WQ_CSRC", os.path.join(HERE, "csrc"))    # experiment builds may point elsewhere
 # Experiment builds: WQ_VARIANT=<name> WQ_NVCC_DEFS="-DX=1 ..." build and load lib/<name>/libwq.so
 # (the same sources with extra defines); unset, the product library lib/libwq.so.
 VARIANT = os.environ.get("WQ_VARIANT", "")

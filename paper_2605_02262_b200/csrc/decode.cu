@@ -67,11 +67,11 @@ struct ItemGeo {
   static constexpr int sz(int k) { return k == 4 ? REST_SZ : (int)rb(k); }
   // Cost of an item ~ its time on one SM inside a full decode launch (the CTA
   // partition balances cost).  Measured per-class CTA-level item times on C5
-  // (tools/dbg_decode_time.py least-squares fit): 2-bit 0.135 us, 4-bit 0.152,
-  // 8-bit 0.177, FP16 0.287 (byte-bound), 16-token rest tile ~ half an FP16 window;
+  // (tools/dbg_decode_time.py least-squares fit): 2-bit 0.167 us, 4-bit 0.182,
+  // 8-bit 0.249, FP16 0.251, 16-token rest tile ~0.1;
   // expressed in units of S*D so other window sizes scale.
   static constexpr int64_t cost(int k) {
-    return k == 4 ? 53LL * D : (int64_t)(k == 0 ? 156 : k == 1 ? 175 : k == 2 ? 204 : 331) * S * D / 100;
+    return k == 4 ? 40LL * D : (int64_t)(k == 0 ? 156 : k == 1 ? 170 : k == 2 ? 233 : 235) * S * D / 100;
   }
 };
 
@@ -860,15 +860,12 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
     if (split) {
       // (3) ticket: the last CTA of the unit merges all CTA partials by log-sum-exp
       named_bar_sync(1, NCW * 32);
-      if (tid == 0) {
-        __threadfence();
-        const int old = atomicAdd(a.ws_cnt + u, 1);
-        *s_flag = (old == c1 - c0 - 1);
-      }
+      // one acq_rel ticket: releases this CTA's partial (written by all threads before
+      // the barrier) and, for the last CTA, acquires every other CTA's partial
+      if (tid == 0) *s_flag = (atom_add_acq_rel_gpu(a.ws_cnt + u, 1) == c1 - c0 - 1);
       named_bar_sync(1, NCW * 32);
       if (ts && tid == 0) { ts[6] = *s_flag; ts[7] = c - c0; }
       if (*s_flag) {
-        __threadfence();
         // every output element: the np partials' (m, l, o) in one batch of
         // independent loads, then the log-sum-exp combination in registers
         const int np = c1 - c0;
