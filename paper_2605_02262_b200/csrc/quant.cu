@@ -36,8 +36,6 @@ __global__ void k_layer_layout(const int32_t *__restrict__ seg_off, int B, int H
   }
 }
 
-constexpr int QT = 256;  // threads per quantize CTA
-
 struct QuantArgs {
   const __half *k, *v;
   int64_t sb, sh, st;     // strides in elements (b, h, t); channel stride 1
@@ -50,18 +48,6 @@ struct QuantArgs {
   uint8_t *packed;
 };
 
-// 16-byte unit ui of a code tile, word e -> (lane, word in the lane's chunk) (D-1:
-// chunks of >= 16 bytes are interleaved in 16-byte groups, 8-byte chunks are linear)
-WQ_DEV void unit_lane_word(int ui, int e, int chunk_words, int &L, int &wl) {
-  if (chunk_words >= 4) {
-    L = ui & 31;
-    wl = 4 * (ui >> 5) + e;
-  } else {
-    L = 2 * ui + (e >> 1);
-    wl = e & 1;
-  }
-}
-
 // Q17 on one element: clamp(rint(fl(fl(x - mn) * r)), 0, qmax).  prod >= +0 (x >= mn,
 // r > 0); clamping the float to qmax before rounding gives the same integer as
 // clamping after it, and adding 1.5*2^23 rounds to nearest-even exactly like
@@ -72,260 +58,313 @@ WQ_DEV uint32_t q17_code(float x, float mn, float r, float qmaxf) {
   const float big = __fadd_rn(prod, 12582912.0f);
   return __float_as_uint(big) & 0xFFu;
 }
+// Q17 scale of a group: s = max(RoundUp_fp16(fl(mx - mn) / qmax), 2^-24)
+WQ_DEV __half q17_scale(float mn, float mx, float qmaxf) {
+  __half s16 = __float2half_ru(__fdiv_rn(__fsub_rn(mx, mn), qmaxf));
+  if (__half2float(s16) < 5.9604644775390625e-08f) s16 = __ushort_as_half(0x0001);
+  return s16;
+}
 
-// Codes of one window in D-1 fragment order: 16-byte units, thread-strided.  For
-// each unit the lane L and its chunk words follow D-1 (unit_lane_word); every pair
-// is two Q17 codes of adjacent columns (K) / adjacent tokens (V).
+// ---------------------------------------------------------------------------------
+// k_quant: persistent.  A CTA runs TEAMS teams of 4 warps; a team owns two window
+// slots in shared memory (double buffering) and quantizes windows gt, gt + nteams, ...
+// of the flattened (request, kv head, slot) space.  A window's K and V rows land by
+// two 1-D bulk copies (TMA engine); its work splits into independent warp tasks --
+// the two channel halves of K (per-channel parameters) and the 16-token tiles of V
+// (per-token parameters) -- so no CTA barrier is ever needed: the slot is released
+// through an mbarrier once the team's 4 warps are done with it.  Fragment-order reads
+// go through a per-warp work buffer with rows padded by 16 bytes (bank-conflict free).
+// ---------------------------------------------------------------------------------
+template <int D, int S>
+struct QuantGeo {
+  static constexpr int WIN = 4 * S * D;                 // K + V rows of a window, as landed
+  static constexpr int WRB = 2 * D + 16;                // padded row bytes, work buffer
+  static constexpr int WORK = 16 * WRB;                 // one 16-row tile
+  static constexpr int SCR = (D > S ? D : S) * 8;       // float2 params scratch per warp
+  static constexpr int PER_TEAM = 2 * WIN + 4 * (WORK + SCR);
+  static constexpr int T0 = (216 * 1024) / PER_TEAM;
+  static constexpr int TEAMS = T0 > 4 ? 4 : (T0 < 1 ? 1 : T0);
+  static constexpr int NT = S / 16 + 2;                 // tasks per window: 2 K halves + S/16 V tiles
+  static constexpr size_t bar_off = (size_t)TEAMS * PER_TEAM;
+  static constexpr size_t total = bar_off + TEAMS * 4 * 8;
+};
+
+// K channel half hf (channels [hf*D/2, (hf+1)*D/2)) of a window: per-channel min/max
+// over the S rows, parameters, then codes tile by tile (the fragment lane's words whose
+// channels fall in this half).
 template <int D, int S, int BITS>
-WQ_DEV void pack_codes(const __half *Ks, const __half *Vs, const float2 *kp2, const float2 *vp2,
-                       uint4 *dst, int tid) {
-  constexpr int PPW = 16 / BITS;
-  constexpr int CW = D * BITS / 64;           // chunk words per lane
-  constexpr int UPT = 2 * D * BITS / 16;      // 16-byte units per tile
-  constexpr int UNITS = (S / 16) * UPT;       // per tensor
+WQ_DEV void quant_k_half(const uint8_t *krows, uint8_t *work, float2 *kp, uint8_t *rec, int hf, int lane) {
+  using QG = QuantGeo<D, S>;
+  constexpr int WRB = QG::WRB;
   constexpr float QMAX = (float)((1 << BITS) - 1);
   constexpr uint32_t MASK = (1u << BITS) - 1u;
-  // K: rows = tokens, cols = channels
-  for (int u = tid; u < UNITS; u += QT) {
-    const int tile = u / UPT, ui = u % UPT;
-    uint32_t wv[4];
+  constexpr int PPW = 16 / BITS;
+  constexpr int CW = D * BITS / 64;                     // chunk words per lane per tile
+  constexpr int TILE = 2 * D * BITS;                    // bytes per 16-token tile
+  constexpr int KBYTES = S * D * BITS / 8;
+  constexpr int HP = D / 4;                             // channel pairs per half
+  // (1) min/max: lane = channel pair (rows read straight from the landed copy)
+  if (lane < HP) {
+    const int cp = hf * HP + lane;
+    __half2 mn2 = __float2half2_rn(65504.f), mx2 = __float2half2_rn(-65504.f);
+#pragma unroll 8
+    for (int t = 0; t < S; t++) {
+      const __half2 x = *reinterpret_cast<const __half2 *>(krows + t * 2 * D + 4 * cp);
+      mn2 = __hmin2(mn2, x);
+      mx2 = __hmax2(mx2, x);
+    }
+    const float mn0 = __low2float(mn2), mn1 = __high2float(mn2);
+    const __half s0 = q17_scale(mn0, __low2float(mx2), QMAX), s1 = q17_scale(mn1, __high2float(mx2), QMAX);
+    kp[2 * cp] = make_float2(mn0, __frcp_rn(__half2float(s0)));
+    kp[2 * cp + 1] = make_float2(mn1, __frcp_rn(__half2float(s1)));
+    // D-1 K group (q, m) = {mn01, s01, mn89, s89}: this pair fills one half of it
+    const int m = cp >> 3, j = cp & 7, q = j & 3, hh = j >> 2;
+    uint2 pv;
+    pv.x = (uint32_t)__half_as_ushort(__low2half(mn2)) | ((uint32_t)__half_as_ushort(__high2half(mn2)) << 16);
+    pv.y = (uint32_t)__half_as_ushort(s0) | ((uint32_t)__half_as_ushort(s1) << 16);
+    *reinterpret_cast<uint2 *>(rec + 2 * KBYTES + (q * (D / 16) + m) * 16 + hh * 8) = pv;
+  }
+  // (2) codes: words of fragment lane L = lane whose pairs lie in this channel half
+  //     (pair P -> m = P/4; m < D/32 is half 0).  WH words per tile per half.
+  constexpr int WH = CW / 2 > 0 ? CW / 2 : 1;          // CW >= 2 always (d >= 64, b >= 2)
+  const int g = lane >> 2, q = lane & 3;
+#pragma unroll 1
+  for (int tile = 0; tile < S / 16; tile++) {
+    // re-lay the tile's 16 half rows (D bytes each) into padded rows
+    __syncwarp();
+    {
+      constexpr int CPR = D / 16;                       // 16-byte chunks per half row
 #pragma unroll
-    for (int e = 0; e < 4; e++) {
-      int L, wl;
-      unit_lane_word(ui, e, CW, L, wl);
-      const int g = L >> 2, q = L & 3;
-      const __half *kb = Ks + (tile * 16 + g) * D + 2 * q;
+      for (int i = lane; i < 16 * CPR; i += 32) {
+        const int t = i / CPR, cc = i - t * CPR;
+        *reinterpret_cast<uint4 *>(work + t * WRB + 16 * cc) =
+            *reinterpret_cast<const uint4 *>(krows + (tile * 16 + t) * 2 * D + hf * D + 16 * cc);
+      }
+    }
+    __syncwarp();
+    uint32_t wv[WH];
+#pragma unroll
+    for (int e = 0; e < WH; e++) {
+      const int wl = hf * WH + e;
       uint32_t acc = 0;
 #pragma unroll
       for (int j = 0; j < PPW; j++) {
         const int P = wl * PPW + j, m = P >> 2, r = P & 3;
-        const int col = 16 * m + 8 * (r >> 1);
-        const float2 x = __half22float2(*reinterpret_cast<const __half2 *>(kb + 8 * (r & 1) * D + col));
-        const float4 pr = *reinterpret_cast<const float4 *>(kp2 + col + 2 * q);
+        const int row = g + 8 * (r & 1), col = 16 * m + 8 * (r >> 1) + 2 * q;     // col in [hf*D/2, ...)
+        const float2 x = __half22float2(*reinterpret_cast<const __half2 *>(work + row * WRB + 2 * (col - hf * D / 2)));
+        const float4 pr = *reinterpret_cast<const float4 *>(kp + col);
         const uint32_t c0 = q17_code(x.x, pr.x, pr.y, QMAX) & MASK;
         const uint32_t c1 = q17_code(x.y, pr.z, pr.w, QMAX) & MASK;
         acc |= (c0 << (BITS * j)) | (c1 << (16 + BITS * j));
       }
       wv[e] = acc;
     }
-    dst[u] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-  }
-  // V: rows = channels, cols = tokens
-  uint4 *vdst = dst + UNITS;
-  for (int u = tid; u < UNITS; u += QT) {
-    const int tile = u / UPT, ui = u % UPT;
-    uint32_t wv[4];
+    // D-1 chunk of lane L: words 4*gi + e at byte gi*512 + L*16 + 4e (chunks >= 16 B) or
+    // L*8 + 4e (8-byte chunks); this half owns words [hf*WH, (hf+1)*WH)
+    uint8_t *tb = rec + tile * TILE;
+    if constexpr (CW >= 4) {
 #pragma unroll
-    for (int e = 0; e < 4; e++) {
-      int L, wl;
-      unit_lane_word(ui, e, CW, L, wl);
-      const int g = L >> 2, q = L & 3;
-      uint32_t acc = 0;
-#pragma unroll
-      for (int j = 0; j < PPW; j++) {
-        const int P = wl * PPW + j, m = P >> 2, r = P & 3;
-        const int ch = 16 * m + g + 8 * (r & 1), t = tile * 16 + 2 * q + 8 * (r >> 1);
-        const float4 pr = *reinterpret_cast<const float4 *>(vp2 + t);     // {mn, r} of t, t+1
-        const uint32_t c0 = q17_code(__half2float(Vs[t * D + ch]), pr.x, pr.y, QMAX) & MASK;
-        const uint32_t c1 = q17_code(__half2float(Vs[(t + 1) * D + ch]), pr.z, pr.w, QMAX) & MASK;
-        acc |= (c0 << (BITS * j)) | (c1 << (16 + BITS * j));
+      for (int e0 = 0; e0 < WH; e0 += (WH >= 4 ? 4 : 2)) {
+        const int wl = hf * WH + e0;
+        uint8_t *dst = tb + (wl >> 2) * 512 + lane * 16 + 4 * (wl & 3);
+        if constexpr (WH >= 4) *reinterpret_cast<uint4 *>(dst) = make_uint4(wv[e0], wv[e0 + 1], wv[e0 + 2], wv[e0 + 3]);
+        else *reinterpret_cast<uint2 *>(dst) = make_uint2(wv[e0], wv[e0 + 1]);
       }
-      wv[e] = acc;
+    } else {
+      *reinterpret_cast<uint32_t *>(tb + lane * 8 + 4 * hf) = wv[0];
     }
-    vdst[u] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
   }
 }
 
-// Quantize + pack one staged window (K, V rows in shared memory) into rec.
-template <int D, int S>
-WQ_DEV void quant_window(const __half *Ks, const __half *Vs, float2 *kp2, float2 *vp2, __half2 *red,
-                         uint8_t *params, uint8_t *rec, int bits, int tid) {
-
-  const int64_t code_bytes = (int64_t)S * D * bits / 8;      // one of K or V
-  if (bits == 16) {
-    // FP16 window: values re-laid in fragment order (pairs of adjacent columns).
-    // word index u over K tiles then V tiles: tile i, lane L, pair P = word in lane chunk
-    constexpr int UPT = 32 * D / 16;                         // 16-byte units per tile
-    constexpr int UNITS = (S / 16) * UPT;                    // per tensor
-    uint4 *dst = reinterpret_cast<uint4 *>(rec);
-    for (int u4 = tid; u4 < 2 * UNITS; u4 += QT) {
-      const int isv = u4 >= UNITS;
-      const int uu = isv ? u4 - UNITS : u4;
-      const int tile = uu / UPT, ui = uu % UPT;
-      uint32_t wv[4];
-#pragma unroll
-      for (int e = 0; e < 4; e++) {
-        int L, P;
-        unit_lane_word(ui, e, D / 4, L, P);
-        int g = L >> 2, q = L & 3, m = P >> 2, r = P & 3;
-        if (!isv) {
-          int row = tile * 16 + g + 8 * (r & 1), col = 16 * m + 2 * q + 8 * (r >> 1);
-          wv[e] = *reinterpret_cast<const uint32_t *>(Ks + row * D + col);
-        } else {
-          int ch = 16 * m + g + 8 * (r & 1), t = tile * 16 + 2 * q + 8 * (r >> 1);
-          uint32_t lo = __half_as_ushort(Vs[t * D + ch]);
-          uint32_t hi = __half_as_ushort(Vs[(t + 1) * D + ch]);
-          wv[e] = lo | (hi << 16);
-        }
-      }
-      dst[u4] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-    }
-    return;
-  }
-
-  const int qmax = (1 << bits) - 1;
-  const float qmaxf = (float)qmax;
-
-  // ---- K: per-channel (min, max) over the S tokens ----
+// V tile vt (tokens [16vt, 16vt+16)): per-token min/max over D channels, parameters,
+// codes of the fragment lane L = lane for this tile.
+template <int D, int S, int BITS>
+WQ_DEV void quant_v_tile(const uint8_t *vrows, uint8_t *work, float2 *vp, uint8_t *rec, int vt, int lane) {
+  using QG = QuantGeo<D, S>;
+  constexpr int WRB = QG::WRB;
+  constexpr float QMAX = (float)((1 << BITS) - 1);
+  constexpr uint32_t MASK = (1u << BITS) - 1u;
+  constexpr int PPW = 16 / BITS;
+  constexpr int CW = D * BITS / 64;
+  constexpr int TILE = 2 * D * BITS;
+  constexpr int KBYTES = S * D * BITS / 8;
+  // re-lay the tile's 16 rows into padded rows
+  __syncwarp();
   {
-    constexpr int CP = D / 2;                 // channel pairs
-    constexpr int TG = QT / CP;               // token groups
-    const int cp = tid % CP, tg = tid / CP;
-    __half2 mn2 = __float2half2_rn(65504.f), mx2 = __float2half2_rn(-65504.f);
-    for (int t = tg; t < S; t += TG) {
-      __half2 x = *reinterpret_cast<const __half2 *>(Ks + t * D + 2 * cp);
-      mn2 = __hmin2(mn2, x);
-      mx2 = __hmax2(mx2, x);
-    }
-    red[2 * tid] = mn2;
-    red[2 * tid + 1] = mx2;
-    __syncthreads();
-    if (tid < CP) {
-      for (int g2 = 1; g2 < TG; g2++) {
-        mn2 = __hmin2(mn2, red[2 * (g2 * CP + cp)]);
-        mx2 = __hmax2(mx2, red[2 * (g2 * CP + cp) + 1]);
-      }
+    constexpr int CPR = 2 * D / 16;
 #pragma unroll
-      for (int e = 0; e < 2; e++) {
-        int c = 2 * cp + e;
-        float mn = __half2float(e ? __high2half(mn2) : __low2half(mn2));
-        float mx = __half2float(e ? __high2half(mx2) : __low2half(mx2));
-        __half s16 = __float2half_ru(__fdiv_rn(__fsub_rn(mx, mn), qmaxf));
-        if (__half2float(s16) < 5.9604644775390625e-08f) s16 = __ushort_as_half(0x0001);
-        kp2[c] = make_float2(mn, __frcp_rn(__half2float(s16)));
-        int m = c / 16, q = (c % 8) / 2, hh = (c % 16) / 8;
-        __half *grp = reinterpret_cast<__half *>(params + (q * (D / 16) + m) * 16);
-        grp[4 * hh + e] = __float2half_rn(mn);      // D-1 K group {mn01, s01, mn89, s89}
-        grp[4 * hh + 2 + e] = s16;
-      }
+    for (int i = lane; i < 16 * CPR; i += 32) {
+      const int t = i / CPR, cc = i - t * CPR;
+      *reinterpret_cast<uint4 *>(work + t * WRB + 16 * cc) = *reinterpret_cast<const uint4 *>(vrows + (vt * 16 + t) * 2 * D + 16 * cc);
     }
   }
-  // ---- V: per-token (min, max) over the D channels ----
+  __syncwarp();
+  // (1) min/max: two lanes per token (each half of the channels), combined by a shuffle
   {
-    constexpr int TPT = QT / S;               // threads per token
-    constexpr int CH = D / TPT;               // channels per thread (multiple of 2)
-    const int t = tid / TPT, part = tid % TPT;
+    const int t = lane >> 1, hc = lane & 1;
     __half2 mn2 = __float2half2_rn(65504.f), mx2 = __float2half2_rn(-65504.f);
-#pragma unroll
-    for (int c = 0; c < CH; c += 2) {
-      __half2 x = *reinterpret_cast<const __half2 *>(Vs + t * D + part * CH + c);
+#pragma unroll 8
+    for (int i = 0; i < D / 4; i++) {
+      const __half2 x = *reinterpret_cast<const __half2 *>(work + t * WRB + 2 * D / 2 * hc + 4 * i);
       mn2 = __hmin2(mn2, x);
       mx2 = __hmax2(mx2, x);
     }
     __half mn = __hmin(__low2half(mn2), __high2half(mn2));
     __half mx = __hmax(__low2half(mx2), __high2half(mx2));
-#pragma unroll
-    for (int o = TPT / 2; o >= 1; o >>= 1) {
-      mn = __hmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = __hmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if (part == 0) {
-      float mnf = __half2float(mn), mxf = __half2float(mx);
-      __half s16 = __float2half_ru(__fdiv_rn(__fsub_rn(mxf, mnf), qmaxf));
-      if (__half2float(s16) < 5.9604644775390625e-08f) s16 = __ushort_as_half(0x0001);
-      vp2[t] = make_float2(mnf, __frcp_rn(__half2float(s16)));
-      int i = t / 16, col = t % 16, q = (col % 8) / 2, hh = col / 8, e = col % 2;
-      __half *grp = reinterpret_cast<__half *>(params + 4 * D + (4 * i + q) * 16);
+    mn = __hmin(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+    mx = __hmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    if (hc == 0) {
+      const float mnf = __half2float(mn);
+      const __half s16 = q17_scale(mnf, __half2float(mx), QMAX);
+      vp[t] = make_float2(mnf, __frcp_rn(__half2float(s16)));
+      // D-1 V group (i, q) = {s(t0), s(t0+1), s(t0+8), s(t0+9), mn(...)}, t0 = 16i + 2q
+      const int qq = (t & 7) >> 1, hh = t >> 3, e = t & 1;
+      __half *grp = reinterpret_cast<__half *>(rec + 2 * KBYTES + 4 * D + (4 * vt + qq) * 16);
       grp[2 * hh + e] = s16;
       grp[4 + 2 * hh + e] = mn;
     }
   }
-  __syncthreads();
-
-  // ---- codes in fragment order (templated per width: unrolled, constant shifts) ----
-  uint4 *dst = reinterpret_cast<uint4 *>(rec);
-  switch (bits) {
-    case 2: pack_codes<D, S, 2>(Ks, Vs, kp2, vp2, dst, tid); break;
-    case 4: pack_codes<D, S, 4>(Ks, Vs, kp2, vp2, dst, tid); break;
-    default: pack_codes<D, S, 8>(Ks, Vs, kp2, vp2, dst, tid); break;
+  __syncwarp();
+  const int g = lane >> 2, q = lane & 3;
+  uint8_t *tb = rec + KBYTES + vt * TILE;
+  constexpr int NG = CW >= 4 ? CW / 4 : 1;
+#pragma unroll
+  for (int gi = 0; gi < NG; gi++) {
+    uint32_t wv[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int e = 0; e < (CW >= 4 ? 4 : CW); e++) {
+      const int wl = 4 * gi + e;
+      uint32_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < PPW; j++) {
+        const int P = wl * PPW + j, m = P >> 2, r = P & 3;
+        const int ch = 16 * m + g + 8 * (r & 1), t = 2 * q + 8 * (r >> 1);
+        const float4 pr = *reinterpret_cast<const float4 *>(vp + t);      // {mn, r} of t, t+1
+        const float x0 = __half2float(*reinterpret_cast<const __half *>(work + t * WRB + 2 * ch));
+        const float x1 = __half2float(*reinterpret_cast<const __half *>(work + (t + 1) * WRB + 2 * ch));
+        const uint32_t c0 = q17_code(x0, pr.x, pr.y, QMAX) & MASK;
+        const uint32_t c1 = q17_code(x1, pr.z, pr.w, QMAX) & MASK;
+        acc |= (c0 << (BITS * j)) | (c1 << (16 + BITS * j));
+      }
+      wv[e] = acc;
+    }
+    if constexpr (CW >= 4)
+      *reinterpret_cast<uint4 *>(tb + gi * 512 + lane * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    else
+      *reinterpret_cast<uint2 *>(tb + lane * 8) = make_uint2(wv[0], wv[1]);
   }
-  // ---- params (K then V) after the codes ----
-  uint4 *pdst = reinterpret_cast<uint4 *>(rec + 2 * code_bytes);
-  const uint4 *psrc = reinterpret_cast<const uint4 *>(params);
-  for (int i = tid; i < (4 * D + 4 * S) / 16; i += QT) pdst[i] = psrc[i];
 }
 
-// Persistent kernel: each CTA walks windows blockIdx.x, +gridDim.x, ... of the
-// flattened (request, kv head, slot) space with an NSTG-deep TMA ring, so the
-// next windows stream in while the current one is quantized.
+// FP16 window, task tk: K halves / V tiles copied into fragment order.
 template <int D, int S>
-struct QuantSmem {
-  static constexpr int WIN = 4 * S * D;                     // K + V bytes of one window
-  static constexpr int NSTG = WIN >= 65536 ? 2 : 3;
-  static constexpr size_t ring = (size_t)NSTG * WIN;
-  static constexpr size_t total = ring + (2 * D + 2 * S) * 8 + 2 * QT * 4 + 4 * D + 4 * S + 64;
-};
-
-template <int D, int S>
-__global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
-  using QS = QuantSmem<D, S>;
-  constexpr int NSTG = QS::NSTG;
-  extern __shared__ __align__(128) uint8_t sm[];
-  float2 *kp2 = reinterpret_cast<float2 *>(sm + QS::ring);  // [D] {mn, 1/s} per channel
-  float2 *vp2 = kp2 + D;                                     // [S] {mn, 1/s} per token
-  __half2 *red = reinterpret_cast<__half2 *>(vp2 + S);       // [QT] x (min2, max2)
-  uint8_t *params = reinterpret_cast<uint8_t *>(red + 2 * QT);  // [4D + 4S]
-  __shared__ uint64_t bar[NSTG];
-  const int tid = threadIdx.x;
-  const int total = a.B * a.H * a.perm_stride;
-
-  // window k of this CTA -> (b, h, slot); valid if slot < seg_off[b][4]
-  auto locate = [&](int k, int &b, int &h, int &slot) -> bool {
-    const int idx = blockIdx.x + k * gridDim.x;
-    if (idx >= total) return false;
-    slot = idx % a.perm_stride;
-    const int bh = idx / a.perm_stride;
-    h = bh % a.H;
-    b = bh / a.H;
-    return true;
-  };
-  auto issue = [&](int k) {                       // thread 0: TMA of window k into its stage
-    int b, h, slot;
-    if (!locate(k, b, h, slot)) return;
-    if (slot >= a.seg_off[5 * b + 4]) {           // no window: complete the phase anyway
-      mbar_arrive(&bar[k % NSTG]);
-      return;
+WQ_DEV void copy_task_fp16(const uint8_t *krows, const uint8_t *vrows, uint8_t *work, uint8_t *rec, int tk, int lane) {
+  using QG = QuantGeo<D, S>;
+  constexpr int WRB = QG::WRB;
+  constexpr int TILE = 2 * D * 16;
+  const int g = lane >> 2, q = lane & 3;
+  if (tk < 2) {
+    // K half tk: groups gi (4 words, m = gi) with 16m in this half, every tile
+#pragma unroll 1
+    for (int tile = 0; tile < S / 16; tile++) {
+      __syncwarp();
+      for (int i = lane; i < 16 * (2 * D / 16); i += 32) {
+        const int t = i / (2 * D / 16), cc = i - t * (2 * D / 16);
+        *reinterpret_cast<uint4 *>(work + t * WRB + 16 * cc) = *reinterpret_cast<const uint4 *>(krows + (tile * 16 + t) * 2 * D + 16 * cc);
+      }
+      __syncwarp();
+      for (int gi = tk * (D / 32); gi < (tk + 1) * (D / 32); gi++) {
+        uint32_t wv[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int P = 4 * gi + e, m = P >> 2, r = P & 3;
+          const int row = g + 8 * (r & 1), col = 16 * m + 2 * q + 8 * (r >> 1);
+          wv[e] = *reinterpret_cast<const uint32_t *>(work + row * WRB + 2 * col);
+        }
+        *reinterpret_cast<uint4 *>(rec + tile * TILE + gi * 512 + lane * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      }
     }
+  } else {
+    const int vt = tk - 2;
+    __syncwarp();
+    for (int i = lane; i < 16 * (2 * D / 16); i += 32) {
+      const int t = i / (2 * D / 16), cc = i - t * (2 * D / 16);
+      *reinterpret_cast<uint4 *>(work + t * WRB + 16 * cc) = *reinterpret_cast<const uint4 *>(vrows + (vt * 16 + t) * 2 * D + 16 * cc);
+    }
+    __syncwarp();
+    for (int gi = 0; gi < D / 16; gi++) {
+      uint32_t wv[4];
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int P = 4 * gi + e, m = P >> 2, r = P & 3;
+        const int ch = 16 * m + g + 8 * (r & 1), t = 2 * q + 8 * (r >> 1);
+        const uint32_t lo = *reinterpret_cast<const uint16_t *>(work + t * WRB + 2 * ch);
+        const uint32_t hi = *reinterpret_cast<const uint16_t *>(work + (t + 1) * WRB + 2 * ch);
+        wv[e] = lo | (hi << 16);
+      }
+      *reinterpret_cast<uint4 *>(rec + S * D * 2 + vt * TILE + gi * 512 + lane * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
+  }
+}
+
+template <int D, int S>
+__global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantArgs a) {
+  using QG = QuantGeo<D, S>;
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int team = warp >> 2, tw = warp & 3;
+  uint8_t *tbase = sm + (size_t)team * QG::PER_TEAM;
+  uint8_t *work = tbase + 2 * QG::WIN + tw * (QG::WORK + QG::SCR);
+  float2 *scr = reinterpret_cast<float2 *>(work + QG::WORK);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + QG::bar_off) + team * 4;   // [2] full, [2] empty
+  uint64_t *empty = full + 2;
+  const int64_t nwin = (int64_t)a.B * a.H * a.perm_stride;
+  const int64_t gt = (int64_t)blockIdx.x * QG::TEAMS + team, nt = (int64_t)gridDim.x * QG::TEAMS;
+  if (tw == 0 && lane == 0) {
+    mbar_init(&full[0], 1); mbar_init(&full[1], 1);
+    mbar_init(&empty[0], 4); mbar_init(&empty[1], 4);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto locate = [&](int64_t wi, int &b, int &h, int &slot) {
+    slot = (int)(wi % a.perm_stride);
+    const int64_t bh = wi / a.perm_stride;
+    h = (int)(bh % a.H);
+    b = (int)(bh / a.H);
+  };
+  // team window k -> slot k & 1 (issued by the team's warp 0, lane 0)
+  auto issue = [&](int64_t k) {
+    const int64_t wi = gt + k * nt;
+    if (wi >= nwin) return;
+    const int sl = (int)(k & 1);
+    mbar_wait(&empty[sl], (uint32_t)((k >> 1) & 1) ^ 1u);
+    int b, h, slot;
+    locate(wi, b, h, slot);
+    if (slot >= a.seg_off[5 * b + 4]) { mbar_arrive(&full[sl]); return; }
     const int w = a.perm[(int64_t)b * a.perm_stride + slot];
-    const __half *K0 = a.k + b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
-    const __half *V0 = a.v + b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
-    __half *Ks = reinterpret_cast<__half *>(sm + (size_t)(k % NSTG) * QS::WIN);
-    __half *Vs = Ks + S * D;
-    uint64_t *bb = &bar[k % NSTG];
-    constexpr uint32_t ROW = D * 2;
-    mbar_arrive_expect_tx(bb, 2u * S * ROW);
+    const int64_t ro = b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
+    uint8_t *dst = tbase + (size_t)sl * QG::WIN;
     const uint64_t pol = policy_evict_first();
+    mbar_arrive_expect_tx(&full[sl], (uint32_t)(4 * S * D));
     if (a.st == D) {
-      bulk_g2s_evict_first(Ks, K0, S * ROW, bb, pol);
-      bulk_g2s_evict_first(Vs, V0, S * ROW, bb, pol);
+      bulk_g2s_evict_first(dst, a.k + ro, S * 2 * D, &full[sl], pol);
+      bulk_g2s_evict_first(dst + S * 2 * D, a.v + ro, S * 2 * D, &full[sl], pol);
     } else {
       for (int t = 0; t < S; t++) {
-        bulk_g2s_evict_first(Ks + t * D, K0 + t * a.st, ROW, bb, pol);
-        bulk_g2s_evict_first(Vs + t * D, V0 + t * a.st, ROW, bb, pol);
+        bulk_g2s_evict_first(dst + t * 2 * D, a.k + ro + t * a.st, 2 * D, &full[sl], pol);
+        bulk_g2s_evict_first(dst + S * 2 * D + t * 2 * D, a.v + ro + t * a.st, 2 * D, &full[sl], pol);
       }
     }
   };
-  if (tid == 0) {
-    for (int i = 0; i < NSTG; i++) mbar_init(&bar[i], 1);
-    fence_mbar_init();
-    for (int k = 0; k < NSTG - 1; k++) issue(k);
-  }
-  __syncthreads();
-  for (int k = 0;; k++) {
+  if (tw == 0 && lane == 0) issue(0);
+  for (int64_t k = 0;; k++) {
+    const int64_t wi = gt + k * nt;
+    if (wi >= nwin) break;
+    if (tw == 0 && lane == 0) issue(k + 1);       // the other slot (released after window k-1)
+    const int sl = (int)(k & 1);
     int b, h, slot;
-    if (!locate(k, b, h, slot)) break;
-    if (tid == 0) issue(k + NSTG - 1);            // its stage was released by the last barrier
+    locate(wi, b, h, slot);
     const int32_t *so = a.seg_off + 5 * b;
+    mbar_wait(&full[sl], (uint32_t)((k >> 1) & 1));
     if (slot < so[4]) {
       int cls = 0;
       while (slot >= so[cls + 1]) cls++;
@@ -333,28 +372,43 @@ __global__ void __launch_bounds__(QT) k_quant(QuantArgs a) {
       int64_t roff = a.offs[(int64_t)b * a.H + h];
       for (int kk = 0; kk < cls; kk++) roff += (int64_t)(so[kk + 1] - so[kk]) * record_bytes(class_bits(kk), D, S);
       roff += (int64_t)(slot - so[cls]) * record_bytes(bits, D, S);
-      mbar_wait(&bar[k % NSTG], (uint32_t)(k / NSTG) & 1u);
-      const __half *Ks = reinterpret_cast<const __half *>(sm + (size_t)(k % NSTG) * QS::WIN);
-      quant_window<D, S>(Ks, Ks + S * D, kp2, vp2, red, params, a.packed + roff, bits, tid);
+      uint8_t *rec = a.packed + roff;
+      const uint8_t *krows = tbase + (size_t)sl * QG::WIN, *vrows = krows + S * 2 * D;
+      for (int tk = tw; tk < QG::NT; tk += 4) {
+        if (bits == 16) {
+          copy_task_fp16<D, S>(krows, vrows, work, rec, tk, lane);
+        } else if (tk < 2) {
+          if (bits == 2) quant_k_half<D, S, 2>(krows, work, scr, rec, tk, lane);
+          else if (bits == 4) quant_k_half<D, S, 4>(krows, work, scr, rec, tk, lane);
+          else quant_k_half<D, S, 8>(krows, work, scr, rec, tk, lane);
+        } else {
+          if (bits == 2) quant_v_tile<D, S, 2>(vrows, work, scr, rec, tk - 2, lane);
+          else if (bits == 4) quant_v_tile<D, S, 4>(vrows, work, scr, rec, tk - 2, lane);
+          else quant_v_tile<D, S, 8>(vrows, work, scr, rec, tk - 2, lane);
+        }
+      }
     }
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sl]);       // this warp is done with the slot
   }
 }
 
 template <int D, int S>
 static cudaError_t launch_quant_t(const QuantArgs &a, cudaStream_t st) {
-  using QS = QuantSmem<D, S>;
-  const size_t smem = QS::total;
-  cudaError_t e = cudaFuncSetAttribute(k_quant<D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quant<D, S>, QT, smem);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t total = (int64_t)a.B * a.H * a.perm_stride;
-  int64_t grid = (int64_t)device_sm_count() * per_sm;
-  if (grid > total) grid = total;
+  using QG = QuantGeo<D, S>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_quant<D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)QG::total);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t nwin = (int64_t)a.B * a.H * a.perm_stride;
+  int64_t grid = device_sm_count();
+  const int64_t need = (nwin + QG::TEAMS - 1) / QG::TEAMS;
+  if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  k_quant<D, S><<<(unsigned)grid, QT, smem, st>>>(a);
+  k_quant<D, S><<<(unsigned)grid, QG::TEAMS * 128, QG::total, st>>>(a);
   return cudaGetLastError();
 }
 
