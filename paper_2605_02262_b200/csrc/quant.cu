@@ -75,6 +75,13 @@ WQ_DEV __half q17_scale(float mn, float mx, float qmaxf) {
 // through an mbarrier once the team's 4 warps are done with it.  Fragment-order reads
 // go through a per-warp work buffer with rows padded by 16 bytes (bank-conflict free).
 // ---------------------------------------------------------------------------------
+// what a team slot holds, written by the issuing lane with the copy (so the consumer
+// warps never wait on the metadata loads): record offset and width, bits = 0 if empty
+struct WinDesc {
+  int64_t roff;
+  int bits, pad;
+};
+
 template <int D, int S>
 struct QuantGeo {
   static constexpr int WIN = 4 * S * D;                 // K + V rows of a window, as landed
@@ -86,7 +93,8 @@ struct QuantGeo {
   static constexpr int TEAMS = T0 > 4 ? 4 : (T0 < 1 ? 1 : T0);
   static constexpr int NT = S / 16 + 2;                 // tasks per window: 2 K halves + S/16 V tiles
   static constexpr size_t bar_off = (size_t)TEAMS * PER_TEAM;
-  static constexpr size_t total = bar_off + TEAMS * 4 * 8;
+  static constexpr size_t desc_off = bar_off + TEAMS * 4 * 8;         // [TEAMS][2] WinDesc
+  static constexpr size_t total = desc_off + TEAMS * 2 * 16;
 };
 
 // K channel half hf (channels [hf*D/2, (hf+1)*D/2)) of a window: per-channel min/max
@@ -317,6 +325,7 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
   float2 *scr = reinterpret_cast<float2 *>(work + QG::WORK);
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + QG::bar_off) + team * 4;   // [2] full, [2] empty
   uint64_t *empty = full + 2;
+  WinDesc *wdesc = reinterpret_cast<WinDesc *>(sm + QG::desc_off) + team * 2;
   const int64_t nwin = (int64_t)a.B * a.H * a.perm_stride;
   const int64_t gt = (int64_t)blockIdx.x * QG::TEAMS + team, nt = (int64_t)gridDim.x * QG::TEAMS;
   if (tw == 0 && lane == 0) {
@@ -339,8 +348,24 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
     mbar_wait(&empty[sl], (uint32_t)((k >> 1) & 1) ^ 1u);
     int b, h, slot;
     locate(wi, b, h, slot);
-    if (slot >= a.seg_off[5 * b + 4]) { mbar_arrive(&full[sl]); return; }
+    const int32_t *so = a.seg_off + 5 * b;
+    int so_[5];
+#pragma unroll
+    for (int i = 0; i < 5; i++) so_[i] = so[i];
+    if (slot >= so_[4]) {
+      wdesc[sl].bits = 0;
+      mbar_arrive(&full[sl]);
+      return;
+    }
     const int w = a.perm[(int64_t)b * a.perm_stride + slot];
+    int cls = 0;
+    while (slot >= so_[cls + 1]) cls++;
+    const int bits = class_bits(cls);
+    int64_t roff = a.offs[(int64_t)b * a.H + h];
+    for (int kk = 0; kk < cls; kk++) roff += (int64_t)(so_[kk + 1] - so_[kk]) * record_bytes(class_bits(kk), D, S);
+    roff += (int64_t)(slot - so_[cls]) * record_bytes(bits, D, S);
+    wdesc[sl].roff = roff;
+    wdesc[sl].bits = bits;
     const int64_t ro = b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
     uint8_t *dst = tbase + (size_t)sl * QG::WIN;
     const uint64_t pol = policy_evict_first();
@@ -361,18 +386,10 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
     if (wi >= nwin) break;
     if (tw == 0 && lane == 0) issue(k + 1);       // the other slot (released after window k-1)
     const int sl = (int)(k & 1);
-    int b, h, slot;
-    locate(wi, b, h, slot);
-    const int32_t *so = a.seg_off + 5 * b;
     mbar_wait(&full[sl], (uint32_t)((k >> 1) & 1));
-    if (slot < so[4]) {
-      int cls = 0;
-      while (slot >= so[cls + 1]) cls++;
-      const int bits = class_bits(cls);
-      int64_t roff = a.offs[(int64_t)b * a.H + h];
-      for (int kk = 0; kk < cls; kk++) roff += (int64_t)(so[kk + 1] - so[kk]) * record_bytes(class_bits(kk), D, S);
-      roff += (int64_t)(slot - so[cls]) * record_bytes(bits, D, S);
-      uint8_t *rec = a.packed + roff;
+    const int bits = wdesc[sl].bits;
+    if (bits) {
+      uint8_t *rec = a.packed + wdesc[sl].roff;
       const uint8_t *krows = tbase + (size_t)sl * QG::WIN, *vrows = krows + S * 2 * D;
       for (int tk = tw; tk < QG::NT; tk += 4) {
         if (bits == 16) {
