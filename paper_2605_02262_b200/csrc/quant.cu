@@ -58,6 +58,23 @@ WQ_DEV uint32_t q17_code(float x, float mn, float r, float qmaxf) {
   const float big = __fadd_rn(prod, 12582912.0f);
   return __float_as_uint(big) & 0xFFu;
 }
+// Q17 code via the float magic, left as big = 0x4B400000 + code: fl(fl(x - mn) * r) lies
+// in [0, q_max + 2^-21] (s = RoundUp(range / q_max) >= range / q_max), so the clamp of
+// Q17 never binds and adding 1.5*2^23 rounds it to nearest-even into the low bits.
+WQ_DEV uint32_t q17_big(float x, float mn, float r) {
+  return __float_as_uint(__fadd_rn(__fmul_rn(__fsub_rn(x, mn), r), 12582912.0f));
+}
+// Packing word = sum_j big_j * 2^(sh_j) + BIAS (mod 2^32): the BIAS cancels the
+// 0x4B400000 of every big, one IMAD per code.
+template <int BITS>
+struct PackBias {
+  static constexpr uint32_t value() {
+    uint32_t b = 0;
+    for (int j = 0; j < 16 / BITS; j++) b += (0x4B400000u << (BITS * j)) + (0x4B400000u << (16 + BITS * j));
+    return 0u - b;
+  }
+};
+
 // Q17 scale of a group: s = max(RoundUp_fp16(fl(mx - mn) / qmax), 2^-24)
 WQ_DEV __half q17_scale(float mn, float mx, float qmaxf) {
   __half s16 = __float2half_ru(__fdiv_rn(__fsub_rn(mx, mn), qmaxf));
@@ -88,13 +105,17 @@ struct QuantGeo {
   static constexpr int WRB = 2 * D + 16;                // padded row bytes, work buffer
   static constexpr int WORK = 16 * WRB;                 // one 16-row tile
   static constexpr int SCR = (D > S ? D : S) * 8;       // float2 params scratch per warp
-  static constexpr int PER_TEAM = 2 * WIN + 4 * (WORK + SCR);
+#ifndef WQ_Q_NSL
+#define WQ_Q_NSL 2
+#endif
+  static constexpr int NSL = WQ_Q_NSL;                  // window slots per team
+  static constexpr int PER_TEAM = NSL * WIN + 4 * (WORK + SCR);
   static constexpr int T0 = (216 * 1024) / PER_TEAM;
   static constexpr int TEAMS = T0 > 4 ? 4 : (T0 < 1 ? 1 : T0);
   static constexpr int NT = S / 16 + 2;                 // tasks per window: 2 K halves + S/16 V tiles
   static constexpr size_t bar_off = (size_t)TEAMS * PER_TEAM;
-  static constexpr size_t desc_off = bar_off + TEAMS * 4 * 8;         // [TEAMS][2] WinDesc
-  static constexpr size_t total = desc_off + TEAMS * 2 * 16;
+  static constexpr size_t desc_off = bar_off + TEAMS * 2 * NSL * 8;   // [TEAMS][NSL] WinDesc
+  static constexpr size_t total = desc_off + TEAMS * NSL * 16;
 };
 
 // K channel half hf (channels [hf*D/2, (hf+1)*D/2)) of a window: per-channel min/max
@@ -154,16 +175,15 @@ WQ_DEV void quant_k_half(const uint8_t *krows, uint8_t *work, float2 *kp, uint8_
 #pragma unroll
     for (int e = 0; e < WH; e++) {
       const int wl = hf * WH + e;
-      uint32_t acc = 0;
+      uint32_t acc = PackBias<BITS>::value();
 #pragma unroll
       for (int j = 0; j < PPW; j++) {
         const int P = wl * PPW + j, m = P >> 2, r = P & 3;
         const int row = g + 8 * (r & 1), col = 16 * m + 8 * (r >> 1) + 2 * q;     // col in [hf*D/2, ...)
         const float2 x = __half22float2(*reinterpret_cast<const __half2 *>(work + row * WRB + 2 * (col - hf * D / 2)));
         const float4 pr = *reinterpret_cast<const float4 *>(kp + col);
-        const uint32_t c0 = q17_code(x.x, pr.x, pr.y, QMAX) & MASK;
-        const uint32_t c1 = q17_code(x.y, pr.z, pr.w, QMAX) & MASK;
-        acc |= (c0 << (BITS * j)) | (c1 << (16 + BITS * j));
+        acc += q17_big(x.x, pr.x, pr.y) * (1u << (BITS * j));
+        acc += q17_big(x.y, pr.z, pr.w) * (1u << (16 + BITS * j));
       }
       wv[e] = acc;
     }
@@ -242,7 +262,7 @@ WQ_DEV void quant_v_tile(const uint8_t *vrows, uint8_t *work, float2 *vp, uint8_
 #pragma unroll
     for (int e = 0; e < (CW >= 4 ? 4 : CW); e++) {
       const int wl = 4 * gi + e;
-      uint32_t acc = 0;
+      uint32_t acc = PackBias<BITS>::value();
 #pragma unroll
       for (int j = 0; j < PPW; j++) {
         const int P = wl * PPW + j, m = P >> 2, r = P & 3;
@@ -250,9 +270,8 @@ WQ_DEV void quant_v_tile(const uint8_t *vrows, uint8_t *work, float2 *vp, uint8_
         const float4 pr = *reinterpret_cast<const float4 *>(vp + t);      // {mn, r} of t, t+1
         const float x0 = __half2float(*reinterpret_cast<const __half *>(work + t * WRB + 2 * ch));
         const float x1 = __half2float(*reinterpret_cast<const __half *>(work + (t + 1) * WRB + 2 * ch));
-        const uint32_t c0 = q17_code(x0, pr.x, pr.y, QMAX) & MASK;
-        const uint32_t c1 = q17_code(x1, pr.z, pr.w, QMAX) & MASK;
-        acc |= (c0 << (BITS * j)) | (c1 << (16 + BITS * j));
+        acc += q17_big(x0, pr.x, pr.y) * (1u << (BITS * j));
+        acc += q17_big(x1, pr.z, pr.w) * (1u << (16 + BITS * j));
       }
       wv[e] = acc;
     }
@@ -321,16 +340,16 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int team = warp >> 2, tw = warp & 3;
   uint8_t *tbase = sm + (size_t)team * QG::PER_TEAM;
-  uint8_t *work = tbase + 2 * QG::WIN + tw * (QG::WORK + QG::SCR);
+  constexpr int NSL = QG::NSL;
+  uint8_t *work = tbase + NSL * QG::WIN + tw * (QG::WORK + QG::SCR);
   float2 *scr = reinterpret_cast<float2 *>(work + QG::WORK);
-  uint64_t *full = reinterpret_cast<uint64_t *>(sm + QG::bar_off) + team * 4;   // [2] full, [2] empty
-  uint64_t *empty = full + 2;
-  WinDesc *wdesc = reinterpret_cast<WinDesc *>(sm + QG::desc_off) + team * 2;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + QG::bar_off) + team * 2 * NSL;   // [NSL] full, [NSL] empty
+  uint64_t *empty = full + NSL;
+  WinDesc *wdesc = reinterpret_cast<WinDesc *>(sm + QG::desc_off) + team * NSL;
   const int64_t nwin = (int64_t)a.B * a.H * a.perm_stride;
   const int64_t gt = (int64_t)blockIdx.x * QG::TEAMS + team, nt = (int64_t)gridDim.x * QG::TEAMS;
   if (tw == 0 && lane == 0) {
-    mbar_init(&full[0], 1); mbar_init(&full[1], 1);
-    mbar_init(&empty[0], 4); mbar_init(&empty[1], 4);
+    for (int i = 0; i < NSL; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 4); }
     fence_mbar_init();
   }
   __syncthreads();
@@ -340,12 +359,12 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
     h = (int)(bh % a.H);
     b = (int)(bh / a.H);
   };
-  // team window k -> slot k & 1 (issued by the team's warp 0, lane 0)
+  // team window k -> slot k % NSL (issued by the team's warp 0, lane 0)
   auto issue = [&](int64_t k) {
     const int64_t wi = gt + k * nt;
     if (wi >= nwin) return;
-    const int sl = (int)(k & 1);
-    mbar_wait(&empty[sl], (uint32_t)((k >> 1) & 1) ^ 1u);
+    const int sl = (int)(k % NSL);
+    mbar_wait(&empty[sl], (uint32_t)((k / NSL) & 1) ^ 1u);
     int b, h, slot;
     locate(wi, b, h, slot);
     const int32_t *so = a.seg_off + 5 * b;
@@ -380,13 +399,14 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
       }
     }
   };
-  if (tw == 0 && lane == 0) issue(0);
+  if (tw == 0 && lane == 0)
+    for (int i = 0; i < NSL - 1; i++) issue(i);
   for (int64_t k = 0;; k++) {
     const int64_t wi = gt + k * nt;
     if (wi >= nwin) break;
-    if (tw == 0 && lane == 0) issue(k + 1);       // the other slot (released after window k-1)
-    const int sl = (int)(k & 1);
-    mbar_wait(&full[sl], (uint32_t)((k >> 1) & 1));
+    if (tw == 0 && lane == 0) issue(k + NSL - 1);  // the slot released after window k-1
+    const int sl = (int)(k % NSL);
+    mbar_wait(&full[sl], (uint32_t)((k / NSL) & 1));
     const int bits = wdesc[sl].bits;
     if (bits) {
       uint8_t *rec = a.packed + wdesc[sl].roff;
