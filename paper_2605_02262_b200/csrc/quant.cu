@@ -377,12 +377,15 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
       return;
     }
     const int w = a.perm[(int64_t)b * a.perm_stride + slot];
-    int cls = 0;
-    while (slot >= so_[cls + 1]) cls++;
+    // class of the slot and its record offset (branch-free: no local arrays)
+    const int cls = (slot >= so_[1]) + (slot >= so_[2]) + (slot >= so_[3]);
     const int bits = class_bits(cls);
     int64_t roff = a.offs[(int64_t)b * a.H + h];
-    for (int kk = 0; kk < cls; kk++) roff += (int64_t)(so_[kk + 1] - so_[kk]) * record_bytes(class_bits(kk), D, S);
-    roff += (int64_t)(slot - so_[cls]) * record_bytes(bits, D, S);
+#pragma unroll
+    for (int kk = 0; kk < 3; kk++)
+      if (kk < cls) roff += (int64_t)(so_[kk + 1] - so_[kk]) * record_bytes(class_bits(kk), D, S);
+    const int sbase = cls == 0 ? so_[0] : cls == 1 ? so_[1] : cls == 2 ? so_[2] : so_[3];
+    roff += (int64_t)(slot - sbase) * record_bytes(bits, D, S);
     wdesc[sl].roff = roff;
     wdesc[sl].bits = bits;
     const int64_t ro = b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
