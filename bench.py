@@ -258,6 +258,28 @@ def run_wq(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    use_graph = world == 1 and not args.no_graph
+    if use_graph:
+        # the step's ~1.4k launches replayed from two CUDA graphs (search + quantize,
+        # decode): no host launch work between kernels; same kernels, same arguments
+        g_sq, g_dec = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_sq):
+            w.search()
+            w.quantize()
+        with torch.cuda.graph(g_dec):
+            w.decode(group)
+        torch.cuda.synchronize()
+
+        def step(ev=None):                                   # noqa: F811
+            g_sq.replay()
+            if ev is not None:
+                ev[0].record(stream)
+            g_dec.replay()
+            if ev is not None:
+                ev[1].record(stream)
+
+        step()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ev_all = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -310,6 +332,7 @@ def run_wq(args, rank, world, local_rank):
         "config": {"workload": cfg.name, "model_shape": cfg.model.name, "layers": cfg.layers, "batch": cfg.B,
                    "visual_tokens": cfg.M, "window": cfg.S, "widths": list(cfg.widths), "gen_tokens": w.n_gen,
                    "parallelism": f"seqsplit{world}" if world > 1 else "single",
+                   "launch": "cuda-graph replay" if use_graph else "host launches",
                    "l2": f"inputs > L2: {cfg.layers} layers x {w.packed_bytes[0] / 1e6:.0f} MB packed rotated",
                    "window_mix": dict(zip(["2", "4", "8", "16"], [int(x) for x in w.class_windows]))},
         "roofline": {"bound": "hbm", "kernel": "wq_decode_attention", "achieved": round(achieved, 1),
@@ -471,6 +494,7 @@ def main():
     ap.add_argument("--n-gen", type=int, default=None, help="override generated tokens (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host (no CUDA graphs)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
