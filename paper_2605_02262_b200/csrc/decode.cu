@@ -1,3 +1,4 @@
+#include <cstdlib>
 // decode.cu -- wq_decode_attention: split-KV flash-decoding over the reordered
 // mixed-precision cache (Alg.2 decode branch P:450-458; Eq.2-3 without mask, P:214;
 // reorder invariance Eq.12-13; fused dequantization P:510), plus the
@@ -24,8 +25,7 @@
 //  * Unit epilogue: warps merged in shared memory, the CTA partial (m, l, o) goes
 //    to the workspace, and the last CTA of the unit (atomic ticket) merges all
 //    partials by log-sum-exp and writes out / partial (Q24).
-#include "wq_device.cuh"
-#include "wq_internal.h"
+#include "decode_common.cuh"
 
 namespace wq {
 
@@ -37,8 +37,6 @@ namespace wq {
 #endif
 constexpr int NCW = WQ_DEC_NCW;                 // consumer warps
 constexpr int DT = (NCW + 1) * 32;      // threads per CTA
-constexpr int MAX_UNITS = 1024;         // B * H
-constexpr int64_t MIN_CTA_BYTES = 49152;
 #ifndef WQ_DEC_QLO
 #define WQ_DEC_QLO 1                     // carry q*s as fp16 hi + lo (0: hi only, experiment)
 #endif
@@ -48,105 +46,8 @@ constexpr int64_t MIN_CTA_BYTES = 49152;
 #ifndef WQ_DEC_STAGE
 #define WQ_DEC_STAGE 32768
 #endif
-constexpr uint32_t WQ_DECODE_EARLY_ = 1u;     // = WQ_DECODE_EARLY (include/wq.h)
-constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trace
 constexpr float LAZY_TH = 8.0f;         // log2 headroom of the lazy softmax rescale
 constexpr int KIND_REST = 4;
-
-// Compile-time item sizes and costs of a (D, S) instantiation.  Work is partitioned
-// across CTAs in COST space, not bytes: every item costs its bytes plus a per-item
-// compute term (a window's dequant + MMA work is nearly independent of its width),
-// so CTAs that get many narrow windows get fewer of them.
-template <int D, int S>
-struct ItemGeo {
-  // record bytes of class k (0..2 = 2/4/8-bit, 3 = FP16), D-1 contract
-  static constexpr int64_t rb(int k) {
-    return k == 3 ? 4LL * S * D : (int64_t)S * D * (2 << k) / 4 + 4LL * D + 4LL * S;
-  }
-  static constexpr int REST_SZ = 64 * D;               // FP16 rest tile: 16 K rows + 16 V rows
-  static constexpr int sz(int k) { return k == 4 ? REST_SZ : (int)rb(k); }
-  // Cost of an item ~ its time on one SM inside a full decode launch (the CTA
-  // partition balances cost).  Measured per-class CTA-level item times on C5
-  // (tools/dbg_decode_time.py least-squares fit): 2-bit 0.167 us, 4-bit 0.182,
-  // 8-bit 0.249, FP16 0.251, 16-token rest tile ~0.1;
-  // expressed in units of S*D so other window sizes scale.
-  static constexpr int64_t cost(int k) {
-    return k == 4 ? 40LL * D : (int64_t)(k == 0 ? 156 : k == 1 ? 170 : k == 2 ? 233 : 235) * S * D / 100;
-  }
-};
-
-// Geometry of one unit (request b, kv head h).
-struct UnitGeo {
-  int b, h, nslots, rl, ntiles;
-  int so[5];
-  int64_t cs[5];                        // byte start of each class segment; cs[4] = image bytes
-  int64_t cc[5];                        // cost start of each class segment; cc[4] = windows' cost
-};
-
-template <int D, int S>
-WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
-  using IG = ItemGeo<D, S>;
-  g.b = u / a.H;
-  g.h = u - g.b * a.H;
-  const int32_t *so = a.seg_off + 5 * g.b;
-#pragma unroll
-  for (int k = 0; k < 5; k++) g.so[k] = so[k];
-  g.cs[0] = 0;
-  g.cc[0] = 0;
-#pragma unroll
-  for (int k = 0; k < 4; k++) {
-    const int64_t n = g.so[k + 1] - g.so[k];
-    g.cs[k + 1] = g.cs[k] + n * IG::rb(k);
-    g.cc[k + 1] = g.cc[k] + n * IG::cost(k);
-  }
-  g.nslots = g.so[4];
-  g.rl = a.rest_len ? a.rest_len[g.b] : 0;
-  g.rl = g.rl < 0 ? 0 : (g.rl > a.R_max ? a.R_max : g.rl);     // contract: rest_len clamped to R_max
-  g.ntiles = (g.rl + 15) / 16;
-}
-template <int D, int S>
-WQ_DEV int64_t unit_cost(const UnitGeo &g) {
-  return g.cc[4] + (int64_t)g.ntiles * ItemGeo<D, S>::cost(4);
-}
-
-// first item whose start (in cost units, relative to the unit) is >= x.  Planning
-// arithmetic runs in double (no 64-bit integer division on the producer's path);
-// every CTA evaluates the same expressions, so neighbouring CTAs agree on the cut.
-template <int D, int S>
-WQ_DEV int first_item(const UnitGeo &g, double x) {
-  using IG = ItemGeo<D, S>;
-  if (x <= 0.0) return 0;
-#pragma unroll
-  for (int k = 0; k < 4; k++) {
-    if (x <= (double)g.cc[k]) return g.so[k];
-    if (x < (double)g.cc[k + 1]) return g.so[k] + (int)ceil((x - (double)g.cc[k]) / (double)IG::cost(k));
-  }
-  if (x <= (double)g.cc[4]) return g.nslots;
-  const int t = (int)ceil((x - (double)g.cc[4]) / (double)IG::cost(4));
-  return g.nslots + (t < g.ntiles ? t : g.ntiles);
-}
-
-// Stage plan of one unit's item range [i0, i1): five "pieces" (the width-class
-// segments 2|4|8|16 and the FP16 rest tiles), each cut into stages of CAP(p)
-// equal-size items.  Producer and consumers walk the same plan.
-struct UnitPlan {
-  int lo[5], hi[5], nst[5];
-};
-template <int D, int S, int STAGE>
-WQ_DEV void plan_unit(const UnitGeo &g, int i0, int i1, UnitPlan &pl) {
-  using IG = ItemGeo<D, S>;
-#pragma unroll
-  for (int p = 0; p < 5; p++) {
-    const int a0 = p < 4 ? g.so[p] : g.nslots;
-    const int a1 = p < 4 ? g.so[p + 1] : g.nslots + g.ntiles;
-    const int lo = i0 > a0 ? i0 : a0;
-    const int hi = i1 < a1 ? i1 : a1;
-    const int cap = STAGE / IG::sz(p);
-    pl.lo[p] = lo;
-    pl.hi[p] = hi > lo ? hi : lo;
-    pl.nst[p] = (pl.hi[p] - pl.lo[p] + cap - 1) / cap;
-  }
-}
 
 struct WarpState {
   float m[2], l[2], vb[2];
@@ -155,57 +56,6 @@ struct WarpState {
 // -------------------------------------------------------------------------------------
 // consumer: one window (BITS in {2,4,8,16}) or one rest tile
 // -------------------------------------------------------------------------------------
-// Exact fp16 value pair of pair-slot P (compile-time after unrolling) of a lane chunk
-// (CENTER: code - 2^(BITS-1), the V side).
-template <int BITS, bool CENTER = false>
-WQ_DEV uint32_t deq_pair(const uint32_t *wd, int P) {
-  constexpr int PPW = 16 / BITS;
-  const uint32_t w = wd[P / PPW];
-  if constexpr (BITS == 16) {
-    return w;
-  } else if constexpr (BITS == 8) {
-    return (P % 2) == 0 ? dq_pair8<0, CENTER>(w) : dq_pair8<1, CENTER>(w);
-  } else if constexpr (BITS == 4) {
-    const uint32_t w8 = w >> 8;
-    switch (P % 4) {
-      case 0: return dq_pair<4, 0, CENTER>(w, w8);
-      case 1: return dq_pair<4, 1, CENTER>(w, w8);
-      case 2: return dq_pair<4, 2, CENTER>(w, w8);
-      default: return dq_pair<4, 3, CENTER>(w, w8);
-    }
-  } else {
-    const uint32_t w8 = w >> 8;
-    switch (P % 8) {
-      case 0: return dq_pair<2, 0, CENTER>(w, w8);
-      case 1: return dq_pair<2, 1, CENTER>(w, w8);
-      case 2: return dq_pair<2, 2, CENTER>(w, w8);
-      case 3: return dq_pair<2, 3, CENTER>(w, w8);
-      case 4: return dq_pair<2, 4, CENTER>(w, w8);
-      case 5: return dq_pair<2, 5, CENTER>(w, w8);
-      case 6: return dq_pair<2, 6, CENTER>(w, w8);
-      default: return dq_pair<2, 7, CENTER>(w, w8);
-    }
-  }
-}
-
-// Load a lane's chunk of one code tile (D*BITS/16 bytes) into words.
-template <int D, int BITS>
-WQ_DEV void load_chunk(uint32_t (&wd)[D * BITS / 64], const uint8_t *tile, int lane) {
-  constexpr int WPL = D * BITS / 64;
-  if constexpr (WPL >= 4) {
-    // D-1: 16-byte groups interleaved across lanes (conflict-free LDS.128)
-    const uint8_t *ch = tile + lane * 16;
-#pragma unroll
-    for (int i = 0; i < WPL / 4; i++) {
-      uint4 v = lds128(ch + 512 * i);
-      wd[4 * i] = v.x; wd[4 * i + 1] = v.y; wd[4 * i + 2] = v.z; wd[4 * i + 3] = v.w;
-    }
-  } else {
-    uint2 v = lds64(tile + lane * (D * BITS / 16));
-    wd[0] = v.x; wd[1] = v.y;
-  }
-}
-
 // V side of one tile: o[mt] += Vcode^T(16 ch x 16 tok) * P'(16 tok x 8 heads)
 template <int D, int BITS>
 WQ_DEV void tile_pv(const uint32_t (&wd)[D * BITS / 64], uint32_t pb0, uint32_t pb1, float (&o)[D / 16][4]) {
@@ -219,11 +69,6 @@ WQ_DEV void tile_pv(const uint32_t (&wd)[D * BITS / 64], uint32_t pb0, uint32_t 
   }
 }
 
-WQ_DEV float ex2f(float x) {                 // 2^x, MUFU.EX2 (rel. error ~2^-22, denormals flushed)
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 // Online softmax over NT tiles of raw scores t (logit = t * scale2 in the log2
 // domain), writes P' (p * s_t) as fp16 [token][8 heads] rows to the warp scratch.
@@ -430,26 +275,6 @@ WQ_DEV void do_rest(const uint8_t *Kb, const uint8_t *Vb, int ntok, const uint8_
 // -------------------------------------------------------------------------------------
 // the kernel
 // -------------------------------------------------------------------------------------
-// A CTA's work is a list of "entries" (unit u, items [i0, i1) of it).  The producer
-// lane publishes each entry's stage plan in a small shared ring and streams its
-// stages; consumers walk the same stages in order and take the items of every
-// stage round-robin (item k of the entry -> warp k % NCW): a static schedule, so
-// the only synchronisation per stage is one full-barrier wait and one
-// empty-barrier arrive per warp (empty counts NCW arrivals).
-struct Entry {
-  int u, n_u, c0, c1, rl, nslots, tag;
-  int lo[5], len[5], nst[5];
-};
-// This CTA's share, planned in the prologue by warp 0 (lane-parallel): units
-// [ua, ub) whole, or one unit split over CTAs [c0, c1) of which this CTA takes
-// items [i0, i1).
-struct CtaPlan {
-  int ua, ub, split, c0, c1, i0, i1;
-  int geo_ok;                           // geo/img_off of unit ua valid (handed over by warp 0)
-  int64_t img_off;
-  UnitGeo geo;
-};
-
 template <int D, int S>
 struct DecodeSmem {
   // a stage must hold the largest item (an FP16 window: 4*S*D bytes)
@@ -472,11 +297,6 @@ struct DecodeSmem {
   static constexpr size_t total = bar_off + 2 * NST * 8;
 };
 
-WQ_DEV uint64_t gtime() {      // profiling clock (debug & 8 only): global ns timer
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 template <int D, int S>
 __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
@@ -501,77 +321,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
 
   // ---- prologue (warp 0): unit cost prefix, then this CTA's share ----
   CtaPlan *cp = reinterpret_cast<CtaPlan *>(sm + SM::plan_off);
-  if (warp == 0) {
-    int64_t carry = 0;
-    UnitGeo gg;                                   // this lane's unit of the last chunk
-    int64_t ioff = 0;
-    for (int base = 0; base < U; base += 32) {
-      const int u = base + lane;
-      int64_t v = 0;
-      if (u < U) {
-        ioff = a.offs[u];
-        unit_geo<D, S>(a, u, gg);
-        v = unit_cost<D, S>(gg);
-      }
-      int64_t x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (u < U) ustart[u] = carry + x - v;
-      carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    if (lane == 0) ustart[U] = carry;
-    __syncwarp();
-    const int64_t T = carry;
-    int G = (int)(T / MIN_CTA_BYTES);
-    G = G < 1 ? 1 : (G > (int)gridDim.x ? (int)gridDim.x : G);
-    const int c = blockIdx.x;
-    if (U >= G || T <= 0) {
-      // whole units to the CTA owning their cost midpoint: a contiguous unit range
-      int ua = 0, ub = 0;
-      for (int base = 0; base < U; base += 32) {
-        const int u = base + lane;
-        int own = G;
-        if (u < U) {
-          const int64_t mid = ustart[u] + (ustart[u + 1] - ustart[u]) / 2;
-          own = T > 0 ? (int)((double)mid * G / (double)T) : 0;
-          own = own >= G ? G - 1 : own;
-        }
-        ua += __popc(__ballot_sync(0xffffffffu, own < c));
-        ub += __popc(__ballot_sync(0xffffffffu, own <= c));
-      }
-      if (lane == 0) { cp->ua = ua; cp->ub = ub; cp->split = 0; cp->c0 = c; cp->c1 = c + 1; }
-    } else {
-      // every unit gets 1 + its cost share of the G - U extra CTAs: unit u owns
-      // CTAs [c0(u), c0(u+1)), c0(U) = G
-      const int64_t extra = G - U;
-      int cnt = 0;
-      for (int base = 0; base < U; base += 32) {
-        const int u = base + lane;
-        const int c0u = u < U ? u + (int)rint((double)ustart[u] * extra / (double)T) : G;
-        cnt += __popc(__ballot_sync(0xffffffffu, u < U && c0u <= c));
-      }
-      const int u = cnt - 1;                      // c0(0) = 0 <= c: u >= 0
-      if (lane == 0) {
-        const int c0 = u + (int)rint((double)ustart[u] * extra / (double)T);
-        const int c1 = (u + 1 < U) ? (u + 1) + (int)rint((double)ustart[u + 1] * extra / (double)T) : G;
-        cp->ua = u; cp->ub = u + 1; cp->split = c1 - c0 > 1; cp->c0 = c0; cp->c1 = c1;
-      }
-    }
-    __syncwarp();
-    const int ua = cp->ua;
-    const int last_base = ((U - 1) / 32) * 32;
-    if (lane == 0) cp->geo_ok = 0;
-    __syncwarp();
-    if (ua < U && ua >= last_base && lane == ua - last_base) {
-      cp->geo = gg;
-      cp->img_off = ioff;
-      cp->geo_ok = 1;
-    }
-    if (lane == 0) *s_flag = G;
-  }
+  if (warp == 0) plan_cta<D, S, false>(a, ustart, cp, s_flag, lane);
   if (tid == 32) {
     for (int s = 0; s < NST; s++) {
       mbar_init(&full[s], 1);
@@ -593,94 +343,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
 
   if (warp == NCW) {
     // =========================== producer ===========================
-    if (lane == 0) {
-      using IG = ItemGeo<D, S>;
-      const uint64_t pol = policy_evict_first();
-      const bool nocopy = (a.debug & 2) != 0;
-      const CtaPlan P = *cp;
-      if (ts) ts[62] = gtime();
-      int sg = 0;                                  // stage number of this CTA
-      int uix = 0;                                 // entry number of this CTA
-      auto publish = [&](int u, int n_u, const UnitGeo *gg, const UnitPlan *pl) {
-        while (*reinterpret_cast<volatile int *>(units_done) < uix - (SM::NUS - 1)) {
-        }
-        Entry &d = ent[uix % SM::NUS];
-        d.u = u;
-        d.n_u = n_u;
-        d.c0 = P.split ? P.c0 : c;
-        d.c1 = P.split ? P.c1 : c + 1;
-        d.rl = gg ? gg->rl : 0;
-        d.nslots = gg ? gg->nslots : 0;
-#pragma unroll
-        for (int pp = 0; pp < 5; pp++) {
-          d.lo[pp] = pl ? pl->lo[pp] : 0;
-          d.len[pp] = pl ? pl->hi[pp] - pl->lo[pp] : 0;
-          d.nst[pp] = pl ? pl->nst[pp] : 0;
-        }
-        __threadfence_block();
-        *reinterpret_cast<volatile int *>(&d.tag) = uix;
-        if (ts && uix == 0) ts[60] = gtime();
-        uix++;
-      };
-      for (int u = P.ua; u < P.ub; u++) {
-        int64_t img_off;
-        UnitGeo gg;
-        if (u == P.ua && P.geo_ok) {
-          gg = P.geo;                              // from the prologue: no global round trip
-          img_off = P.img_off;
-        } else {
-          img_off = a.offs[u];
-          unit_geo<D, S>(a, u, gg);
-        }
-        int i0 = 0, i1 = gg.nslots + gg.ntiles;
-        if (P.split) {
-          const double ucost = (double)(ustart[u + 1] - ustart[u]);
-          const int k = c - P.c0, n = P.c1 - P.c0;
-          i0 = first_item<D, S>(gg, ucost * k / n);
-          if (k < n - 1) i1 = first_item<D, S>(gg, ucost * (k + 1) / n);
-        }
-        UnitPlan pl;
-        plan_unit<D, S, STAGE>(gg, i0, i1, pl);
-        bool published = false;
-        const uint8_t *img = a.packed + img_off;
-        const __half *kr = a.k_rest + gg.b * a.rs_b + gg.h * a.rs_h;
-        const __half *vr = a.v_rest + gg.b * a.rs_b + gg.h * a.rs_h;
-#pragma unroll
-        for (int p = 0; p < 5; p++) {
-          const int cap = STAGE / IG::sz(p);
-          for (int t = 0; t < pl.nst[p]; t++, sg++) {
-            const int slot = sg % NST;
-            const uint32_t fill = (uint32_t)(sg / NST);
-            const int f0 = pl.lo[p] + t * cap;
-            const int f1 = min(pl.hi[p], f0 + cap);
-            mbar_wait(&empty[slot], (fill & 1) ^ 1);
-            if (ts && sg < 64) ts[72 + sg] = clock64();
-            uint8_t *dst = ring + (size_t)slot * STAGE;
-            if (nocopy) {
-              mbar_arrive(&full[slot]);
-            } else if (p < 4) {
-              const uint32_t nb = (uint32_t)(f1 - f0) * IG::sz(p);
-              mbar_arrive_expect_tx(&full[slot], nb);
-              bulk_g2s_evict_first(dst, img + gg.cs[p] + (int64_t)(f0 - gg.so[p]) * IG::sz(p), nb, &full[slot], pol);
-            } else {
-              // rest tiles [f0, f1) = rows [r0, r1): one bulk copy for K, one for V
-              // (the rest buffers may be written by the preceding work: wait for it)
-              if (a.flags & WQ_DECODE_EARLY_) griddep_wait();
-              const int r0 = 16 * (f0 - gg.nslots);
-              const int r1 = min(gg.rl, 16 * (f1 - gg.nslots));
-              const uint32_t nb = (uint32_t)(r1 - r0) * 2u * D;
-              mbar_arrive_expect_tx(&full[slot], 2 * nb);
-              bulk_g2s_evict_first(dst, kr + (int64_t)r0 * D, nb, &full[slot], pol);
-              bulk_g2s_evict_first(dst + cap * 32 * D, vr + (int64_t)r0 * D, nb, &full[slot], pol);
-            }
-            if (!published) { publish(u, i1 - i0, &gg, &pl); published = true; }
-          }
-        }
-        if (!published) publish(u, i1 - i0, &gg, &pl);
-      }
-      publish(-1, 0, nullptr, nullptr);           // terminator
-      if (ts) ts[2] = gtime();
-    }
+    if (lane == 0) produce<D, S, false, STAGE, NST, SM::NUS>(a, *cp, ustart, ring, full, empty, ent, units_done, ts);
     return;
   }
 
@@ -740,7 +403,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
     int kbase = 0;                                 // entry item index of the stage's first item
 #pragma unroll
     for (int p = 0; p < 5; p++) {
-      using IG = ItemGeo<D, S>;
+      using IG = ItemGeo<D, S, false>;
       constexpr int SZ_[5] = {IG::sz(0), IG::sz(1), IG::sz(2), IG::sz(3), IG::sz(4)};
       const int sz = SZ_[p];
       const int cap = STAGE / sz;
@@ -865,70 +528,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       if (tid == 0) *s_flag = (atom_add_acq_rel_gpu(a.ws_cnt + u, 1) == c1 - c0 - 1);
       named_bar_sync(1, NCW * 32);
       if (ts && tid == 0) { ts[6] = *s_flag; ts[7] = c - c0; }
-      if (*s_flag) {
-        // every output element: the np partials' (m, l, o) in one batch of
-        // independent loads, then the log-sum-exp combination in registers
-        const int np = c1 - c0;
-        const int64_t stride = (int64_t)grp * (D + 2);
-        const float *pb = a.ws_part + (int64_t)(c0 + u) * stride;
-        constexpr int EPT_ = (8 * D + NCW * 32 - 1) / (NCW * 32);
-        float mM[EPT_], mL[EPT_], mO[EPT_];
-#pragma unroll
-        for (int e = 0; e < EPT_; e++) { mM[e] = -INFINITY; mL[e] = 0.f; mO[e] = 0.f; }
-        constexpr int CHP = 4;                    // partials per load batch
-        constexpr int EPT = (8 * D + NCW * 32 - 1) / (NCW * 32);   // elements per thread (max)
-        for (int b0 = 0; b0 < np || b0 == 0; b0 += CHP) {
-          // (the common case np <= CHP is one pass with every load of the thread in flight)
-          float mv[EPT][CHP], lv[EPT][CHP], ov[EPT][CHP];
-#pragma unroll
-          for (int e = 0; e < EPT; e++) {
-            const int idx = tid + e * NCW * 32;
-            const int j = idx / D, cc = idx - j * D;
-            const bool ie = idx < grp * D;
-            const float *hb = pb + j * (D + 2);
-#pragma unroll
-            for (int i = 0; i < CHP; i++) {
-              const bool ok = ie && b0 + i < np;
-              mv[e][i] = ok ? __ldcg(hb + (b0 + i) * stride) : -INFINITY;
-              lv[e][i] = ok ? __ldcg(hb + (b0 + i) * stride + 1) : 0.f;
-              ov[e][i] = ok ? __ldcg(hb + (b0 + i) * stride + 2 + cc) : 0.f;
-            }
-          }
-#pragma unroll
-          for (int e = 0; e < EPT; e++) {
-            float Mn = mM[e];
-#pragma unroll
-            for (int i = 0; i < CHP; i++) Mn = fmaxf(Mn, lv[e][i] > 0.f ? mv[e][i] : -INFINITY);
-            if (Mn != -INFINITY) {
-              const float r = exp2f(mM[e] - Mn);
-              mL[e] *= r;
-              mO[e] *= r;
-#pragma unroll
-              for (int i = 0; i < CHP; i++) {
-                const float f = lv[e][i] > 0.f ? exp2f(mv[e][i] - Mn) : 0.f;
-                mL[e] = fmaf(f, lv[e][i], mL[e]);
-                mO[e] = fmaf(f, ov[e][i], mO[e]);
-              }
-              mM[e] = Mn;
-            }
-          }
-          if (b0 + CHP >= np) break;
-        }
-#pragma unroll
-        for (int e = 0; e < EPT; e++) {
-          const int idx = tid + e * NCW * 32;
-          if (idx >= grp * D) continue;
-          const int j = idx / D, cc = idx - j * D;
-          const int64_t row = (int64_t)b * a.Hq + h * grp + j;
-          if (a.out) a.out[row * D + cc] = __float2half_rn(mL[e] > 0.f ? mO[e] / mL[e] : 0.f);
-          if (a.partial) {
-            float *pp = a.partial + row * (D + 2);
-            if (cc == 0) { pp[0] = mM[e] * 0.69314718055994530942f; pp[1] = mL[e]; }
-            pp[2 + cc] = mO[e];
-          }
-        }
-        if (tid == 0) a.ws_cnt[u] = 0;
-      }
+      if (*s_flag) merge_unit<D, NCW * 32>(a, tid, u, b, h, c0, c1);
     }
     if (ts && tid == 0) {
       const uint64_t t_e2 = clock64();
@@ -999,6 +599,11 @@ static cudaError_t launch_decode_t(const DecodeArgs &a, int num_sms, cudaStream_
 }
 
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st) {
+  // WQ_DECODE_TC=1 (head dim 128): the tcgen05/TMEM kernel of decode_tc.cu instead of
+  // this file's mma.sync kernel.  Parity-clean but ~4x slower on C5 (its dequantization
+  // warps are issue/latency bound), so it is opt-in.
+  static const bool use_tc = getenv("WQ_DECODE_TC") && atoi(getenv("WQ_DECODE_TC")) != 0;
+  if (a.d == 128 && use_tc) return launch_decode_tc(a, num_sms, st);
 #define WQ_D(DD, SS) \
   if (a.d == DD && a.S == SS) return launch_decode_t<DD, SS>(a, num_sms, st);
   WQ_D(64, 16) WQ_D(64, 32) WQ_D(64, 64) WQ_D(64, 128)

@@ -43,6 +43,31 @@ WQ_DEV void mbar_wait(uint64_t *b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// blocking wait with a suspend-time hint: the thread sleeps in hardware until the phase
+// completes (no spin loop competing for issue slots)
+WQ_DEV void mbar_wait_hint(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWQ_WAITH_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WQ_WAITH_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+// non-blocking: has the phase with this parity completed?
+WQ_DEV bool mbar_test(uint64_t *b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// polling wait with a nanosleep back-off, for waiters off the critical path (the
+// producer refilling a ring slot, consumers idling while the bottleneck stage runs)
+WQ_DEV void mbar_wait_sleep(uint64_t *b, uint32_t parity, uint32_t ns) {
+  while (!mbar_test(b, parity)) __nanosleep(ns);
+}
 // global -> shared bulk copy (TMA engine, 1-D), completes tx bytes on mbarrier b.
 // dst/src 16-byte aligned, bytes a multiple of 16.
 WQ_DEV void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
@@ -70,6 +95,119 @@ WQ_DEV uint64_t policy_evict_first() {
 // grid was launched without a programmatic dependency); allow dependents to launch.
 WQ_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 WQ_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+WQ_DEV uint64_t gtime() {      // profiling clock (debug & 8 only): global ns timer
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 (5th-gen tensor cores) and tensor memory, sm_100a.  Register layouts
+// and descriptor encodings verified against a CPU product by tools/tc_probe.cu.
+// ---------------------------------------------------------------------------
+WQ_DEV void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {     // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+WQ_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {      // whole warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+WQ_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+WQ_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+WQ_DEV void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+WQ_DEV void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
+WQ_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 16 TMEM lanes x 256 bits, x1: thread t holds r0,r1 = (lane t/4, cols 2(t%4), +1),
+// r2,r3 = (lane t/4 + 8, same cols): an mma.sync A fragment {a0,a1,a2,a3} stored as
+// {a0,a2,a1,a3} puts column pair p of each k16 block at elements 2(p>>1)+8(p&1)+{0,1}.
+WQ_DEV void tmem_st_16x256b_x1(uint32_t ta, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta), "r"(r0), "r"(r1),
+               "r"(r2), "r"(r3)
+               : "memory");
+}
+// x8: 8 consecutive 8-column blocks, registers 4i..4i+3 -> block i
+WQ_DEV void tmem_st_16x256b_x8(uint32_t ta, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+// 32 lanes x 32 bits: thread t <-> lane (warp%4)*32 + t, registers = 8 consecutive columns
+WQ_DEV void tmem_ld_32x32b_x8(uint32_t ta, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(ta)
+               : "memory");
+}
+WQ_DEV void tmem_ld_32x32b_x16(uint32_t ta, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(ta)
+      : "memory");
+}
+WQ_DEV void tmem_st_32x32b_x8(uint32_t ta, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem descriptor], kind::f16, fp32 accumulate (one thread)
+WQ_DEV void tc_mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// arrive on an mbarrier once every previously issued tcgen05.mma of this thread completed
+WQ_DEV void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// warp-wide variants: every lane executes, one elected lane issues
+WQ_DEV void tc_mma_ts_elect(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+WQ_DEV void tc_commit_elect(uint64_t *bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// instruction descriptor: fp16 A/B, fp32 D, A K-major, B K-major (0) or MN-major (1)
+__host__ __device__ constexpr uint32_t tc_idesc_f16(int M, int N, int b_mn_major) {
+  return (1u << 4) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// shared-memory matrix descriptor, no swizzle: core matrices of 8 rows x 16 B;
+// lbo = byte stride between core matrices along K, sbo = along M/N
+WQ_DEV uint64_t tc_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);
+}
+WQ_DEV void mbar_arrive_cnt(uint64_t *b, uint32_t cnt) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+WQ_DEV void sts128(void *p, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+WQ_DEV void sts64(void *p, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(smem_u32(p)), "r"(x), "r"(y) : "memory");
+}
 
 WQ_DEV int atom_add_acq_rel_gpu(int *p, int v) {
   int old;
@@ -183,6 +321,12 @@ WQ_DEV uint32_t dq_pair8(uint32_t w) {
   if constexpr (J == 0) asm("prmt.b32 %0, %1, %2, 0x7250;" : "=r"(x) : "r"(w), "r"(0x64646464u));
   else asm("prmt.b32 %0, %1, %2, 0x7351;" : "=r"(x) : "r"(w), "r"(0x64646464u));
   return h2u(__hsub2(u2h(x), u2h(CENTER ? 0x64806480u : 0x64006400u)));
+}
+
+WQ_DEV float ex2f(float x) {                 // 2^x, MUFU.EX2 (rel. error ~2^-22, denormals flushed)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 WQ_DEV float warp_max(float v, int xor_from = 1) {

@@ -54,6 +54,7 @@ struct DecodeArgs {
 };
 size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms);
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st);
+cudaError_t launch_decode_tc(const DecodeArgs &a, int num_sms, cudaStream_t st);   // d = 128
 cudaError_t launch_merge(const float *parts, int G, int BHq, int d, __half *out, cudaStream_t st);
 
 int device_sm_count();

@@ -339,3 +339,14 @@ def test_decode_early_flag_matches(orc):
         torch.cuda.synchronize()
         outs.append(torch.stack(got))
     assert torch.equal(outs[0], outs[1])
+
+
+def test_decode_tcgen05_variant_parity():
+    """The opt-in tcgen05/TMEM decode kernel (WQ_DECODE_TC=1, head dim 128) passes the same
+    decode parity cases against the oracle (run in a child process: the switch is read once)."""
+    import os, subprocess, sys
+    env = dict(os.environ, WQ_DECODE_TC="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", os.path.abspath(__file__),
+                        "-k", "(decode_parity or decode_all16 or decode_edge or config_layer) and not tcgen05"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
