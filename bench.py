@@ -346,11 +346,73 @@ def run_wq(args, rank, world, local_rank):
         "gpu_launches": w.launches_per_step() * args.steps,
         "clocks": clk.summary(),
     }
+    if rank == 0 and world == 1 and not args.no_ablation:
+        result["ablation_unfused_t9"] = run_ablation_unfused(w, stream)
     if rank == 0 and not args.no_e2e:
         result["e2e"] = run_e2e(w, args, stream)
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(cfg, w, args)
     return result
+
+
+def run_ablation_unfused(w, stream, n_layers=4, reps=5):
+    """SURVEY §8(f) row 3 / the paper's fusion ablation (T9): per decode
+    step the unfused path dequantizes the layer's cache to FP16 in HBM
+    (wq_dequantize_image) and then runs FP16 attention over it; the fused path is
+    wq_decode_attention on the packed image.  Per-layer device times over n_layers
+    rotated layers (each image >> L2), reps passes each."""
+    import torch
+    wq = w.wq
+    L = min(n_layers, w.L)
+    imgs = []
+    for l in range(L):
+        seg16, offs16 = wq.wq_dequant_layout(w.g, w.seg_r[l])
+        img16 = torch.zeros(int(offs16[-1].item()) + 16, dtype=torch.uint8, device=w.dev)
+        imgs.append((seg16, offs16, img16))
+    rl = w.rest_len[0]
+
+    def fused(l):
+        wq.wq_decode_attention(w.q[0, l], w.packed[l], w.offs[l], w.seg_r[l], w.g, w.kr[l], w.vr[l], rl,
+                               w.sm_scale, out=w.out[0, l], workspace=w.dws)
+
+    def dequant(l):
+        seg16, offs16, img16 = imgs[l]
+        wq.wq_dequantize_image(w.packed[l], w.offs[l], w.seg_r[l], w.g, offs16, img16)
+
+    def dec16(l):
+        seg16, offs16, img16 = imgs[l]
+        wq.wq_decode_attention(w.q[0, l], img16, offs16, seg16, w.g, w.kr[l], w.vr[l], rl, w.sm_scale,
+                               out=w.out[0, l], workspace=w.dws)
+
+    def timed(fn):
+        for l in range(L):
+            fn(l)                                          # warm-up pass
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            for l in range(L):
+                fn(l)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / (reps * L)       # us per layer call
+
+    t_f, t_d, t_16 = timed(fused), timed(dequant), timed(dec16)
+    del imgs
+    peak, _ = peaks()
+    dq_bytes = float(w.packed_bytes[0] + imgs_bytes(w, 0))
+    return {"fused_decode_us": round(t_f, 2), "dequantize_us": round(t_d, 2), "fp16_decode_us": round(t_16, 2),
+            "dequantize_GBps": round(dq_bytes / (t_d * 1e-6) / 1e9, 1),
+            "unfused_at_hbm_floor_us": round(dq_bytes / (peak * 1e9) * 1e6 + t_16, 2),
+            "unfused_us": round(t_d + t_16, 2), "unfused_over_fused": round((t_d + t_16) / t_f, 3),
+            "fp16_image_MB": round(imgs_bytes(w, 0) / 1e6, 1), "packed_image_MB": round(w.packed_bytes[0] / 1e6, 1),
+            "paper": "T9 (P:1026-1027, A800): attention per layer per token 0.82 ms fused vs 1.25 ms unfused "
+                     "(ratio 1.52)"}
+
+
+def imgs_bytes(w, l):
+    """bytes of layer l's FP16 image: every slot at 4*S*d bytes per (b, h)."""
+    n_slots = int(w.seg_r[l][:, 4].sum().item())
+    return n_slots * w.m.H * 4 * w.cfg.S * w.m.d
 
 
 def run_e2e(w, args, stream):
@@ -495,6 +557,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host (no CUDA graphs)")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the T9 unfused-baseline measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

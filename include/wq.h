@@ -253,6 +253,25 @@ wq_status wq_merge_partials(const float *parts, int32_t G, const wq_geom *g,
 wq_status wq_shard_slots(const int32_t *perm_l, const int32_t *seg_off_l, int32_t B, int32_t W,
                          int32_t G, int32_t r, int32_t *perm_r, int32_t *seg_off_r, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Unfused baseline of the fusion ablation (T9).
+ * The paper fuses dequantization into attention; the ablation first writes
+ * the whole cache back to FP16 in HBM and then runs FP16 attention.
+ *
+ * wq_dequant_layout: seg16 i32 [B][5] = {0,0,0,0,nslots_b} (every slot of the FP16
+ *   image is in class 16) and offs16 i64 [B*H+1], the FP16 image's (b, h) offsets.
+ * wq_dequantize_image: img16 (>= offs16[B*H] bytes, 16-byte aligned) receives, for
+ *   every slot of the packed layer image, an FP16 record (D-1 width-16 layout, same
+ *   slot order, so perm_l still maps slots to windows) holding
+ *     x^16 = RN_fp16(mn + s * code)    (the exact Eq.15 value, one rounding to fp16)
+ *   for b-bit records and the stored values for FP16 records.  Bit-exact with the
+ *   oracle.  Decode the result with wq_decode_attention(..., img16, offs16, seg16, ...).
+ * Errors: WQ_EINVAL (NULL, misaligned), WQ_ESHAPE (geometry). */
+wq_status wq_dequant_layout(const wq_geom *g, const int32_t *seg_off_l, int32_t *seg16, int64_t *offs16,
+                            void *stream);
+wq_status wq_dequantize_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l,
+                              const wq_geom *g, const int64_t *offs16, uint8_t *img16, void *stream);
+
 /* Thread-local message of the last non-OK status of this thread. */
 const char *wq_last_error(void);
 

@@ -85,6 +85,8 @@ def lib():
                 "wqo_bruteforce_attention": (None, [P, P, P, P, I32, C.POINTER(Geom), P, I32, P,
                                                     P, P, P, P, F32, P]),
                 "wqo_merge": (None, [P, I32, I32, I32, P]),
+                "wqo_f64_to_f16_rn": (C.c_uint16, [F64]),
+                "wqo_dequantize_image": (None, [P, P, P, C.POINTER(Geom), P, P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -282,3 +284,19 @@ def merge(parts: np.ndarray) -> np.ndarray:
     out = np.zeros((B, Hq, d2 - 2), np.float64)
     lib().wqo_merge(_p(parts), G, B * Hq, d2 - 2, _p(out))
     return out
+
+
+def f64_to_f16_rn(x: float) -> int:
+    return int(lib().wqo_f64_to_f16_rn(float(x)))
+
+
+def dequantize_image(packed, offs, seg_off_l, g: Geom):
+    """T9 unfused baseline: the FP16 image (u8) of a packed layer image and its (b, h) offsets."""
+    seg_off_l = np.ascontiguousarray(seg_off_l, np.int32)
+    seg16 = np.zeros_like(seg_off_l)
+    seg16[:, 4] = seg_off_l[:, 4]
+    offs16 = layer_layout(g, seg16)
+    img16 = np.zeros(max(int(offs16[-1]), 16), np.uint8)
+    lib().wqo_dequantize_image(_p(np.ascontiguousarray(packed, np.uint8)), _p(np.ascontiguousarray(offs, np.int64)),
+                               _p(seg_off_l), C.byref(g), _p(offs16), _p(img16))
+    return img16, offs16, seg16

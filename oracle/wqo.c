@@ -72,6 +72,20 @@ uint16_t wqo_f32_to_f16_rn(float xf) {
   return sign | enc_mag(n * qu);
 }
 
+uint16_t wqo_f64_to_f16_rn(double x) {
+  if (isnan(x)) return 0x7E00;
+  uint16_t sign = signbit(x) ? 0x8000 : 0;
+  double a = fabs(x);
+  if (isinf(x)) return sign | 0x7C00;
+  if (a >= 65520.0) return sign | 0x7C00;                /* halfway to 2^16 rounds to inf */
+  if (a == 0.0) return sign;
+  double qu = quantum(a);
+  double n = floor(a / qu);
+  double rem = a / qu - n;                               /* exact for dyadic a */
+  if (rem > 0.5 || (rem == 0.5 && fmod(n, 2.0) == 1.0)) n += 1.0;
+  return sign | enc_mag(n * qu);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Eq.10-11, readings Q9 (n widths) and Q10 (clamp s, alpha > 0)  */
 /* ------------------------------------------------------------------------ */
@@ -642,5 +656,38 @@ void wqo_merge(const double *parts, int32_t G, int32_t BHq, int32_t d, double *o
       for (int c = 0; c < d; c++) out[i * d + c] += f * p[2 + c];
     }
     for (int c = 0; c < d; c++) out[i * d + c] = (l > 0.0) ? out[i * d + c] / l : 0.0;
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* T9 unfused baseline: dequantize the whole image to FP16.      */
+/* ------------------------------------------------------------------------ */
+void wqo_dequantize_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l,
+                          const wqo_geom *g, const int64_t *offs16, uint8_t *img16) {
+  int d = g->d, S = g->S;
+  int64_t rec16 = wqo_record_bytes(16, d, S), kbytes16 = (int64_t)S * d * 2;
+#pragma omp parallel for collapse(2) schedule(dynamic)
+  for (int b = 0; b < g->B; b++) {
+    for (int h = 0; h < g->H; h++) {
+      const int32_t *so = seg_off_l + (int64_t)b * 5;
+      double *kh = (double *)malloc(sizeof(double) * (size_t)S * d);
+      double *vh = (double *)malloc(sizeof(double) * (size_t)S * d);
+      for (int slot = 0; slot < so[4]; slot++) {
+        int bits;
+        int64_t roff = slot_offset(g, so, slot, &bits);
+        const uint8_t *rec = packed + offs[(int64_t)b * g->H + h] + roff;
+        uint8_t *dst = img16 + offs16[(int64_t)b * g->H + h] + (int64_t)slot * rec16;
+        wqo_dequant_record(rec, bits, d, S, kh, vh);       /* exact x^ = mn + s*code (fp16 values if 16) */
+        for (int t = 0; t < S; t++)
+          for (int c = 0; c < d; c++) {
+            int64_t bo; int bit;
+            wqo_code_pos(0, d, 16, t, c, &bo, &bit);
+            put_code(dst, bo, bit, 16, wqo_f64_to_f16_rn(kh[(int64_t)t * d + c]));
+            wqo_code_pos(1, d, 16, t, c, &bo, &bit);
+            put_code(dst + kbytes16, bo, bit, 16, wqo_f64_to_f16_rn(vh[(int64_t)t * d + c]));
+          }
+      }
+      free(kh); free(vh);
+    }
   }
 }

@@ -19,6 +19,8 @@
  *                         rebuilt in ORIGINAL token order (Eq.12-13)
  *   wqo_bruteforce_attention    Eq.2-3 on the unquantized fp16 K/V
  *   wqo_merge             LSE merge of shard partials
+ *   wqo_dequantize_image  T9 unfused baseline: every record
+ *                         rewritten as FP16, x^16 = RN_fp16(mn + s*code)
  */
 #ifndef WQO_H_
 #define WQO_H_
@@ -33,6 +35,7 @@ typedef struct {
 double   wqo_f16_to_f64(uint16_t h);
 uint16_t wqo_f32_to_f16_ru(float x);   /* round toward +infinity */
 uint16_t wqo_f32_to_f16_rn(float x);   /* round to nearest, ties to even */
+uint16_t wqo_f64_to_f16_rn(double x);  /* round to nearest, ties to even */
 
 /* Eq.10-11 */
 double wqo_f1(double s, double alpha);
@@ -101,5 +104,13 @@ void wqo_bruteforce_attention(const uint16_t *q, const uint16_t *k, const uint16
 
 /* parts [G][B*Hq][d+2] (m, l, o) -> out [B*Hq][d] */
 void wqo_merge(const double *parts, int32_t G, int32_t BHq, int32_t d, double *out);
+
+/* T9's unfused baseline: every slot of the
+ * packed layer image rewritten as an FP16 record (D-1 width-16 layout) in the same
+ * slot order at img16 + offs16[b*H+h] + slot * 4*S*d; b-bit values become
+ * RN_fp16(mn + s*code) (Eq.15, exact sum, one rounding), FP16 values are copied.
+ * offs16 = wqo_layer_layout of seg16 = {0,0,0,0,nslots}. */
+void wqo_dequantize_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l,
+                          const wqo_geom *g, const int64_t *offs16, uint8_t *img16);
 
 #endif

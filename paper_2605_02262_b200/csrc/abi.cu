@@ -256,4 +256,25 @@ wq_status wq_shard_slots(const int32_t *perm_l, const int32_t *seg_off_l, int32_
                      "shard");
 }
 
+wq_status wq_dequant_layout(const wq_geom *g, const int32_t *seg_off_l, int32_t *seg16, int64_t *offs16, void *stream) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!seg_off_l || !seg16 || !offs16) return fail(WQ_EINVAL, "NULL pointer");
+  if (g->B > 4096) return fail(WQ_ESHAPE, "B=%d > 4096", g->B);
+  return cuda_status(wq::launch_dequant_layout(seg_off_l, g->B, g->H, g->d, g->S, seg16, offs16, S_(stream)),
+                     "dequant layout");
+}
+
+wq_status wq_dequantize_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l, const wq_geom *g,
+                              const int64_t *offs16, uint8_t *img16, void *stream) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!packed || !offs || !seg_off_l || !offs16 || !img16) return fail(WQ_EINVAL, "NULL pointer");
+  if (!aligned16(packed) || !aligned16(img16)) return fail(WQ_EINVAL, "images must be 16-byte aligned");
+  const int W = g->M / g->S;
+  return cuda_status(wq::launch_dequant_image(packed, offs, seg_off_l, g->B, g->H, W, g->d, g->S, offs16, img16,
+                                              S_(stream)),
+                     "dequantize image");
+}
+
 }  // extern "C"

@@ -57,6 +57,11 @@ cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st);
 cudaError_t launch_decode_tc(const DecodeArgs &a, int num_sms, cudaStream_t st);   // d = 128
 cudaError_t launch_merge(const float *parts, int G, int BHq, int d, __half *out, cudaStream_t st);
 
+cudaError_t launch_dequant_layout(const int32_t *seg_off, int B, int H, int d, int S, int32_t *seg16, int64_t *offs16,
+                                  cudaStream_t st);
+cudaError_t launch_dequant_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off, int B, int H,
+                                 int W, int d, int S, const int64_t *offs16, uint8_t *img16, cudaStream_t st);
+
 int device_sm_count();
 
 }  // namespace wq

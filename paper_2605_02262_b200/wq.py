@@ -71,6 +71,8 @@ def load(build_if_missing: bool = True):
         "wq_decode_attention_ex": [P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, P, SZ, C.c_uint32, P],
         "wq_merge_partials": [P, I32, C.POINTER(Geom), P, P],
         "wq_shard_slots": [P, P, I32, I32, I32, I32, P, P, P],
+        "wq_dequant_layout": [C.POINTER(Geom), P, P, P, P],
+        "wq_dequantize_image": [P, P, P, C.POINTER(Geom), P, P, P],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -87,7 +89,8 @@ def load(build_if_missing: bool = True):
 def exported_symbols():
     return ["wq_thresholds", "wq_window_scores_workspace", "wq_window_scores", "wq_assign_bits",
             "wq_packed_bytes", "wq_layer_layout", "wq_reorder_quantize_pack", "wq_decode_workspace",
-            "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_last_error", "wq_version"]
+            "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_dequant_layout", "wq_dequantize_image",
+            "wq_last_error", "wq_version"]
 
 
 def _check(rc: int):
@@ -241,3 +244,19 @@ def wq_shard_slots(perm_l: torch.Tensor, seg_off_l: torch.Tensor, G: int, r: int
     _check(load().wq_shard_slots(_ptr(perm_l), _ptr(seg_off_l), B, W, G, r, _ptr(perm_r), _ptr(seg_off_r),
                                  _stream(stream)))
     return perm_r, seg_off_r
+
+
+def wq_dequant_layout(g: Geom, seg_off_l: torch.Tensor, stream=None):
+    """(seg16 i32 [B][5], offs16 i64 [B*H+1]) of the FP16 image of the unfused baseline (T9)."""
+    seg16 = torch.empty_like(seg_off_l)
+    offs16 = torch.empty(g.B * g.H + 1, dtype=torch.int64, device=seg_off_l.device)
+    _check(load().wq_dequant_layout(C.byref(g), _ptr(seg_off_l), _ptr(seg16), _ptr(offs16), _stream(stream)))
+    return seg16, offs16
+
+
+def wq_dequantize_image(packed: torch.Tensor, offs: torch.Tensor, seg_off_l: torch.Tensor, g: Geom,
+                        offs16: torch.Tensor, img16: torch.Tensor, stream=None) -> torch.Tensor:
+    """Dequantize every record of a packed layer image into the FP16 image img16 (T9 unfused path)."""
+    _check(load().wq_dequantize_image(_ptr(packed), _ptr(offs), _ptr(seg_off_l), C.byref(g), _ptr(offs16),
+                                      _ptr(img16), _stream(stream)))
+    return img16

@@ -350,3 +350,32 @@ def test_decode_tcgen05_variant_parity():
                         "-k", "(decode_parity or decode_all16 or decode_edge or config_layer) and not tcgen05"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("d,S,W,tail,B,H,Hq", [(128, 32, 12, 7, 2, 4, 28), (64, 16, 9, 5, 2, 2, 14),
+                                               (128, 128, 3, 9, 2, 2, 8)])
+def test_unfused_baseline_parity(orc, d, S, W, tail, B, H, Hq):
+    """T9 unfused path: the FP16 image is bit-exact with the oracle's and its decode
+    matches the oracle's attention over that image."""
+    c = small_case(300 + d + S, d=d, S=S, W=W, tail=tail, B=B, H=H, Hq=Hq)
+    g = c["g"]
+    sc = wq.wq_window_scores(c["vis"], c["txt"], S)
+    thr = orc.thresholds([0.45], 2.0, 4)
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
+    sm = 1 / math.sqrt(d)
+    offs, packed, _, _ = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm[0], seg[0], c["q"], sm)
+    seg16, offs16 = wq.wq_dequant_layout(g, seg[0])
+    img16 = torch.zeros(int(offs16[-1].item()) + 16, dtype=torch.uint8, device="cuda")
+    wq.wq_dequantize_image(packed, offs, seg[0], g, offs16, img16)
+    out = torch.empty((g.B, g.Hq, g.d), dtype=torch.float16, device="cuda")
+    wq.wq_decode_attention(c["q"], img16, offs16, seg16, g, c["kr"], c["vr"], c["rest_len"], sm, out=out)
+    torch.cuda.synchronize()
+    rimg, roffs16, rseg16 = orc.dequantize_image(packed.cpu().numpy(), offs.cpu().numpy(), seg[0].cpu().numpy(),
+                                                 ogeom(orc, g))
+    assert np.array_equal(seg16.cpu().numpy(), rseg16)
+    assert np.array_equal(offs16.cpu().numpy(), roffs16)
+    n = int(roffs16[-1])
+    assert np.array_equal(img16.cpu().numpy()[:n], rimg[:n])
+    ref = orc.decode_attention(c["q"].cpu().numpy(), rimg, roffs16, rseg16, perm[0].cpu().numpy(), ogeom(orc, g),
+                               c["kr"].cpu().numpy(), c["vr"].cpu().numpy(), c["rest_len"].cpu().numpy(), sm)
+    assert rel_err(out.float().cpu().numpy(), ref) <= ATTN_TOL

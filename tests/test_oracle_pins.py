@@ -599,3 +599,55 @@ def test_param_layout_hand_derived(orc):
     # every param slot used exactly once (K: 2 x d halves in 4d bytes)
     used = sorted(orc.param_pos(0, 128, c, m) for c in range(128) for m in (0, 1))
     assert used == list(range(0, 4 * 128, 2))
+
+
+# --------------------------------------------------------------------------------------
+# T9 unfused baseline: dequantize the image to FP16
+# --------------------------------------------------------------------------------------
+def test_f64_to_f16_rn_matches_numpy(orc):
+    """RN to fp16 from fp64 (incl. exact ties of dyadic values) against numpy's astype."""
+    x = _boundary_floats().astype(np.float64)
+    h = np.arange(0, 0x7BFF, dtype=np.uint16).view(np.float16).astype(np.float64)
+    ties = (h[:-1] + h[1:]) / 2                         # exact midpoints: ties to even
+    x = np.concatenate([x, ties, -ties, ties + 2.0 ** -40, ties - 2.0 ** -40])
+    x = x[np.abs(x) < 65520]
+    got = np.array([orc.f64_to_f16_rn(float(v)) for v in x], np.uint16)
+    assert np.array_equal(got, x.astype(np.float16).view(np.uint16))
+
+
+def test_dequantize_image_values(orc):
+    """Every FP16 record holds RN_fp16 of the exact dequantized values (numpy rounding of
+    the fp64 record dequantization); FP16 windows are copied; slot order is kept."""
+    c = _small_case(orc, seed=13)
+    g = c["g"]
+    packed, offs = orc.reorder_quantize_pack(c["K"], c["V"], 0, g, c["perm"], c["seg"])
+    img16, offs16, seg16 = orc.dequantize_image(packed, offs, c["seg"], g)
+    assert np.array_equal(seg16[:, :4], np.zeros_like(seg16[:, :4]))
+    assert np.array_equal(seg16[:, 4], c["seg"][:, 4])
+    rb16 = orc.record_bytes(16, c["d"], c["S"])
+    for b in range(g.B):
+        for h in range(g.H):
+            off, off16 = int(offs[b * g.H + h]), int(offs16[b * g.H + h])
+            for slot in range(c["seg"][b, 4]):
+                k = int(np.searchsorted(c["seg"][b, 1:], slot, side="right"))
+                bits = (2, 4, 8, 16)[k]
+                rb = orc.record_bytes(bits, c["d"], c["S"])
+                kx, vx = orc.dequant_record(packed[off:off + rb], bits, c["d"], c["S"])
+                k16, v16 = orc.dequant_record(img16[off16 + slot * rb16:off16 + (slot + 1) * rb16], 16, c["d"], c["S"])
+                assert np.array_equal(k16, kx.astype(np.float16).astype(np.float64))
+                assert np.array_equal(v16, vx.astype(np.float16).astype(np.float64))
+                off += rb
+
+
+def test_dequantize_image_decode_close_to_fused(orc):
+    """Attention over the FP16 image differs from the fused (exact-dequant) attention
+    only by the fp16 rounding of the dequantized values."""
+    c = _small_case(orc, seed=14)
+    g = c["g"]
+    packed, offs = orc.reorder_quantize_pack(c["K"], c["V"], 0, g, c["perm"], c["seg"])
+    img16, offs16, seg16 = orc.dequantize_image(packed, offs, c["seg"], g)
+    sm = 1 / math.sqrt(c["d"])
+    a = orc.decode_attention(c["q"], packed, offs, c["seg"], c["perm"], g, c["kr"], c["vr"], c["rest_len"], sm)
+    b = orc.decode_attention(c["q"], img16, offs16, seg16, c["perm"], g, c["kr"], c["vr"], c["rest_len"], sm)
+    assert np.max(np.abs(a - b)) / np.max(np.abs(a)) < 5e-3
+    assert not np.array_equal(a, b)

@@ -4,7 +4,7 @@
 set -e
 RE=$1; TAG=$2; SKIP=${3:-2}; shift 3 || true
 mkdir -p gpurun_out
-ARGS="--layers 2 --n-gen 1 --steps 1 --warmup 1 --no-e2e --no-cpu $*"
+ARGS="--layers 2 --n-gen 1 --steps 1 --warmup 1 --no-e2e --no-cpu --no-ablation $*"
 python bench.py $ARGS > gpurun_out/prof_plain_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:$RE -s $SKIP -c 1 \
     -o gpurun_out/prof_$TAG -f python bench.py $ARGS > gpurun_out/prof_ncu_$TAG.log 2>&1
