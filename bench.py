@@ -348,6 +348,7 @@ def run_wq(args, rank, world, local_rank):
     }
     if rank == 0 and world == 1 and not args.no_ablation:
         result["ablation_unfused_t9"] = run_ablation_unfused(w, stream)
+        result["ablation_unreordered_t8"] = run_ablation_unreordered(w, stream)
     if rank == 0 and not args.no_e2e:
         result["e2e"] = run_e2e(w, args, stream)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -407,6 +408,50 @@ def run_ablation_unfused(w, stream, n_layers=4, reps=5):
             "fp16_image_MB": round(imgs_bytes(w, 0) / 1e6, 1), "packed_image_MB": round(w.packed_bytes[0] / 1e6, 1),
             "paper": "T9 (P:1026-1027, A800): attention per layer per token 0.82 ms fused vs 1.25 ms unfused "
                      "(ratio 1.52)"}
+
+
+def run_ablation_unreordered(w, stream, n_layers=4, reps=5):
+    """SURVEY §8(f) row 1 / the paper's reordering ablation (T8, "Module III
+    off"): the same records stored in original window order (wq_unreorder_image) and
+    decoded in that order with a per-window width dispatch, against the reordered decode.
+    Per-layer device times over n_layers rotated layers, reps passes each."""
+    import torch
+    wq = w.wq
+    L = min(n_layers, w.L)
+    ur = []
+    for l in range(L):
+        woff = wq.wq_unreordered_layout(w.g, w.bits[l].contiguous())
+        uimg = torch.zeros_like(w.packed[l])
+        wq.wq_unreorder_image(w.packed[l], w.offs[l], w.seg_r[l], w.perm_r[l], w.g, woff, uimg)
+        ur.append((woff, uimg))
+    rl = w.rest_len[0]
+
+    def reordered(l):
+        wq.wq_decode_attention(w.q[0, l], w.packed[l], w.offs[l], w.seg_r[l], w.g, w.kr[l], w.vr[l], rl,
+                               w.sm_scale, out=w.out[0, l], workspace=w.dws)
+
+    def unreordered(l):
+        woff, uimg = ur[l]
+        wq.wq_decode_attention_unreordered(w.q[0, l], uimg, w.offs[l], w.seg_r[l], woff, w.g, w.kr[l], w.vr[l],
+                                           rl, w.sm_scale, out=w.out[0, l], workspace=w.dws)
+
+    def timed(fn):
+        for l in range(L):
+            fn(l)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            for l in range(L):
+                fn(l)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / (reps * L)
+
+    t_r, t_u = timed(reordered), timed(unreordered)
+    del ur
+    return {"reordered_decode_us": round(t_r, 2), "unreordered_decode_us": round(t_u, 2),
+            "unreordered_over_reordered": round(t_u / t_r, 3),
+            "paper": "T8 (P:1006-1008, A800, whole model): 1250 tokens/s with reordering vs 500 without (2.5x)"}
 
 
 def imgs_bytes(w, l):

@@ -272,6 +272,31 @@ wq_status wq_dequant_layout(const wq_geom *g, const int32_t *seg_off_l, int32_t 
 wq_status wq_dequantize_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l,
                               const wq_geom *g, const int64_t *offs16, uint8_t *img16, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * "Module III off" baseline of the reordering ablation (T8; P:401:
+ * without reordering, windows of different precision stay interleaved in the cache).
+ * SURVEY.md §8(f) row 1.
+ *
+ * wq_unreordered_layout: woff i64 [B][W+1], woff[b][w] = sum_{w'<w} record bytes of
+ *   width bits_l[b][w'] (bits_l u8 [B][W] of the layer, from wq_assign_bits).
+ * wq_unreorder_image: uimg (>= offs[B*H] bytes, 16-byte aligned) receives the records of
+ *   the packed image in ORIGINAL window order: window w of (b, h) at
+ *   offs[b*H+h] + woff[b][w] (records are quantized independently, so this is the byte
+ *   image a quantizer without the reordering step writes).
+ * wq_decode_attention_unreordered: wq_decode_attention over uimg; windows are visited
+ *   in original order, each dispatched on its own width.  Same outputs/workspace/errors
+ *   as wq_decode_attention (the result equals the reordered decode, Eq.12-13). */
+wq_status wq_unreordered_layout(const wq_geom *g, const uint8_t *bits_l, int64_t *woff, void *stream);
+wq_status wq_unreorder_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l,
+                             const int32_t *perm_l, const wq_geom *g, const int64_t *woff, uint8_t *uimg,
+                             void *stream);
+wq_status wq_decode_attention_unreordered(const void *q, const uint8_t *uimg, const int64_t *offs,
+                                          const int32_t *seg_off_l, const int64_t *woff, const wq_geom *g,
+                                          const void *k_rest, const void *v_rest,
+                                          const int64_t rest_strides[2], const int32_t *rest_len,
+                                          int32_t R_max, float sm_scale, void *out, float *partial,
+                                          void *workspace, size_t workspace_bytes, void *stream);
+
 /* Thread-local message of the last non-OK status of this thread. */
 const char *wq_last_error(void);
 

@@ -198,11 +198,11 @@ wq_status wq_decode_attention(const void *q, const uint8_t *packed, const int64_
                                 sm_scale, out, partial, workspace, workspace_bytes, 0u, stream);
 }
 
-wq_status wq_decode_attention_ex(const void *q, const uint8_t *packed, const int64_t *offs,
-                                 const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
-                                 const void *v_rest, const int64_t rest_strides[2], const int32_t *rest_len,
-                                 int32_t R_max, float sm_scale, void *out, float *partial, void *workspace,
-                                 size_t workspace_bytes, uint32_t flags, void *stream) {
+static wq_status decode_impl(const void *q, const uint8_t *packed, const int64_t *offs,
+                             const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
+                             const void *v_rest, const int64_t rest_strides[2], const int32_t *rest_len,
+                             int32_t R_max, float sm_scale, void *out, float *partial, void *workspace,
+                             size_t workspace_bytes, uint32_t flags, const int64_t *woff, void *stream) {
   if (flags & ~(uint32_t)WQ_DECODE_EARLY) return fail(WQ_EINVAL, "unknown decode flags 0x%x", flags);
   wq_status s = check_geom(g, true);
   if (s != WQ_OK) return s;
@@ -228,6 +228,7 @@ wq_status wq_decode_attention_ex(const void *q, const uint8_t *packed, const int
   { const char *dbg = getenv("WQ_DECODE_DEBUG"); a.debug = dbg ? atoi(dbg) : 0; }
   a.out = (__half *)out; a.partial = partial;
   a.flags = flags;
+  a.woff = woff;
   const int grp = a.grp;
   size_t part = (size_t)(sms + g->B * g->H) * grp * (g->d + 2) * sizeof(float);
   part = (part + 255) / 256 * 256;
@@ -237,6 +238,45 @@ wq_status wq_decode_attention_ex(const void *q, const uint8_t *packed, const int
   a.ws_ts = (a.debug & 8) ? reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(workspace) + part + cntb)
                           : nullptr;
   return cuda_status(wq::launch_decode(a, sms, S_(stream)), "decode");
+}
+
+wq_status wq_decode_attention_ex(const void *q, const uint8_t *packed, const int64_t *offs,
+                                 const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
+                                 const void *v_rest, const int64_t rest_strides[2], const int32_t *rest_len,
+                                 int32_t R_max, float sm_scale, void *out, float *partial, void *workspace,
+                                 size_t workspace_bytes, uint32_t flags, void *stream) {
+  return decode_impl(q, packed, offs, seg_off_l, g, k_rest, v_rest, rest_strides, rest_len, R_max, sm_scale, out,
+                     partial, workspace, workspace_bytes, flags, nullptr, stream);
+}
+
+wq_status wq_unreordered_layout(const wq_geom *g, const uint8_t *bits_l, int64_t *woff, void *stream) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!bits_l || !woff) return fail(WQ_EINVAL, "NULL pointer");
+  return cuda_status(wq::launch_unreordered_layout(bits_l, g->B, g->M / g->S, g->d, g->S, woff, S_(stream)),
+                     "unreordered layout");
+}
+
+wq_status wq_unreorder_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l,
+                             const int32_t *perm_l, const wq_geom *g, const int64_t *woff, uint8_t *uimg,
+                             void *stream) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!packed || !offs || !seg_off_l || !perm_l || !woff || !uimg) return fail(WQ_EINVAL, "NULL pointer");
+  if (!aligned16(packed) || !aligned16(uimg)) return fail(WQ_EINVAL, "images must be 16-byte aligned");
+  return cuda_status(wq::launch_unreorder_image(packed, offs, seg_off_l, perm_l, g->B, g->H, g->M / g->S, g->d, g->S,
+                                                woff, uimg, S_(stream)),
+                     "unreorder image");
+}
+
+wq_status wq_decode_attention_unreordered(const void *q, const uint8_t *uimg, const int64_t *offs,
+                                          const int32_t *seg_off_l, const int64_t *woff, const wq_geom *g,
+                                          const void *k_rest, const void *v_rest, const int64_t rest_strides[2],
+                                          const int32_t *rest_len, int32_t R_max, float sm_scale, void *out,
+                                          float *partial, void *workspace, size_t workspace_bytes, void *stream) {
+  if (!woff) return fail(WQ_EINVAL, "NULL woff");
+  return decode_impl(q, uimg, offs, seg_off_l, g, k_rest, v_rest, rest_strides, rest_len, R_max, sm_scale, out,
+                     partial, workspace, workspace_bytes, 0u, woff, stream);
 }
 
 wq_status wq_merge_partials(const float *parts, int32_t G, const wq_geom *g, void *out, void *stream) {

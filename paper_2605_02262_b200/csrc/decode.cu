@@ -294,11 +294,105 @@ struct DecodeSmem {
   static constexpr size_t plan_off = ent_off + NUS * sizeof(Entry);
   static constexpr size_t misc_off = plan_off + sizeof(CtaPlan);
   static constexpr size_t bar_off = (misc_off + 16 + 15) / 16 * 16;
-  static constexpr size_t total = bar_off + 2 * NST * 8;
+  // unreordered mode (UR): per ring slot the producer's item table {n, (offset, class) x n}
+  static constexpr int MAXI = (int)(STAGE / (S * D / 2 + 4 * D + 4 * S));   // most records per stage
+  static constexpr int TABN = 2 + 2 * MAXI;
+  static constexpr size_t tab_off = bar_off + 2 * NST * 8;
+  static constexpr size_t total = tab_off + (size_t)NST * TABN * 4;
 };
 
+// Producer of the unreordered image (UR): a unit's windows are
+// streamed in ORIGINAL order; a stage is the longest run of consecutive records (mixed
+// widths, contiguous bytes) that fits, one bulk copy, described to the consumers by a
+// table {n, (byte offset, class) per record} written before the stage's full barrier
+// arrive (release).  Split units give CTA k of n the windows [W k/n, W (k+1)/n) and the
+// last CTA the FP16 rest tiles.
+template <int D, int S, int STAGE, int NST, int NUS, int TABN>
+WQ_DEV void produce_ur(const DecodeArgs &a, const CtaPlan &P, uint8_t *ring, uint64_t *full, uint64_t *empty,
+                       Entry *ent, int *units_done, int *tab) {
+  using IG = ItemGeo<D, S, false>;
+  constexpr int MAXI = (TABN - 2) / 2;
+  const int c = blockIdx.x;
+  const uint64_t pol = policy_evict_first();
+  int sg = 0, uix = 0;
+  auto publish = [&](int u, int n_u, int lo0, int len0, int rl, int nslots, int lo4, int len4, int nst4) {
+    while (*reinterpret_cast<volatile int *>(units_done) < uix - (NUS - 1)) {
+    }
+    Entry &d = ent[uix % NUS];
+    d.u = u; d.n_u = n_u;
+    d.c0 = P.split ? P.c0 : c;
+    d.c1 = P.split ? P.c1 : c + 1;
+    d.rl = rl; d.nslots = nslots;
+#pragma unroll
+    for (int pp = 0; pp < 5; pp++) { d.lo[pp] = 0; d.len[pp] = 0; d.nst[pp] = 0; }
+    d.lo[0] = lo0; d.len[0] = len0;
+    d.lo[4] = lo4; d.len[4] = len4; d.nst[4] = nst4;
+    __threadfence_block();
+    *reinterpret_cast<volatile int *>(&d.tag) = uix;
+    uix++;
+  };
+  for (int u = P.ua; u < P.ub; u++) {
+    UnitGeo gg;
+    unit_geo<D, S, false>(a, u, gg);
+    const int W = gg.nslots;
+    int w0 = 0, w1 = W, t0 = 0, t1 = gg.ntiles;
+    if (P.split) {
+      const int k = c - P.c0, n = P.c1 - P.c0;
+      w0 = (int)((int64_t)W * k / n);
+      w1 = (int)((int64_t)W * (k + 1) / n);
+      if (k < n - 1) t1 = 0;
+    }
+    const int cap4 = STAGE / IG::sz(4);
+    const int nst4 = (t1 - t0 + cap4 - 1) / cap4;
+    publish(u, (w1 - w0) + (t1 - t0), w0, w1 - w0, gg.rl, W, W + t0, t1 - t0, nst4);
+    const uint8_t *img = a.packed + a.offs[u];
+    const int64_t *wo = a.woff + (int64_t)gg.b * (W + 1);
+    for (int w = w0; w < w1;) {
+      // the longest run [w, w + n) of records fitting one stage (offsets batch-loaded)
+      int64_t o[MAXI + 1];
+#pragma unroll
+      for (int i = 0; i <= MAXI; i++) o[i] = (w + i <= w1) ? __ldg(wo + w + i) : INT64_MAX;
+      int n = 0;
+#pragma unroll
+      for (int i = 1; i <= MAXI; i++) n += (o[i] - o[0] <= STAGE) ? 1 : 0;
+      const int slot = sg % NST;
+      mbar_wait_sleep(&empty[slot], ((uint32_t)(sg / NST) & 1u) ^ 1u, 64);
+      int *tb = tab + slot * TABN;
+      tb[0] = n;
+#pragma unroll
+      for (int i = 0; i < MAXI; i++) {
+        if (i < n) {
+          const int64_t rb = o[i + 1] - o[i];
+          tb[2 + 2 * i] = (int)(o[i] - o[0]);
+          tb[3 + 2 * i] = rb == IG::rb(0) ? 0 : rb == IG::rb(1) ? 1 : rb == IG::rb(2) ? 2 : 3;
+        }
+      }
+      const uint32_t nb = (uint32_t)(o[n] - o[0]);
+      mbar_arrive_expect_tx(&full[slot], nb);
+      bulk_g2s_evict_first(ring + (size_t)slot * STAGE, img + o[0], nb, &full[slot], pol);
+      w += n;
+      sg++;
+    }
+    const __half *kr = a.k_rest + gg.b * a.rs_b + gg.h * a.rs_h;
+    const __half *vr = a.v_rest + gg.b * a.rs_b + gg.h * a.rs_h;
+    for (int t = 0; t < nst4; t++, sg++) {
+      const int slot = sg % NST;
+      const int f0 = t0 + t * cap4, f1 = min(t1, f0 + cap4);
+      mbar_wait_sleep(&empty[slot], ((uint32_t)(sg / NST) & 1u) ^ 1u, 64);
+      uint8_t *dst = ring + (size_t)slot * STAGE;
+      if (a.flags & WQ_DECODE_EARLY_) griddep_wait();
+      const int r0 = 16 * f0, r1 = min(gg.rl, 16 * f1);
+      const uint32_t nb = (uint32_t)(r1 - r0) * 2u * D;
+      mbar_arrive_expect_tx(&full[slot], 2 * nb);
+      bulk_g2s_evict_first(dst, kr + (int64_t)r0 * D, nb, &full[slot], pol);
+      bulk_g2s_evict_first(dst + cap4 * 32 * D, vr + (int64_t)r0 * D, nb, &full[slot], pol);
+    }
+  }
+  publish(-1, 0, 0, 0, 0, 0, 0, 0, 0);
+}
 
-template <int D, int S>
+
+template <int D, int S, bool UR>
 __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   using SM = DecodeSmem<D, S>;
   constexpr int KT = D / 16;
@@ -343,7 +437,12 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
 
   if (warp == NCW) {
     // =========================== producer ===========================
-    if (lane == 0) produce<D, S, false, STAGE, NST, SM::NUS>(a, *cp, ustart, ring, full, empty, ent, units_done, ts);
+    if constexpr (UR) {
+      if (lane == 0) produce_ur<D, S, STAGE, NST, SM::NUS, SM::TABN>(a, *cp, ring, full, empty, ent, units_done,
+                                                                      reinterpret_cast<int *>(sm + SM::tab_off));
+    } else {
+      if (lane == 0) produce<D, S, false, STAGE, NST, SM::NUS>(a, *cp, ustart, ring, full, empty, ent, units_done, ts);
+    }
     return;
   }
 
@@ -401,8 +500,33 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
     }
     int nxt = warp;                                // next entry item of this warp
     int kbase = 0;                                 // entry item index of the stage's first item
+    if constexpr (UR) {
+      // windows in original order: item k of a stage at its table offset, own width
+      const int *tabs = reinterpret_cast<const int *>(sm + SM::tab_off);
+      for (int done = 0; done < E.len[0]; sg++) {
+        const int slot = sg % NST;
+        mbar_wait(&full[slot], (uint32_t)(sg / NST) & 1u);
+        const int *tb = tabs + slot * SM::TABN;
+        const int n = tb[0];
+        const uint8_t *sbase = ring + (size_t)slot * STAGE;
+        for (; nxt < kbase + n; nxt += NCW) {
+          const int k = nxt - kbase;
+          const uint8_t *rec = sbase + tb[2 + 2 * k];
+          switch (tb[3 + 2 * k]) {
+            case 0: do_window<D, S, 2>(rec, qs, a.scale_log2, st, o, scratch, lane); break;
+            case 1: do_window<D, S, 4>(rec, qs, a.scale_log2, st, o, scratch, lane); break;
+            case 2: do_window<D, S, 8>(rec, qs, a.scale_log2, st, o, scratch, lane); break;
+            default: do_window<D, S, 16>(rec, qs, a.scale_log2, st, o, scratch, lane); break;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        kbase += n;
+        done += n;
+      }
+    }
 #pragma unroll
-    for (int p = 0; p < 5; p++) {
+    for (int p = UR ? 4 : 0; p < 5; p++) {
       using IG = ItemGeo<D, S, false>;
       constexpr int SZ_[5] = {IG::sz(0), IG::sz(1), IG::sz(2), IG::sz(3), IG::sz(4)};
       const int sz = SZ_[p];
@@ -573,12 +697,12 @@ size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms) {
   return part + cnt + (size_t)num_sms * TS_PER_CTA * sizeof(uint64_t);
 }
 
-template <int D, int S>
+template <int D, int S, bool UR>
 static cudaError_t launch_decode_t(const DecodeArgs &a, int num_sms, cudaStream_t st) {
   using SM = DecodeSmem<D, S>;
   static bool attr_set = false;                  // per instantiation (per process: one device)
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_decode<D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_decode<D, S, UR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)SM::total);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -595,7 +719,7 @@ static cudaError_t launch_decode_t(const DecodeArgs &a, int num_sms, cudaStream_
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, k_decode<D, S>, a);
+  return cudaLaunchKernelEx(&cfg, k_decode<D, S, UR>, a);
 }
 
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st) {
@@ -603,9 +727,9 @@ cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st) {
   // this file's mma.sync kernel.  Parity-clean but ~4x slower on C5 (its dequantization
   // warps are issue/latency bound), so it is opt-in.
   static const bool use_tc = getenv("WQ_DECODE_TC") && atoi(getenv("WQ_DECODE_TC")) != 0;
-  if (a.d == 128 && use_tc) return launch_decode_tc(a, num_sms, st);
+  if (a.d == 128 && use_tc && !a.woff) return launch_decode_tc(a, num_sms, st);
 #define WQ_D(DD, SS) \
-  if (a.d == DD && a.S == SS) return launch_decode_t<DD, SS>(a, num_sms, st);
+  if (a.d == DD && a.S == SS) return a.woff ? launch_decode_t<DD, SS, true>(a, num_sms, st) : launch_decode_t<DD, SS, false>(a, num_sms, st);
   WQ_D(64, 16) WQ_D(64, 32) WQ_D(64, 64) WQ_D(64, 128)
   WQ_D(128, 16) WQ_D(128, 32) WQ_D(128, 64) WQ_D(128, 128)
 #undef WQ_D

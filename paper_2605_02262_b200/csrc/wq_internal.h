@@ -51,6 +51,7 @@ struct DecodeArgs {
   float *ws_part;            // [(G + B*H)][grp][d + 2]
   int32_t *ws_cnt;           // [B*H]
   uint64_t *ws_ts;           // [num_sms][8] timestamps when debug & 8, else NULL
+  const int64_t *woff;       // non-NULL: unreordered image, window offsets [B][W+1]
 };
 size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms);
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st);
@@ -61,6 +62,11 @@ cudaError_t launch_dequant_layout(const int32_t *seg_off, int B, int H, int d, i
                                   cudaStream_t st);
 cudaError_t launch_dequant_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off, int B, int H,
                                  int W, int d, int S, const int64_t *offs16, uint8_t *img16, cudaStream_t st);
+
+cudaError_t launch_unreordered_layout(const uint8_t *bits_l, int B, int W, int d, int S, int64_t *woff, cudaStream_t st);
+cudaError_t launch_unreorder_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off,
+                                   const int32_t *perm_l, int B, int H, int W, int d, int S, const int64_t *woff,
+                                   uint8_t *uimg, cudaStream_t st);
 
 int device_sm_count();
 

@@ -73,6 +73,9 @@ def load(build_if_missing: bool = True):
         "wq_shard_slots": [P, P, I32, I32, I32, I32, P, P, P],
         "wq_dequant_layout": [C.POINTER(Geom), P, P, P, P],
         "wq_dequantize_image": [P, P, P, C.POINTER(Geom), P, P, P],
+        "wq_unreordered_layout": [C.POINTER(Geom), P, P, P],
+        "wq_unreorder_image": [P, P, P, P, C.POINTER(Geom), P, P, P],
+        "wq_decode_attention_unreordered": [P, P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, P, SZ, P],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -90,6 +93,7 @@ def exported_symbols():
     return ["wq_thresholds", "wq_window_scores_workspace", "wq_window_scores", "wq_assign_bits",
             "wq_packed_bytes", "wq_layer_layout", "wq_reorder_quantize_pack", "wq_decode_workspace",
             "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_dequant_layout", "wq_dequantize_image",
+            "wq_unreordered_layout", "wq_unreorder_image", "wq_decode_attention_unreordered",
             "wq_last_error", "wq_version"]
 
 
@@ -260,3 +264,33 @@ def wq_dequantize_image(packed: torch.Tensor, offs: torch.Tensor, seg_off_l: tor
     _check(load().wq_dequantize_image(_ptr(packed), _ptr(offs), _ptr(seg_off_l), C.byref(g), _ptr(offs16),
                                       _ptr(img16), _stream(stream)))
     return img16
+
+
+def wq_unreordered_layout(g: Geom, bits_l: torch.Tensor, woff=None, stream=None) -> torch.Tensor:
+    """woff i64 [B][W+1]: original-order record offsets of the unreordered image (T8 baseline)."""
+    B, W = bits_l.shape
+    if woff is None:
+        woff = torch.empty((B, W + 1), dtype=torch.int64, device=bits_l.device)
+    _check(load().wq_unreordered_layout(C.byref(g), _ptr(bits_l), _ptr(woff), _stream(stream)))
+    return woff
+
+
+def wq_unreorder_image(packed, offs, seg_off_l, perm_l, g: Geom, woff, uimg, stream=None):
+    """Copy the packed (reordered) image's records into original window order (T8 baseline)."""
+    _check(load().wq_unreorder_image(_ptr(packed), _ptr(offs), _ptr(seg_off_l), _ptr(perm_l), C.byref(g),
+                                     _ptr(woff), _ptr(uimg), _stream(stream)))
+    return uimg
+
+
+def wq_decode_attention_unreordered(q, uimg, offs, seg_off_l, woff, g: Geom, k_rest, v_rest, rest_len,
+                                    sm_scale: float, out=None, partial=None, workspace=None, stream=None):
+    """Decode over the unreordered image (windows in original order, per-window width)."""
+    if workspace is None:
+        workspace = torch.zeros(wq_decode_workspace(g), dtype=torch.uint8, device=q.device)
+    R_max = 0 if k_rest is None else k_rest.shape[2]
+    rs = (C.c_int64 * 2)(*(k_rest.stride(0), k_rest.stride(1))) if k_rest is not None else None
+    _check(load().wq_decode_attention_unreordered(_ptr(q), _ptr(uimg), _ptr(offs), _ptr(seg_off_l), _ptr(woff),
+                                                  C.byref(g), _ptr(k_rest), _ptr(v_rest), rs, _ptr(rest_len), R_max,
+                                                  float(sm_scale), _ptr(out), _ptr(partial), _ptr(workspace),
+                                                  workspace.numel(), _stream(stream)))
+    return out, partial

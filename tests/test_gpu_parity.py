@@ -379,3 +379,45 @@ def test_unfused_baseline_parity(orc, d, S, W, tail, B, H, Hq):
     ref = orc.decode_attention(c["q"].cpu().numpy(), rimg, roffs16, rseg16, perm[0].cpu().numpy(), ogeom(orc, g),
                                c["kr"].cpu().numpy(), c["vr"].cpu().numpy(), c["rest_len"].cpu().numpy(), sm)
     assert rel_err(out.float().cpu().numpy(), ref) <= ATTN_TOL
+
+
+@pytest.mark.parametrize("d,S,W,tail,B,H,Hq", [(128, 32, 40, 7, 2, 4, 28), (64, 16, 30, 5, 2, 2, 14),
+                                               (128, 128, 5, 9, 2, 2, 8), (128, 16, 90, 0, 1, 4, 28)])
+def test_unreordered_baseline_parity(orc, d, S, W, tail, B, H, Hq):
+    """T8 "Module III off" path: the unreordered image holds the packed records in original
+    window order at the prefix offsets, and its decode (windows in original order, per-window
+    width) matches the oracle's attention over the same codes (Eq.12-13: order-invariant)."""
+    c = small_case(400 + d + S + W, d=d, S=S, W=W, tail=tail, B=B, H=H, Hq=Hq)
+    g = c["g"]
+    sc = wq.wq_window_scores(c["vis"], c["txt"], S)
+    thr = orc.thresholds([0.45], 2.0, 4)
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
+    sm = 1 / math.sqrt(d)
+    offs, packed, _, _ = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm[0], seg[0], c["q"], sm)
+    woff = wq.wq_unreordered_layout(g, bits[0].contiguous())
+    uimg = torch.zeros_like(packed)
+    wq.wq_unreorder_image(packed, offs, seg[0], perm[0], g, woff, uimg)
+    out = torch.empty((g.B, g.Hq, g.d), dtype=torch.float16, device="cuda")
+    part = torch.empty((g.B, g.Hq, g.d + 2), dtype=torch.float32, device="cuda")
+    wq.wq_decode_attention_unreordered(c["q"], uimg, offs, seg[0], woff, g, c["kr"], c["vr"], c["rest_len"], sm,
+                                       out=out, partial=part)
+    torch.cuda.synchronize()
+    bl, pm, sg, of = bits[0].cpu().numpy(), perm[0].cpu().numpy(), seg[0].cpu().numpy(), offs.cpu().numpy()
+    wo, ui, pk = woff.cpu().numpy(), uimg.cpu().numpy(), packed.cpu().numpy()
+    rb = {b_: orc.record_bytes(b_, d, S) for b_ in (2, 4, 8, 16)}
+    for b in range(g.B):
+        assert np.array_equal(wo[b], np.concatenate([[0], np.cumsum([rb[int(x)] for x in bl[b]])]))
+        for h in range(g.H):
+            u = b * g.H + h
+            so = 0
+            for slot in range(sg[b, 4]):
+                k = int(np.searchsorted(sg[b, 1:], slot, side="right"))
+                n = rb[(2, 4, 8, 16)[k]]
+                w = pm[b, slot]
+                assert bl[b, w] == (2, 4, 8, 16)[k]
+                assert np.array_equal(ui[of[u] + wo[b, w]:of[u] + wo[b, w] + n], pk[of[u] + so:of[u] + so + n])
+                so += n
+    ref = _decode_ref(orc, c, g, offs, packed, perm[0], seg[0], sm)[0]
+    assert rel_err(out.float().cpu().numpy(), ref) <= ATTN_TOL
+    p = part.double().cpu().numpy()
+    assert rel_err(p[..., 2:] / p[..., 1:2], ref) <= ATTN_TOL
