@@ -349,6 +349,7 @@ def run_wq(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_ablation:
         result["ablation_unfused_t9"] = run_ablation_unfused(w, stream)
         result["ablation_unreordered_t8"] = run_ablation_unreordered(w, stream)
+        result["ablation_similarity_t11"] = run_ablation_similarity(w, stream)
     if rank == 0 and not args.no_e2e:
         result["e2e"] = run_e2e(w, args, stream)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -452,6 +453,27 @@ def run_ablation_unreordered(w, stream, n_layers=4, reps=5):
     return {"reordered_decode_us": round(t_r, 2), "unreordered_decode_us": round(t_u, 2),
             "unreordered_over_reordered": round(t_u / t_r, 3),
             "paper": "T8 (P:1006-1008, A800, whole model): 1250 tokens/s with reordering vs 500 without (2.5x)"}
+
+
+def run_ablation_similarity(w, stream, reps=5):
+    """The paper's similarity-function comparison (T11): window scoring
+    (wq_window_scores) with cosine (Eq.8) vs Pearson correlation on the bench workload."""
+    import torch
+    wq = w.wq
+    out = {}
+    for name, metric in (("cosine_us", wq.WQ_SIM_COSINE), ("pearson_us", wq.WQ_SIM_PEARSON)):
+        wq.wq_window_scores(w.vis, w.txt, w.cfg.S, scores=w.scores, workspace=w.sws, metric=metric)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            wq.wq_window_scores(w.vis, w.txt, w.cfg.S, scores=w.scores, workspace=w.sws, metric=metric)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out[name] = round(e0.elapsed_time(e1) * 1e3 / reps, 1)
+    out["visual_MB"] = round(w.vis.numel() * 2 / 1e6, 1)
+    out["paper"] = ("T11 (P:1059-1061, batch 1, 100 frames): cosine 48 ms, Pearson 55 ms, Euclidean 49 ms; "
+                    "cosine kept (Euclidean not provided here, include/wq.h)")
+    return out
 
 
 def imgs_bytes(w, l):

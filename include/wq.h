@@ -140,6 +140,21 @@ wq_status wq_window_scores(const void *vis, int64_t vis_row_stride, int64_t vis_
                            double *scores, void *workspace, size_t workspace_bytes,
                            void *stream);
 
+/* Similarity-function variants of the scorer (T11: the paper compares
+ * cosine, Pearson correlation and Euclidean distance and keeps cosine).
+ *   WQ_SIM_COSINE  Eq.8 as above.
+ *   WQ_SIM_PEARSON scores[b][w] = 1/(S*N) sum_j sum_k pearson(t_j, v_k), pearson(x, y) =
+ *                  cos(x - mean(x), y - mean(y)) (means over the D channels); the pooled
+ *                  identity holds for the centred normalized rows; a constant row
+ *                  (zero variance) contributes 0.
+ * (Euclidean distance is not a similarity in [0, 1] the thresholds of Eq.10-11 could
+ * band, and the paper does not say how it maps one; not provided.) */
+enum { WQ_SIM_COSINE = 0, WQ_SIM_PEARSON = 1 };
+wq_status wq_window_scores_ex(const void *vis, int64_t vis_row_stride, int64_t vis_batch_stride,
+                              const void *txt, int64_t txt_row_stride, int64_t txt_batch_stride,
+                              int32_t B, int32_t M, int32_t N, int32_t D, int32_t S, int32_t metric,
+                              double *scores, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Bit assignment + permutation (Alg.1 lines 8-16, P:313, P:316-322, P:395;
  * Alg.2 lines 2-13).  For each layer l and request b:
  *   1. rank[b][w]: position of window w in (-score, w) order (0 = most similar, Q7)

@@ -70,6 +70,7 @@ def lib():
                 "wqo_thresholds": (C.c_int, [P, I32, F64, I32, P]),
                 "wqo_window_score": (F64, [P, I64, P, I64, I32, I32, I32, I32]),
                 "wqo_window_scores": (None, [P, I64, I64, P, I64, I64, I32, I32, I32, I32, I32, P]),
+                "wqo_window_scores_pearson": (None, [P, I64, I64, P, I64, I64, I32, I32, I32, I32, I32, P]),
                 "wqo_assign_bits": (C.c_int, [P, P, I32, C.POINTER(Geom), F64, I32, I32, P, P, P, P]),
                 "wqo_record_bytes": (I64, [I32, I32, I32]),
                 "wqo_packed_bytes": (I64, [C.POINTER(Geom), P, I32]),
@@ -147,6 +148,16 @@ def window_scores(vis: np.ndarray, txt: np.ndarray, S: int) -> np.ndarray:
     N = txt.shape[1]
     out = np.zeros((B, M // S), np.float64)
     lib().wqo_window_scores(_p(vis), D, M * D, _p(txt), D, N * D, B, M, N, D, S, _p(out))
+    return out
+
+
+def window_scores_pearson(vis: np.ndarray, txt: np.ndarray, S: int) -> np.ndarray:
+    """T11 variant: Eq.8 with the Pearson correlation of every (text, window) token pair."""
+    vis, txt = _u16(vis), _u16(txt)
+    B, M, D = vis.shape
+    N = txt.shape[1]
+    out = np.zeros((B, M // S), np.float64)
+    lib().wqo_window_scores_pearson(_p(vis), D, M * D, _p(txt), D, N * D, B, M, N, D, S, _p(out))
     return out
 
 

@@ -691,3 +691,34 @@ void wqo_dequantize_image(const uint8_t *packed, const int64_t *offs, const int3
     }
   }
 }
+
+/* T11 similarity variant: Pearson correlation instead of cosine in Eq.8,
+ * the mean over the S*N pairs of corr(t_j, v_k); a zero-variance row contributes 0.
+ * Literal double sum, every pair's correlation from its own means and variances. */
+static double pearson(const uint16_t *x, const uint16_t *y, int32_t D) {
+  double mx = 0.0, my = 0.0;
+  for (int c = 0; c < D; c++) { mx += wqo_f16_to_f64(x[c]); my += wqo_f16_to_f64(y[c]); }
+  mx /= D; my /= D;
+  double sxy = 0.0, sxx = 0.0, syy = 0.0;
+  for (int c = 0; c < D; c++) {
+    double a = wqo_f16_to_f64(x[c]) - mx, b = wqo_f16_to_f64(y[c]) - my;
+    sxy += a * b; sxx += a * a; syy += b * b;
+  }
+  if (sxx == 0.0 || syy == 0.0) return 0.0;
+  return sxy / (sqrt(sxx) * sqrt(syy));
+}
+
+void wqo_window_scores_pearson(const uint16_t *vis, int64_t vrs, int64_t vbs,
+                               const uint16_t *txt, int64_t trs, int64_t tbs,
+                               int32_t B, int32_t M, int32_t N, int32_t D, int32_t S, double *scores) {
+  int W = M / S;
+#pragma omp parallel for collapse(2) schedule(dynamic)
+  for (int b = 0; b < B; b++)
+    for (int w = 0; w < W; w++) {
+      double sum = 0.0;
+      for (int j = 0; j < N; j++)
+        for (int k = 0; k < S; k++)
+          sum += pearson(txt + b * tbs + (int64_t)j * trs, vis + b * vbs + (int64_t)(w * S + k) * vrs, D);
+      scores[(int64_t)b * W + w] = sum / ((double)S * (double)N);
+    }
+}

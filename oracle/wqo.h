@@ -51,6 +51,12 @@ void   wqo_window_scores(const uint16_t *vis, int64_t vrs, int64_t vbs,
                          int32_t B, int32_t M, int32_t N, int32_t D, int32_t S,
                          double *scores);
 
+/* T11 variant: Eq.8 with Pearson correlation per pair */
+void   wqo_window_scores_pearson(const uint16_t *vis, int64_t vrs, int64_t vbs,
+                                 const uint16_t *txt, int64_t trs, int64_t tbs,
+                                 int32_t B, int32_t M, int32_t N, int32_t D, int32_t S,
+                                 double *scores);
+
 /* Alg.1 band/pin/vote + budget + Alg.2 partition.  Returns 0, or 3 if the
  * budget is infeasible. */
 int wqo_assign_bits(const double *scores, const double *thr, int32_t L,

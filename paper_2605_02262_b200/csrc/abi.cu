@@ -95,10 +95,12 @@ wq_status wq_window_scores_workspace(int32_t B, int32_t D, size_t *bytes_host) {
   return WQ_OK;
 }
 
-wq_status wq_window_scores(const void *vis, int64_t vrs, int64_t vbs, const void *txt, int64_t trs,
-                           int64_t tbs, int32_t B, int32_t M, int32_t N, int32_t D, int32_t S,
-                           double *scores, void *workspace, size_t workspace_bytes, void *stream) {
+wq_status wq_window_scores_ex(const void *vis, int64_t vrs, int64_t vbs, const void *txt, int64_t trs,
+                              int64_t tbs, int32_t B, int32_t M, int32_t N, int32_t D, int32_t S,
+                              int32_t metric, double *scores, void *workspace, size_t workspace_bytes,
+                              void *stream) {
   if (!vis || !txt || !scores || !workspace) return fail(WQ_EINVAL, "NULL pointer");
+  if (metric != WQ_SIM_COSINE && metric != WQ_SIM_PEARSON) return fail(WQ_EINVAL, "metric=%d", metric);
   if (!(S == 16 || S == 32 || S == 64 || S == 128)) return fail(WQ_ESHAPE, "S=%d not in {16,32,64,128}", S);
   if (B < 1 || N < 1 || M < S) return fail(WQ_ESHAPE, "B=%d N=%d M=%d (need M >= S=%d)", B, N, M, S);
   if (D % 8 || D < 8 || D > 4096) return fail(WQ_ESHAPE, "D=%d must be a multiple of 8 in [8, 4096]", D);
@@ -106,12 +108,19 @@ wq_status wq_window_scores(const void *vis, int64_t vrs, int64_t vbs, const void
     return fail(WQ_EINVAL, "rows must be 16-byte aligned (strides multiple of 8 elements)");
   if (workspace_bytes < (size_t)B * D * sizeof(double)) return fail(WQ_EINVAL, "workspace too small");
   double *tbar = reinterpret_cast<double *>(workspace);
-  wq_status s = cuda_status(wq::launch_text_pool((const __half *)txt, trs, tbs, B, N, D, tbar, S_(stream)),
+  wq_status s = cuda_status(wq::launch_text_pool((const __half *)txt, trs, tbs, B, N, D, tbar, metric, S_(stream)),
                             "text pool");
   if (s != WQ_OK) return s;
   return cuda_status(
-      wq::launch_window_scores((const __half *)vis, vrs, vbs, B, M, N, D, S, tbar, scores, S_(stream)),
+      wq::launch_window_scores((const __half *)vis, vrs, vbs, B, M, N, D, S, tbar, scores, metric, S_(stream)),
       "window scores");
+}
+
+wq_status wq_window_scores(const void *vis, int64_t vrs, int64_t vbs, const void *txt, int64_t trs,
+                           int64_t tbs, int32_t B, int32_t M, int32_t N, int32_t D, int32_t S,
+                           double *scores, void *workspace, size_t workspace_bytes, void *stream) {
+  return wq_window_scores_ex(vis, vrs, vbs, txt, trs, tbs, B, M, N, D, S, WQ_SIM_COSINE, scores, workspace,
+                             workspace_bytes, stream);
 }
 
 wq_status wq_assign_bits(const double *scores, const double *thr_host, int32_t L, const wq_geom *g,

@@ -41,6 +41,7 @@ WQ_DEV void load8(const __half *p, double (&x)[8]) {
   }
 }
 
+template <bool CENTER>
 __global__ void __launch_bounds__(ST) k_text_pool(const __half *__restrict__ txt, int64_t trs,
                                                   int64_t tbs, int N, int D, double *__restrict__ tbar) {
   extern __shared__ double pooled[];  // [D]
@@ -49,12 +50,24 @@ __global__ void __launch_bounds__(ST) k_text_pool(const __half *__restrict__ txt
   for (int c = threadIdx.x; c < D; c += ST) pooled[c] = 0.0;
   for (int j = 0; j < N; j++) {
     const __half *row = txt + b * tbs + (int64_t)j * trs;
+    double mu = 0.0;
+    if (CENTER) {                                  // Pearson: centre the row first (T11)
+      double sm[1] = {0.0};
+      for (int k = threadIdx.x; k < nchunk; k += ST) {
+        double x[8];
+        load8(row + 8 * k, x);
+#pragma unroll
+        for (int i = 0; i < 8; i++) sm[0] += x[i];
+      }
+      block_sum<1>(sm, red);
+      mu = sm[0] / (double)D;
+    }
     double ss[1] = {0.0};
     for (int k = threadIdx.x; k < nchunk; k += ST) {
       double x[8];
       load8(row + 8 * k, x);
 #pragma unroll
-      for (int i = 0; i < 8; i++) ss[0] = fma(x[i], x[i], ss[0]);
+      for (int i = 0; i < 8; i++) ss[0] = fma(x[i] - mu, x[i] - mu, ss[0]);
     }
     block_sum<1>(ss, red);
     double inv = ss[0] > 0.0 ? 1.0 / sqrt(ss[0]) : 0.0;
@@ -62,14 +75,14 @@ __global__ void __launch_bounds__(ST) k_text_pool(const __half *__restrict__ txt
       double x[8];
       load8(row + 8 * k, x);
 #pragma unroll
-      for (int i = 0; i < 8; i++) pooled[8 * k + i] = fma(x[i], inv, pooled[8 * k + i]);
+      for (int i = 0; i < 8; i++) pooled[8 * k + i] = fma(x[i] - mu, inv, pooled[8 * k + i]);
     }
   }
   __syncthreads();
   for (int c = threadIdx.x; c < D; c += ST) tbar[(int64_t)b * D + c] = pooled[c];
 }
 
-template <int NC>  // 16-byte chunks per thread per row: ceil(D / 8 / ST)
+template <int NC, bool CENTER>  // 16-byte chunks per thread per row: ceil(D / 8 / ST); CENTER: Pearson
 __global__ void __launch_bounds__(ST) k_window_scores(const __half *__restrict__ vis, int64_t vrs,
                                                       int64_t vbs, int M, int N, int D, int S,
                                                       const double *__restrict__ tbar,
@@ -94,6 +107,27 @@ __global__ void __launch_bounds__(ST) k_window_scores(const __half *__restrict__
         raw[r][i] = k < nchunk ? __ldcs(reinterpret_cast<const uint4 *>(base + (int64_t)(r0 + r) * vrs) + k)
                                : make_uint4(0, 0, 0, 0);
       }
+    double mu[RB];
+#pragma unroll
+    for (int r = 0; r < RB; r++) mu[r] = 0.0;
+    if constexpr (CENTER) {                        // Pearson: row means first (T11)
+#pragma unroll
+      for (int r = 0; r < RB; r++) {
+#pragma unroll
+        for (int i = 0; i < NC; i++) {
+          const __half2 *h = reinterpret_cast<const __half2 *>(&raw[r][i]);
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            float2 f = __half22float2(h[e]);
+            mu[r] += (double)f.x;
+            mu[r] += (double)f.y;
+          }
+        }
+      }
+      block_sum<RB>(mu, red);
+#pragma unroll
+      for (int r = 0; r < RB; r++) mu[r] /= (double)D;
+    }
     double ss[RB];
 #pragma unroll
     for (int r = 0; r < RB; r++) {
@@ -101,11 +135,13 @@ __global__ void __launch_bounds__(ST) k_window_scores(const __half *__restrict__
 #pragma unroll
       for (int i = 0; i < NC; i++) {
         const __half2 *h = reinterpret_cast<const __half2 *>(&raw[r][i]);
+        const bool in = tid + ST * i < nchunk;     // padding chunks are zeros, not (0 - mu)
 #pragma unroll
         for (int e = 0; e < 4; e++) {
           float2 f = __half22float2(h[e]);
-          ss[r] = fma((double)f.x, (double)f.x, ss[r]);
-          ss[r] = fma((double)f.y, (double)f.y, ss[r]);
+          const double x0 = in ? (double)f.x - mu[r] : 0.0, x1 = in ? (double)f.y - mu[r] : 0.0;
+          ss[r] = fma(x0, x0, ss[r]);
+          ss[r] = fma(x1, x1, ss[r]);
         }
       }
     }
@@ -119,8 +155,8 @@ __global__ void __launch_bounds__(ST) k_window_scores(const __half *__restrict__
 #pragma unroll
         for (int e = 0; e < 4; e++) {
           float2 f = __half22float2(h[e]);
-          pool[i][2 * e] = fma((double)f.x, inv, pool[i][2 * e]);
-          pool[i][2 * e + 1] = fma((double)f.y, inv, pool[i][2 * e + 1]);
+          pool[i][2 * e] = fma((double)f.x - mu[r], inv, pool[i][2 * e]);
+          pool[i][2 * e + 1] = fma((double)f.y - mu[r], inv, pool[i][2 * e + 1]);
         }
       }
     }
@@ -139,26 +175,30 @@ __global__ void __launch_bounds__(ST) k_window_scores(const __half *__restrict__
 }
 
 cudaError_t launch_text_pool(const __half *txt, int64_t trs, int64_t tbs, int B, int N, int D,
-                             double *tbar, cudaStream_t st) {
+                             double *tbar, int metric, cudaStream_t st) {
   size_t smem = (size_t)D * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_text_pool, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = metric == 1 ? k_text_pool<true> : k_text_pool<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_text_pool<<<B, ST, smem, st>>>(txt, trs, tbs, N, D, tbar);
+  kern<<<B, ST, smem, st>>>(txt, trs, tbs, N, D, tbar);
   return cudaGetLastError();
 }
 
 cudaError_t launch_window_scores(const __half *vis, int64_t vrs, int64_t vbs, int B, int M, int N,
-                                 int D, int S, const double *tbar, double *scores, cudaStream_t st) {
+                                 int D, int S, const double *tbar, double *scores, int metric, cudaStream_t st) {
   int W = M / S;
   int nc = (D / 8 + ST - 1) / ST;
   dim3 grid(W, B);
+#define WQ_WS(NCV)                                                                                   \
+  case NCV:                                                                                          \
+    if (metric == 1) k_window_scores<NCV, true><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores); \
+    else k_window_scores<NCV, false><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores);          \
+    break;
   switch (nc) {
-    case 1: k_window_scores<1><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores); break;
-    case 2: k_window_scores<2><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores); break;
-    case 3: k_window_scores<3><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores); break;
-    case 4: k_window_scores<4><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores); break;
+    WQ_WS(1) WQ_WS(2) WQ_WS(3) WQ_WS(4)
     default: return cudaErrorInvalidValue;
   }
+#undef WQ_WS
   return cudaGetLastError();
 }
 

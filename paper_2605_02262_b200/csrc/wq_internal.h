@@ -16,9 +16,9 @@ struct AssignParams {
 };
 
 cudaError_t launch_text_pool(const __half *txt, int64_t trs, int64_t tbs, int B, int N, int D,
-                             double *tbar, cudaStream_t st);
+                             double *tbar, int metric, cudaStream_t st);
 cudaError_t launch_window_scores(const __half *vis, int64_t vrs, int64_t vbs, int B, int M, int N,
-                                 int D, int S, const double *tbar, double *scores, cudaStream_t st);
+                                 int D, int S, const double *tbar, double *scores, int metric, cudaStream_t st);
 
 cudaError_t launch_rank(const double *scores, int B, int W, int32_t *rank, cudaStream_t st);
 cudaError_t launch_assign(const double *scores, const AssignParams &p, uint8_t *bits, int32_t *perm,

@@ -62,6 +62,7 @@ def load(build_if_missing: bool = True):
         "wq_thresholds": [P, I32, F64, I32, P],
         "wq_window_scores_workspace": [I32, I32, P],
         "wq_window_scores": [P, I64, I64, P, I64, I64, I32, I32, I32, I32, I32, P, P, SZ, P],
+        "wq_window_scores_ex": [P, I64, I64, P, I64, I64, I32, I32, I32, I32, I32, I32, P, P, SZ, P],
         "wq_assign_bits": [P, P, I32, C.POINTER(Geom), C.POINTER(AssignOpts), P, P, P, P, P],
         "wq_packed_bytes": [C.POINTER(Geom), P, I32, P],
         "wq_layer_layout": [C.POINTER(Geom), P, P, P],
@@ -90,7 +91,7 @@ def load(build_if_missing: bool = True):
 
 
 def exported_symbols():
-    return ["wq_thresholds", "wq_window_scores_workspace", "wq_window_scores", "wq_assign_bits",
+    return ["wq_thresholds", "wq_window_scores_workspace", "wq_window_scores", "wq_window_scores_ex", "wq_assign_bits",
             "wq_packed_bytes", "wq_layer_layout", "wq_reorder_quantize_pack", "wq_decode_workspace",
             "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_dequant_layout", "wq_dequantize_image",
             "wq_unreordered_layout", "wq_unreorder_image", "wq_decode_attention_unreordered",
@@ -140,17 +141,27 @@ def wq_window_scores_workspace(B: int, D: int) -> int:
     return n.value
 
 
-def wq_window_scores(vis: torch.Tensor, txt: torch.Tensor, S: int, scores=None, workspace=None, stream=None):
-    """vis fp16 [B][M][D] (rows contiguous), txt fp16 [B][N][D] -> scores fp64 [B][M//S]."""
+WQ_SIM_COSINE, WQ_SIM_PEARSON = 0, 1
+
+
+def wq_window_scores(vis: torch.Tensor, txt: torch.Tensor, S: int, scores=None, workspace=None, stream=None,
+                     metric: int = WQ_SIM_COSINE):
+    """vis fp16 [B][M][D] (rows contiguous), txt fp16 [B][N][D] -> scores fp64 [B][M//S].
+    metric: WQ_SIM_COSINE (Eq.8) or WQ_SIM_PEARSON (T11 variant) -> wq_window_scores_ex."""
     B, M, D = vis.shape
     N = txt.shape[1]
     if scores is None:
         scores = torch.empty((B, M // S), dtype=torch.float64, device=vis.device)
     if workspace is None:
         workspace = torch.empty(wq_window_scores_workspace(B, D), dtype=torch.uint8, device=vis.device)
-    _check(load().wq_window_scores(_ptr(vis), vis.stride(1), vis.stride(0), _ptr(txt), txt.stride(1),
-                                   txt.stride(0), B, M, N, D, S, _ptr(scores), _ptr(workspace),
-                                   workspace.numel(), _stream(stream)))
+    if metric == WQ_SIM_COSINE:
+        _check(load().wq_window_scores(_ptr(vis), vis.stride(1), vis.stride(0), _ptr(txt), txt.stride(1),
+                                       txt.stride(0), B, M, N, D, S, _ptr(scores), _ptr(workspace),
+                                       workspace.numel(), _stream(stream)))
+    else:
+        _check(load().wq_window_scores_ex(_ptr(vis), vis.stride(1), vis.stride(0), _ptr(txt), txt.stride(1),
+                                          txt.stride(0), B, M, N, D, S, int(metric), _ptr(scores),
+                                          _ptr(workspace), workspace.numel(), _stream(stream)))
     return scores
 
 

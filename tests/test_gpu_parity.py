@@ -421,3 +421,17 @@ def test_unreordered_baseline_parity(orc, d, S, W, tail, B, H, Hq):
     assert rel_err(out.float().cpu().numpy(), ref) <= ATTN_TOL
     p = part.double().cpu().numpy()
     assert rel_err(p[..., 2:] / p[..., 1:2], ref) <= ATTN_TOL
+
+
+def test_pearson_scores_parity(orc):
+    """T11 similarity variant: GPU Pearson window scores vs the literal oracle (1e-12 abs)."""
+    rng = np.random.default_rng(5)
+    B, M, N, D, S = 2, 6 * 32 + 7, 9, 136, 32
+    vis = torch.from_numpy(rng.standard_normal((B, M, D)).astype(np.float16) + 0.3).cuda()
+    txt = torch.from_numpy(rng.standard_normal((B, N, D)).astype(np.float16) - 0.2).cuda()
+    vis[0, 5] = 0.75                                   # constant row: contributes 0
+    got = wq.wq_window_scores(vis, txt, S, metric=wq.WQ_SIM_PEARSON).cpu().numpy()
+    ref = orc.window_scores_pearson(vis.cpu().numpy(), txt.cpu().numpy(), S)
+    assert np.max(np.abs(got - ref)) < 1e-12
+    cos = wq.wq_window_scores(vis, txt, S).cpu().numpy()
+    assert np.max(np.abs(cos - orc.window_scores(vis.cpu().numpy(), txt.cpu().numpy(), S))) < 1e-12

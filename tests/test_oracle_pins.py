@@ -651,3 +651,37 @@ def test_dequantize_image_decode_close_to_fused(orc):
     b = orc.decode_attention(c["q"], img16, offs16, seg16, c["perm"], g, c["kr"], c["vr"], c["rest_len"], sm)
     assert np.max(np.abs(a - b)) / np.max(np.abs(a)) < 5e-3
     assert not np.array_equal(a, b)
+
+
+# --------------------------------------------------------------------------------------
+# T11 similarity variant: Pearson correlation in Eq.8
+# --------------------------------------------------------------------------------------
+def test_pearson_scores_vs_numpy_and_invariants(orc):
+    rng = np.random.default_rng(21)
+    S, N, D = 16, 5, 24
+    vis = rng.standard_normal((1, 3 * S, D)).astype(np.float16)
+    txt = rng.standard_normal((1, N, D)).astype(np.float16)
+    got = orc.window_scores_pearson(vis, txt, S)
+    v64, t64 = vis[0].astype(np.float64), txt[0].astype(np.float64)
+    for w in range(3):
+        c = np.corrcoef(np.concatenate([t64, v64[w * S:(w + 1) * S]]))[:N, N:]
+        assert abs(got[0, w] - c.mean()) < 1e-12
+    # invariant under affine maps x -> a x + b (a > 0) of any row; equals cosine for centred rows
+    vis2 = vis.copy()
+    vis2[0, 3] = (vis[0, 3].astype(np.float32) * 0.5 + 0.25).astype(np.float16)
+    exact = np.allclose(vis2[0, 3].astype(np.float64), vis[0, 3].astype(np.float64) * 0.5 + 0.25, rtol=0, atol=0)
+    if exact:
+        assert abs(orc.window_scores_pearson(vis2, txt, S)[0, 0] - got[0, 0]) < 1e-12
+    vc = (v64 - v64.mean(1, keepdims=True)).astype(np.float16)[None]
+    tc = (t64 - t64.mean(1, keepdims=True)).astype(np.float16)[None]
+    vc64, tc64 = vc[0].astype(np.float64), tc[0].astype(np.float64)
+    if np.allclose(vc64.mean(1), 0, atol=0) and np.allclose(tc64.mean(1), 0, atol=0):
+        assert np.allclose(orc.window_scores_pearson(vc, tc, S), orc.window_scores(vc, tc, S), atol=1e-12)
+    # perfectly correlated / anti-correlated / constant rows
+    base = rng.standard_normal(D).astype(np.float16)
+    v = np.tile(base, (S, 1))[None]
+    t = np.stack([base, (-base.astype(np.float32)).astype(np.float16)])[None]
+    assert abs(orc.window_scores_pearson(v, t[:, :1], S)[0, 0] - 1.0) < 1e-12
+    assert abs(orc.window_scores_pearson(v, t[:, 1:], S)[0, 0] + 1.0) < 1e-12
+    const = np.full((1, S, D), 0.5, np.float16)
+    assert orc.window_scores_pearson(const, t[:, :1], S)[0, 0] == 0.0
