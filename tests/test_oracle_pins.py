@@ -685,3 +685,22 @@ def test_pearson_scores_vs_numpy_and_invariants(orc):
     assert abs(orc.window_scores_pearson(v, t[:, 1:], S)[0, 0] + 1.0) < 1e-12
     const = np.full((1, S, D), 0.5, np.float16)
     assert orc.window_scores_pearson(const, t[:, :1], S)[0, 0] == 0.0
+
+
+def test_alpha_sweep_trend(orc):
+    """Fig. thre_para: for fixed scores, raising alpha lowers T_low = f1(s) and
+    raises T_high = f2(s) (Eq.10-11), so INT2 and FP16 windows never grow and INT4 never
+    shrinks (3 widths {2,4,16}, no budget, no pin)."""
+    rng = np.random.default_rng(11)
+    W = 400
+    g = orc.geom(1, 1, 1, 64, W * 16, 16, (2, 4, 16))
+    sc = rng.uniform(0, 1, (1, W))
+    prev = None
+    for a in (0.25, 0.5, 1.0, 2.0, 4.0, 8.0, 16.0):
+        thr = orc.thresholds([0.5], a, 3)
+        bits, _, _, _ = orc.assign_bits(sc, thr, g, pin=0)
+        n = [int((bits == b).sum()) for b in (2, 4, 16)]
+        if prev is not None:
+            assert n[0] <= prev[0] and n[2] <= prev[2] and n[1] >= prev[1]
+        prev = n
+    assert prev[1] > prev[0] and prev[1] > prev[2]
