@@ -114,7 +114,7 @@ class Workload:
     scratch buffers of the path.  Under a sequence split each rank quantizes and
     decodes its share of every width segment (wq_shard_slots)."""
 
-    def __init__(self, cfg, device, rank=0, world=1, n_gen=None):
+    def __init__(self, cfg, device, rank=0, world=1, n_gen=None, merge="peer"):
         import torch
         from paper_2605_02262_b200 import synth, wq
         self.torch, self.wq = torch, wq
@@ -156,6 +156,15 @@ class Workload:
         self.part = torch.empty((B, m.Hq, m.d + 2), dtype=torch.float32, device=device) if world > 1 else None
         self.gathered = (torch.empty((world, B, m.Hq, m.d + 2), dtype=torch.float32, device=device)
                          if world > 1 else None)
+        # cross-GPU merge of the sequence split: fused peer-memory exchange (default) or
+        # partial -> NCCL all-gather -> wq_merge_partials (merge="nccl", the baseline)
+        self.peer, self.merge_note = None, None
+        if world > 1 and merge == "peer":
+            try:
+                from paper_2605_02262_b200.parallel import PeerMerge
+                self.peer = PeerMerge(self.g, device=device)
+            except Exception as e:                           # no IPC / peer access: NCCL path
+                self.merge_note = f"peer setup failed ({type(e).__name__}: {e}); NCCL all-gather used"
         # size the packed images once (setup, untimed): they depend only on the inputs
         self.packed = None
         self._setup_pass()
@@ -204,6 +213,13 @@ class Workload:
                     wq.wq_decode_attention(self.q[t, l], self.packed[l], self.offs[l], self.seg_r[l], self.g,
                                            self.kr[l], self.vr[l], rl, self.sm_scale, out=self.out[t, l],
                                            workspace=self.dws, flags=flags)
+                elif self.peer is not None:
+                    # fused path: the decode kernel exchanges the (m, l, o) partials over
+                    # NVLink peer memory and merges them (no NCCL call, no merge kernel)
+                    wq.wq_decode_attention_peer(self.q[t, l], self.packed[l], self.offs[l], self.seg_r[l], self.g,
+                                                self.kr[l], self.vr[l], rl, self.sm_scale, self.out[t, l],
+                                                self.peer.ptrs, self.peer.local, self.world, self.rank,
+                                                self.peer.next_epoch(), workspace=self.dws)
                 else:
                     wq.wq_decode_attention(self.q[t, l], self.packed[l], self.offs[l], self.seg_r[l], self.g,
                                            self.kr[l], self.vr[l], rl, self.sm_scale, partial=self.part,
@@ -212,7 +228,7 @@ class Workload:
                     wq.wq_merge_partials(self.gathered, self.g, out=self.out[t, l])
 
     def launches_per_step(self):
-        per_dec = 1 if self.world == 1 else 2
+        per_dec = 1 if (self.world == 1 or self.peer is not None) else 2
         shard = self.L if self.world > 1 else 0
         return 2 + 2 + shard + 2 * self.L + self.n_gen * self.L * per_dec
 
@@ -242,7 +258,7 @@ def run_wq(args, rank, world, local_rank):
     cfg = configs.CONFIGS[args.config]
     if args.layers:
         cfg = cfg.with_(layers=args.layers)
-    w = Workload(cfg, dev, rank, world, n_gen=args.n_gen)
+    w = Workload(cfg, dev, rank, world, n_gen=args.n_gen, merge=args.merge)
     group = dist.group.WORLD if world > 1 else None
     stream = torch.cuda.current_stream()
 
@@ -295,10 +311,15 @@ def run_wq(args, rank, world, local_rank):
         dist.barrier()
     total_ms = ev_all[0].elapsed_time(ev_all[1])
     dec_ms = sum(e[0].elapsed_time(e[1]) for e in ev_dec)
-    # isolated quantize timing (one pass over the L layers), for the quantize GB/s figure
+    # isolated wq_reorder_quantize_pack timing for the quantize GB/s figure: the L layers'
+    # layouts first (untimed, they are separate wq_layer_layout calls), then one timed
+    # pass of the L quantize launches back to back
+    for l in range(w.L):
+        w.wq.wq_layer_layout(w.g, w.seg_r[l], w.offs[l])
     qe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     qe[0].record(stream)
-    w.quantize()
+    for l in range(w.L):
+        w.wq.wq_reorder_quantize_pack(w.K[l], w.V[l], 0, w.g, w.perm_r[l], w.seg_r[l], w.offs[l], w.packed[l])
     qe[1].record(stream)
     torch.cuda.synchronize()
     quant_ms = qe[0].elapsed_time(qe[1])
@@ -332,6 +353,8 @@ def run_wq(args, rank, world, local_rank):
         "config": {"workload": cfg.name, "model_shape": cfg.model.name, "layers": cfg.layers, "batch": cfg.B,
                    "visual_tokens": cfg.M, "window": cfg.S, "widths": list(cfg.widths), "gen_tokens": w.n_gen,
                    "parallelism": f"seqsplit{world}" if world > 1 else "single",
+                   "merge": (("fused peer-memory LSE merge" if w.peer is not None else (w.merge_note or
+                              "NCCL all-gather + wq_merge_partials")) if world > 1 else None),
                    "launch": "cuda-graph replay" if use_graph else "host launches",
                    "l2": f"inputs > L2: {cfg.layers} layers x {w.packed_bytes[0] / 1e6:.0f} MB packed rotated",
                    "window_mix": dict(zip(["2", "4", "8", "16"], [int(x) for x in w.class_windows]))},
@@ -624,7 +647,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host (no CUDA graphs)")
-    ap.add_argument("--no-ablation", action="store_true", help="skip the T9 unfused-baseline measurement")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the T8/T9/T11 ablation measurements")
+    ap.add_argument("--merge", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: fused peer-memory LSE merge in the decode kernel, or NCCL all-gather + merge")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

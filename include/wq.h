@@ -312,6 +312,31 @@ wq_status wq_decode_attention_unreordered(const void *q, const uint8_t *uimg, co
                                           int32_t R_max, float sm_scale, void *out, float *partial,
                                           void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Fused cross-GPU log-sum-exp merge of the long-video sequence split (§8(e) P2,
+ * SURVEY.md §8(f) row 2): the decode kernel itself exchanges the per-rank (m, l, o)
+ * partials over NVLink peer memory and merges them, instead of partial -> NCCL
+ * all-gather -> wq_merge_partials.
+ *
+ * wq_peer_buffer_bytes: bytes of the symmetric per-rank buffer
+ *   [2 parities][G][B][Hq][d+2] fp32 + one u32 counter per (b, h), 256-B aligned.
+ *   Every rank allocates one (cudaMalloc, zero-filled ONCE), maps the peers' buffers
+ *   (CUDA IPC, peer access over NVLink) and keeps a device array of the G pointers.
+ * wq_decode_attention_peer: wq_decode_attention of rank `rank` over its shard
+ *   (wq_shard_slots) that writes the MERGED fp16 out [B][Hq][d] of all G ranks.
+ *   `epoch` = 1, 2, 3, ... on every call (the same on all ranks); all G ranks must make
+ *   the same sequence of calls (the kernel waits on its peers' contributions).
+ *   peer_bufs: device array [G] of device pointers (entry `rank` = local_buf).
+ *   No PDL flag.  With G = 1 it is the ordinary decode through the exchange path.
+ * Errors: as wq_decode_attention, WQ_EINVAL for rank/G/epoch/NULL. */
+wq_status wq_peer_buffer_bytes(const wq_geom *g, int32_t G, size_t *bytes_host);
+wq_status wq_decode_attention_peer(const void *q, const uint8_t *packed, const int64_t *offs,
+                                   const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
+                                   const void *v_rest, const int64_t rest_strides[2],
+                                   const int32_t *rest_len, int32_t R_max, float sm_scale, void *out,
+                                   void *workspace, size_t workspace_bytes, void *const *peer_bufs,
+                                   void *local_buf, int32_t G, int32_t rank, uint32_t epoch, void *stream);
+
 /* Thread-local message of the last non-OK status of this thread. */
 const char *wq_last_error(void);
 

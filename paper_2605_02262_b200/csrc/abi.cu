@@ -207,11 +207,19 @@ wq_status wq_decode_attention(const void *q, const uint8_t *packed, const int64_
                                 sm_scale, out, partial, workspace, workspace_bytes, 0u, stream);
 }
 
+struct PeerCfg {
+  uint8_t *const *bufs;      // device array [G]
+  void *local;               // this rank's buffer (host-known device pointer)
+  int32_t G, rank;
+  uint32_t epoch;
+};
+
 static wq_status decode_impl(const void *q, const uint8_t *packed, const int64_t *offs,
                              const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
                              const void *v_rest, const int64_t rest_strides[2], const int32_t *rest_len,
                              int32_t R_max, float sm_scale, void *out, float *partial, void *workspace,
-                             size_t workspace_bytes, uint32_t flags, const int64_t *woff, void *stream) {
+                             size_t workspace_bytes, uint32_t flags, const int64_t *woff, void *stream,
+                             const PeerCfg *pc = nullptr) {
   if (flags & ~(uint32_t)WQ_DECODE_EARLY) return fail(WQ_EINVAL, "unknown decode flags 0x%x", flags);
   wq_status s = check_geom(g, true);
   if (s != WQ_OK) return s;
@@ -238,6 +246,15 @@ static wq_status decode_impl(const void *q, const uint8_t *packed, const int64_t
   a.out = (__half *)out; a.partial = partial;
   a.flags = flags;
   a.woff = woff;
+  if (pc) {
+    // the rank-local unit results go to this rank's slot of the current parity; the
+    // kernel exchanges them with the peers and writes the merged result to out
+    const int64_t slotf = (int64_t)g->B * g->Hq * (g->d + 2);
+    a.peer_bufs = pc->bufs; a.peer_G = pc->G; a.peer_rank = pc->rank; a.peer_epoch = pc->epoch;
+    a.peer_out = (__half *)out;
+    a.out = nullptr;
+    a.partial = reinterpret_cast<float *>(pc->local) + ((int64_t)(pc->epoch & 1u) * pc->G + pc->rank) * slotf;
+  }
   const int grp = a.grp;
   size_t part = (size_t)(sms + g->B * g->H) * grp * (g->d + 2) * sizeof(float);
   part = (part + 255) / 256 * 256;
@@ -256,6 +273,29 @@ wq_status wq_decode_attention_ex(const void *q, const uint8_t *packed, const int
                                  size_t workspace_bytes, uint32_t flags, void *stream) {
   return decode_impl(q, packed, offs, seg_off_l, g, k_rest, v_rest, rest_strides, rest_len, R_max, sm_scale, out,
                      partial, workspace, workspace_bytes, flags, nullptr, stream);
+}
+
+wq_status wq_peer_buffer_bytes(const wq_geom *g, int32_t G, size_t *bytes_host) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!bytes_host) return fail(WQ_EINVAL, "NULL pointer");
+  if (G < 1 || G > 64) return fail(WQ_EINVAL, "G=%d", G);
+  *bytes_host = wq::peer_buffer_bytes(g->B, g->H, g->Hq, g->d, G);
+  return WQ_OK;
+}
+
+wq_status wq_decode_attention_peer(const void *q, const uint8_t *packed, const int64_t *offs,
+                                   const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
+                                   const void *v_rest, const int64_t rest_strides[2], const int32_t *rest_len,
+                                   int32_t R_max, float sm_scale, void *out, void *workspace,
+                                   size_t workspace_bytes, void *const *peer_bufs, void *local_buf, int32_t G,
+                                   int32_t rank, uint32_t epoch, void *stream) {
+  if (!out || !peer_bufs || !local_buf) return fail(WQ_EINVAL, "NULL pointer (out / peer buffers)");
+  if (G < 1 || G > 64 || rank < 0 || rank >= G) return fail(WQ_EINVAL, "rank %d of %d", rank, G);
+  if (epoch == 0) return fail(WQ_EINVAL, "epoch must start at 1");
+  PeerCfg pc{reinterpret_cast<uint8_t *const *>(peer_bufs), local_buf, G, rank, epoch};
+  return decode_impl(q, packed, offs, seg_off_l, g, k_rest, v_rest, rest_strides, rest_len, R_max, sm_scale, out,
+                     nullptr, workspace, workspace_bytes, 0u, nullptr, stream, &pc);
 }
 
 wq_status wq_unreordered_layout(const wq_geom *g, const uint8_t *bits_l, int64_t *woff, void *stream) {

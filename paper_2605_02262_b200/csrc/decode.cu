@@ -392,6 +392,79 @@ WQ_DEV void produce_ur(const DecodeArgs &a, const CtaPlan &P, uint8_t *ring, uin
 }
 
 
+// ---- fused cross-GPU log-sum-exp merge ----
+// Symmetric buffer of every rank (peer_buffer_bytes): [2 parities][G ranks][B*Hq][d+2]
+// fp32 partials, then one u32 arrival counter per unit (zero-filled once).  The CTA that
+// holds the rank-local final partial of unit u (written to its own slot, a.partial)
+// stores the unit's rows into slot [parity][rank] of every peer over NVLink (plain
+// stores to IPC-mapped peer memory), releases them system-wide and bumps every peer's
+// counter of u; it then waits for its own counter to reach G * epoch (every rank's
+// rows of u have landed) and merges the G partials of u by log-sum-exp into out.
+// Parity: a rank can run at most one call ahead of a peer (call e+1 of a rank needs
+// every rank's rows of e+1), so two parities never collide.
+WQ_DEV void red_release_sys_add(uint32_t *p, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+WQ_DEV uint32_t ld_acquire_sys(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+template <int D, int NT>
+WQ_DEV void peer_exchange_merge(const DecodeArgs &a, int tid, int u, int b, int h) {
+  const int grp = a.grp, G = a.peer_G, r = a.peer_rank;
+  const int64_t slotf = (int64_t)a.B * a.Hq * (D + 2);            // floats per (parity, rank) slot
+  const int par = (int)(a.peer_epoch & 1u);
+  const int64_t row0 = (int64_t)b * a.Hq + h * grp;
+  const int nrow = grp * (D + 2);
+  named_bar_sync(1, NT);                          // the unit's rows in the own slot are complete
+  const float *mine = a.partial + row0 * (D + 2);
+  for (int p = 0; p < G; p++) {
+    if (p == r) continue;
+    float *dst = reinterpret_cast<float *>(a.peer_bufs[p]) + (par * G + r) * slotf + row0 * (D + 2);
+    for (int i = tid; i < nrow; i += NT) dst[i] = mine[i];
+  }
+  __threadfence_system();
+  named_bar_sync(1, NT);
+  const int64_t ctr_off = 2LL * G * slotf * 4;                    // bytes: counters after the slots
+  if (tid == 0) {
+    for (int p = 0; p < G; p++) red_release_sys_add(reinterpret_cast<uint32_t *>(a.peer_bufs[p] + ctr_off) + u, 1u);
+    const uint32_t *my = reinterpret_cast<const uint32_t *>(a.peer_bufs[r] + ctr_off) + u;
+    const uint32_t want = (uint32_t)G * a.peer_epoch;
+    // bounded wait (10 s of globaltimer): a peer that never arrives (a rank that skipped
+    // the call, a broken mapping) must not hang the GPU; the result is then invalid
+    const uint64_t t0 = gtime();
+    while ((int32_t)(ld_acquire_sys(my) - want) < 0) {
+      __nanosleep(64);
+      if (gtime() - t0 > 10000000000ull) break;
+    }
+  }
+  named_bar_sync(1, NT);
+  const float *base = reinterpret_cast<const float *>(a.peer_bufs[r]) + par * G * slotf + row0 * (D + 2);
+  for (int idx = tid; idx < grp * D; idx += NT) {
+    const int j = idx / D, cc = idx - j * D;
+    float M = -INFINITY;
+    for (int p = 0; p < G; p++) {
+      const float *pp = base + p * slotf + j * (D + 2);
+      if (__ldcv(pp + 1) > 0.f) M = fmaxf(M, __ldcv(pp));
+    }
+    float L = 0.f, O = 0.f;
+    for (int p = 0; p < G; p++) {
+      const float *pp = base + p * slotf + j * (D + 2);
+      const float l = __ldcv(pp + 1);
+      if (!(l > 0.f)) continue;
+      const float f = expf(__ldcv(pp) - M);
+      L = fmaf(f, l, L);
+      O = fmaf(f, __ldcv(pp + 2 + cc), O);
+    }
+    a.peer_out[(row0 + j) * D + cc] = __float2half_rn(L > 0.f ? O / L : 0.f);
+  }
+}
+
+size_t peer_buffer_bytes(int B, int H, int Hq, int d, int G) {
+  return 2ull * G * B * Hq * (d + 2) * sizeof(float) + (((size_t)B * H * sizeof(uint32_t) + 255) / 256) * 256;
+}
+
 template <int D, int S, bool UR>
 __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   using SM = DecodeSmem<D, S>;
@@ -654,6 +727,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       if (ts && tid == 0) { ts[6] = *s_flag; ts[7] = c - c0; }
       if (*s_flag) merge_unit<D, NCW * 32>(a, tid, u, b, h, c0, c1);
     }
+    if (a.peer_bufs && (!split || *s_flag)) peer_exchange_merge<D, NCW * 32>(a, tid, u, b, h);
     if (ts && tid == 0) {
       const uint64_t t_e2 = clock64();
       ts[68] += t_e1 - t_e0; ts[69] += t_e2 - t_e1;

@@ -82,6 +82,15 @@ WQ_DEV __half q17_scale(float mn, float mx, float qmaxf) {
   return s16;
 }
 
+#ifndef WQ_Q_SLEEP
+#define WQ_Q_SLEEP 0           // ns of back-off between mbarrier polls (0: spin)
+#endif
+// waiting warps back off so the warps that compute get the issue slots
+WQ_DEV void qwait(uint64_t *b, uint32_t parity) {
+  if (WQ_Q_SLEEP > 0) mbar_wait_sleep(b, parity, WQ_Q_SLEEP);
+  else mbar_wait(b, parity);
+}
+
 // ---------------------------------------------------------------------------------
 // k_quant: persistent.  A CTA runs TEAMS teams of 4 warps; a team owns two window
 // slots in shared memory (double buffering) and quantizes windows gt, gt + nteams, ...
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
     const int64_t wi = gt + k * nt;
     if (wi >= nwin) return;
     const int sl = (int)(k % NSL);
-    mbar_wait(&empty[sl], (uint32_t)((k / NSL) & 1) ^ 1u);
+    qwait(&empty[sl], (uint32_t)((k / NSL) & 1) ^ 1u);
     int b, h, slot;
     locate(wi, b, h, slot);
     const int32_t *so = a.seg_off + 5 * b;
@@ -409,7 +418,7 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
     if (wi >= nwin) break;
     if (tw == 0 && lane == 0) issue(k + NSL - 1);  // the slot released after window k-1
     const int sl = (int)(k % NSL);
-    mbar_wait(&full[sl], (uint32_t)((k / NSL) & 1));
+    qwait(&full[sl], (uint32_t)((k / NSL) & 1));
     const int bits = wdesc[sl].bits;
     if (bits) {
       uint8_t *rec = a.packed + wdesc[sl].roff;

@@ -52,7 +52,13 @@ struct DecodeArgs {
   int32_t *ws_cnt;           // [B*H]
   uint64_t *ws_ts;           // [num_sms][8] timestamps when debug & 8, else NULL
   const int64_t *woff;       // non-NULL: unreordered image, window offsets [B][W+1]
+  // fused cross-GPU LSE merge; peer_bufs NULL: off
+  uint8_t *const *peer_bufs; // device array [G] of the ranks' symmetric buffers (IPC-mapped)
+  int peer_G, peer_rank;
+  uint32_t peer_epoch;       // 1, 2, ... per call: the counters reach G * epoch
+  __half *peer_out;          // out [B][Hq][d] of the merged result
 };
+size_t peer_buffer_bytes(int B, int H, int Hq, int d, int G);
 size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms);
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st);
 cudaError_t launch_decode_tc(const DecodeArgs &a, int num_sms, cudaStream_t st);   // d = 128

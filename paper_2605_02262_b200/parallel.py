@@ -8,6 +8,11 @@
   partials are exchanged with ONE all-gather and merged by log-sum-exp
   (``wq_merge_partials``).
 
+* P2 fused: ``PeerMerge`` sets up one symmetric buffer per rank
+  (cudaMalloc, CUDA IPC handles exchanged over the process group, peers mapped with
+  peer access over NVLink) for ``wq_decode_attention_peer``, whose kernel exchanges the
+  partials through peer memory and merges them itself -- no NCCL call, no merge kernel.
+
 Only host-side orchestration lives here; every arithmetic step runs in libwq.
 """
 from __future__ import annotations
@@ -46,3 +51,67 @@ def all_gather_partials(part: torch.Tensor, group=None) -> torch.Tensor:
     else:                                  # gloo (CPU tests): list form
         dist.all_gather(list(out.unbind(0)), part.contiguous(), group=group)
     return out
+
+
+def _cudart():
+    from cuda.bindings import runtime as cudart
+    return cudart
+
+
+def _ck(res):
+    err = res[0] if isinstance(res, tuple) else res
+    if int(err) != 0:
+        raise RuntimeError(f"CUDA runtime error {err}")
+    return res[1] if isinstance(res, tuple) and len(res) > 1 else None
+
+
+class PeerMerge:
+    """Symmetric buffers of the fused cross-GPU LSE merge (include/wq.h wq_peer_buffer_bytes).
+
+    Every rank cudaMallocs one zero-filled buffer, publishes its IPC handle with
+    all_gather_object, and maps the peers' buffers (cudaIpcOpenMemHandle, lazy peer
+    access).  ``ptrs`` is the int64 device tensor of the G buffer addresses (entry rank =
+    own buffer); ``next_epoch()`` numbers the calls 1, 2, ... identically on all ranks."""
+
+    def __init__(self, g, group=None, device=None):
+        from paper_2605_02262_b200 import wq
+        self.G = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.bytes = wq.wq_peer_buffer_bytes(g, self.G)
+        rt = _cudart()
+        self.local = int(_ck(rt.cudaMalloc(self.bytes)))
+        _ck(rt.cudaMemset(self.local, 0, self.bytes))
+        self.opened = []
+        addrs = [0] * self.G
+        addrs[self.rank] = self.local
+        if self.G > 1:
+            h = _ck(rt.cudaIpcGetMemHandle(self.local))
+            handles = [None] * self.G
+            dist.all_gather_object(handles, bytes(h.reserved), group=group)
+            for p in range(self.G):
+                if p == self.rank:
+                    continue
+                hp = rt.cudaIpcMemHandle_t()
+                hp.reserved = handles[p]
+                ptr = int(_ck(rt.cudaIpcOpenMemHandle(hp, rt.cudaIpcMemLazyEnablePeerAccess)))
+                self.opened.append(ptr)
+                addrs[p] = ptr
+        _ck(rt.cudaDeviceSynchronize())
+        self.ptrs = torch.tensor(addrs, dtype=torch.int64, device=dev)
+        self.epoch = 0
+        if self.G > 1:
+            dist.barrier(group=group)
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        return self.epoch
+
+    def close(self):
+        rt = _cudart()
+        for p in self.opened:
+            rt.cudaIpcCloseMemHandle(p)
+        self.opened = []
+        if self.local:
+            rt.cudaFree(self.local)
+            self.local = 0

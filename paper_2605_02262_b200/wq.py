@@ -75,6 +75,9 @@ def load(build_if_missing: bool = True):
         "wq_dequant_layout": [C.POINTER(Geom), P, P, P, P],
         "wq_dequantize_image": [P, P, P, C.POINTER(Geom), P, P, P],
         "wq_unreordered_layout": [C.POINTER(Geom), P, P, P],
+        "wq_peer_buffer_bytes": [C.POINTER(Geom), I32, P],
+        "wq_decode_attention_peer": [P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, SZ, P, P, I32, I32,
+                                     C.c_uint32, P],
         "wq_unreorder_image": [P, P, P, P, C.POINTER(Geom), P, P, P],
         "wq_decode_attention_unreordered": [P, P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, P, SZ, P],
     }
@@ -95,6 +98,7 @@ def exported_symbols():
             "wq_packed_bytes", "wq_layer_layout", "wq_reorder_quantize_pack", "wq_decode_workspace",
             "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_dequant_layout", "wq_dequantize_image",
             "wq_unreordered_layout", "wq_unreorder_image", "wq_decode_attention_unreordered",
+            "wq_peer_buffer_bytes", "wq_decode_attention_peer",
             "wq_last_error", "wq_version"]
 
 
@@ -305,3 +309,26 @@ def wq_decode_attention_unreordered(q, uimg, offs, seg_off_l, woff, g: Geom, k_r
                                                   float(sm_scale), _ptr(out), _ptr(partial), _ptr(workspace),
                                                   workspace.numel(), _stream(stream)))
     return out, partial
+
+
+def wq_peer_buffer_bytes(g: Geom, G: int) -> int:
+    n = C.c_size_t(0)
+    _check(load().wq_peer_buffer_bytes(C.byref(g), int(G), C.byref(n)))
+    return n.value
+
+
+def wq_decode_attention_peer(q, packed, offs, seg_off_l, g: Geom, k_rest, v_rest, rest_len, sm_scale: float,
+                             out, peer_ptrs: torch.Tensor, local_ptr: int, G: int, rank: int, epoch: int,
+                             workspace=None, stream=None):
+    """Decode of this rank's shard with the fused cross-GPU LSE merge: out receives the merged
+    result of all G ranks.  peer_ptrs: int64 device tensor [G] of the symmetric buffers."""
+    if workspace is None:
+        workspace = torch.zeros(wq_decode_workspace(g), dtype=torch.uint8, device=q.device)
+    R_max = 0 if k_rest is None else k_rest.shape[2]
+    rs = (C.c_int64 * 2)(*(k_rest.stride(0), k_rest.stride(1))) if k_rest is not None else None
+    _check(load().wq_decode_attention_peer(_ptr(q), _ptr(packed), _ptr(offs), _ptr(seg_off_l), C.byref(g),
+                                           _ptr(k_rest), _ptr(v_rest), rs, _ptr(rest_len), R_max, float(sm_scale),
+                                           _ptr(out), _ptr(workspace), workspace.numel(), _ptr(peer_ptrs),
+                                           C.c_void_p(local_ptr), int(G), int(rank), C.c_uint32(epoch),
+                                           _stream(stream)))
+    return out

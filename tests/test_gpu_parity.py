@@ -435,3 +435,29 @@ def test_pearson_scores_parity(orc):
     assert np.max(np.abs(got - ref)) < 1e-12
     cos = wq.wq_window_scores(vis, txt, S).cpu().numpy()
     assert np.max(np.abs(cos - orc.window_scores(vis.cpu().numpy(), txt.cpu().numpy(), S))) < 1e-12
+
+
+def test_peer_merge_single_rank(orc):
+    """The fused cross-GPU merge path (wq_decode_attention_peer) with G = 1: the kernel writes
+    its partials to its slot of the symmetric buffer, bumps the arrival counter, waits for it
+    and merges -- over several epochs (both parities) it must equal the plain decode."""
+    from paper_2605_02262_b200.parallel import PeerMerge
+    for d, S, W, tail, B, H, Hq in [(128, 32, 40, 7, 2, 4, 28), (64, 16, 30, 5, 2, 2, 14)]:
+        c = small_case(500 + d + S, d=d, S=S, W=W, tail=tail, B=B, H=H, Hq=Hq)
+        g = c["g"]
+        sc = wq.wq_window_scores(c["vis"], c["txt"], S)
+        thr = orc.thresholds([0.45], 2.0, 4)
+        bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
+        sm = 1 / math.sqrt(d)
+        offs, packed, out, _ = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm[0], seg[0],
+                                         c["q"], sm)
+        pm = PeerMerge(g)
+        ref = _decode_ref(orc, c, g, offs, packed, perm[0], seg[0], sm)[0]
+        for _ in range(3):
+            o2 = torch.zeros_like(out)
+            wq.wq_decode_attention_peer(c["q"], packed, offs, seg[0], g, c["kr"], c["vr"], c["rest_len"], sm, o2,
+                                        pm.ptrs, pm.local, 1, 0, pm.next_epoch())
+            torch.cuda.synchronize()
+            assert rel_err(o2.float().cpu().numpy(), ref) <= ATTN_TOL
+            assert torch.equal(o2, out)
+        pm.close()
