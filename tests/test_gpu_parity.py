@@ -461,3 +461,51 @@ def test_peer_merge_single_rank(orc):
             assert rel_err(o2.float().cpu().numpy(), ref) <= ATTN_TOL
             assert torch.equal(o2, out)
         pm.close()
+
+
+def _peer_ipc_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2605_02262_b200.parallel import PeerMerge, _cudart, _ck
+        g = wq.geom(2, 2, 14, 64, 160, 16, (2, 4, 8, 16))
+        pm = PeerMerge(g, device=torch.device("cuda", 0))
+        ptrs = pm.ptrs.cpu().tolist()
+        assert ptrs[rank] == pm.local and len(set(ptrs)) == world
+        rt = _cudart()
+        # every rank writes its signature into slot `rank` of every peer's buffer
+        sig = np.full(16, 1000 + rank, np.int32)
+        for p in range(world):
+            _ck(rt.cudaMemcpy(ptrs[p] + 64 * rank, sig.ctypes.data, 64, rt.cudaMemcpyKind.cudaMemcpyHostToDevice))
+        torch.cuda.synchronize()
+        dist.barrier()
+        got = np.zeros(16 * world, np.int32)
+        _ck(rt.cudaMemcpy(got.ctypes.data, pm.local, 64 * world, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost))
+        ok = all((got[16 * p:16 * (p + 1)] == 1000 + p).all() for p in range(world))
+        dist.barrier()
+        pm.close()
+        dist.destroy_process_group()
+        q.put((rank, bool(ok), ""))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, False, repr(e)))
+
+
+def test_peer_merge_ipc_setup_two_processes():
+    """PeerMerge's CUDA IPC exchange (the setup of the fused cross-GPU merge) between two
+    processes on one GPU: every rank writes into every peer's mapped buffer and reads back
+    its own.  (No kernel waits on another process: only the mappings are exercised.)"""
+    import multiprocessing as mp
+    import random
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29000 + random.randint(0, 999)
+    procs = [ctx.Process(target=_peer_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
