@@ -509,3 +509,58 @@ def test_peer_merge_ipc_setup_two_processes():
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
+
+
+def test_ablation_paths_full_size_c5(orc):
+    """The T8 (unreordered) and T9 (unfused) baselines and the fused peer-merge path at the
+    full C5 size bench.py times, with the oracle on a sampled request: unreordered and peer
+    decodes within 2e-3 of the oracle over the same codes; the unfused path within 2e-3 of the
+    oracle's attention over its FP16 image."""
+    from paper_2605_02262_b200.parallel import PeerMerge
+    cfg = configs.CONFIGS["C5"]
+    m = cfg.model
+    B, layer = cfg.B, cfg.layers - 1
+    vis, txt = synth.embeddings(B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, "cuda")
+    sc = wq.wq_window_scores(vis, txt, cfg.S)
+    del vis, txt
+    thr = orc.thresholds(cfg.sensitivities(), cfg.alpha, len(cfg.widths))
+    g = wq.geom(B, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, cfg.layers, g)
+    bl, perm, seg = bits[layer].contiguous(), perm[layer].contiguous(), seg[layer].contiguous()
+    K, V, kr, vr, rest_len = synth.layer_tensors(cfg, layer, "cuda")
+    q = synth.queries(B, m.Hq, m.H, m.d, cfg.seed, layer, device="cuda")
+    sm = 1 / math.sqrt(m.d)
+    offs, packed, out, _ = run_layer(g, K, V, kr, vr, rest_len, perm, seg, q, sm)
+    del K, V
+    woff = wq.wq_unreordered_layout(g, bl)
+    uimg = torch.zeros_like(packed)
+    wq.wq_unreorder_image(packed, offs, seg, perm, g, woff, uimg)
+    out_u = torch.empty_like(out)
+    wq.wq_decode_attention_unreordered(q, uimg, offs, seg, woff, g, kr, vr, rest_len, sm, out=out_u)
+    seg16, offs16 = wq.wq_dequant_layout(g, seg)
+    img16 = torch.zeros(int(offs16[-1].item()) + 16, dtype=torch.uint8, device="cuda")
+    wq.wq_dequantize_image(packed, offs, seg, g, offs16, img16)
+    out_16 = torch.empty_like(out)
+    wq.wq_decode_attention(q, img16, offs16, seg16, g, kr, vr, rest_len, sm, out=out_16)
+    pm = PeerMerge(g)
+    out_p = torch.empty_like(out)
+    wq.wq_decode_attention_peer(q, packed, offs, seg, g, kr, vr, rest_len, sm, out_p, pm.ptrs, pm.local, 1, 0,
+                                pm.next_epoch())
+    torch.cuda.synchronize()
+    pm.close()
+    assert torch.equal(out_p, out)
+    b = B - 1
+    sub = dict(q=q[b:b + 1], kr=kr[b:b + 1], vr=vr[b:b + 1], rest_len=rest_len[b:b + 1])
+    gb = wq.geom(1, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
+    ob = offs[b * m.H:(b + 1) * m.H + 1] - offs[b * m.H]
+    pk = packed[int(offs[b * m.H].item()):int(offs[(b + 1) * m.H].item())]
+    r = _decode_ref(orc, sub, gb, ob, pk, perm[b:b + 1], seg[b:b + 1], sm)[0]
+    assert rel_err(out_u[b:b + 1].float().cpu().numpy(), r) <= ATTN_TOL
+    # the FP16 image of request b, bit-exact, and its attention
+    ob16 = offs16[b * m.H:(b + 1) * m.H + 1] - offs16[b * m.H]
+    pk16 = img16[int(offs16[b * m.H].item()):int(offs16[(b + 1) * m.H].item())]
+    rimg, roffs16, rseg16 = orc.dequantize_image(pk.cpu().numpy(), ob.cpu().numpy(), seg[b:b + 1].cpu().numpy(),
+                                                 ogeom(orc, gb))
+    assert np.array_equal(pk16.cpu().numpy(), rimg[:int(roffs16[-1])])
+    r16 = _decode_ref(orc, sub, gb, ob16, pk16, perm[b:b + 1], seg16[b:b + 1], sm)[0]
+    assert rel_err(out_16[b:b + 1].float().cpu().numpy(), r16) <= ATTN_TOL
