@@ -115,9 +115,12 @@ struct QuantGeo {
   static constexpr int WORK = 16 * WRB;                 // one 16-row tile
   static constexpr int SCR = (D > S ? D : S) * 8;       // float2 params scratch per warp
 #ifndef WQ_Q_NSL
-#define WQ_Q_NSL 2
+#define WQ_Q_NSL 0                                      // 0: by window size (below)
 #endif
-  static constexpr int NSL = WQ_Q_NSL;                  // window slots per team
+  // window slots per team: double buffering pays while it leaves room for 4 teams; for
+  // S >= 64 (32-64 KB windows) one slot per team and more teams per SM win (C4 shape:
+  // S = 64 716 -> 583 us, S = 128 992 -> 662 us; S = 32 needs two: 493 vs 641 us)
+  static constexpr int NSL = WQ_Q_NSL > 0 ? WQ_Q_NSL : (S >= 64 ? 1 : 2);
   static constexpr int PER_TEAM = NSL * WIN + 4 * (WORK + SCR);
   static constexpr int T0 = (216 * 1024) / PER_TEAM;
   static constexpr int TEAMS = T0 > 4 ? 4 : (T0 < 1 ? 1 : T0);

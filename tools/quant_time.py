@@ -10,6 +10,8 @@ import oracle
 from paper_2605_02262_b200 import configs, synth, wq
 
 cfg = configs.CONFIGS[os.environ.get("CFG", "C5")]
+if os.environ.get("S"):
+    cfg = cfg.with_(S=int(os.environ["S"]), name=f"{cfg.name}-S{os.environ['S']}")
 m = cfg.model
 L = int(os.environ.get("NL", "4"))
 dev = "cuda"
