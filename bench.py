@@ -309,6 +309,8 @@ def run_wq(args, rank, world, local_rank):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    if w.peer is not None and w.peer.timed_out():
+        raise RuntimeError("fused cross-GPU merge: a peer wait timed out (outputs invalid)")
     total_ms = ev_all[0].elapsed_time(ev_all[1])
     dec_ms = sum(e[0].elapsed_time(e[1]) for e in ev_dec)
     # isolated wq_reorder_quantize_pack timing for the quantize GB/s figure: the L layers'

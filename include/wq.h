@@ -319,7 +319,9 @@ wq_status wq_decode_attention_unreordered(const void *q, const uint8_t *uimg, co
  * all-gather -> wq_merge_partials.
  *
  * wq_peer_buffer_bytes: bytes of the symmetric per-rank buffer
- *   [2 parities][G][B][Hq][d+2] fp32 + one u32 counter per (b, h), 256-B aligned.
+ *   [2 parities][G][B][Hq][d+2] fp32 + one u32 counter per (b, h) + one u32 error
+ *   word (set when a wait for the peers timed out after 10 s: the output of that call
+ *   is invalid; read it with wq_peer_error), 256-B aligned.
  *   Every rank allocates one (cudaMalloc, zero-filled ONCE), maps the peers' buffers
  *   (CUDA IPC, peer access over NVLink) and keeps a device array of the G pointers.
  * wq_decode_attention_peer: wq_decode_attention of rank `rank` over its shard
@@ -330,6 +332,8 @@ wq_status wq_decode_attention_unreordered(const void *q, const uint8_t *uimg, co
  *   No PDL flag.  With G = 1 it is the ordinary decode through the exchange path.
  * Errors: as wq_decode_attention, WQ_EINVAL for rank/G/epoch/NULL. */
 wq_status wq_peer_buffer_bytes(const wq_geom *g, int32_t G, size_t *bytes_host);
+/* Byte offset of the error word inside the symmetric buffer (u32; 0 = no timeout). */
+wq_status wq_peer_error_offset(const wq_geom *g, int32_t G, size_t *offset_host);
 wq_status wq_decode_attention_peer(const void *q, const uint8_t *packed, const int64_t *offs,
                                    const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
                                    const void *v_rest, const int64_t rest_strides[2],

@@ -284,6 +284,15 @@ wq_status wq_peer_buffer_bytes(const wq_geom *g, int32_t G, size_t *bytes_host) 
   return WQ_OK;
 }
 
+wq_status wq_peer_error_offset(const wq_geom *g, int32_t G, size_t *offset_host) {
+  wq_status s = check_geom(g, true);
+  if (s != WQ_OK) return s;
+  if (!offset_host) return fail(WQ_EINVAL, "NULL pointer");
+  if (G < 1 || G > 64) return fail(WQ_EINVAL, "G=%d", G);
+  *offset_host = 2ull * G * g->B * g->Hq * (g->d + 2) * sizeof(float) + (size_t)g->B * g->H * sizeof(uint32_t);
+  return WQ_OK;
+}
+
 wq_status wq_decode_attention_peer(const void *q, const uint8_t *packed, const int64_t *offs,
                                    const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
                                    const void *v_rest, const int64_t rest_strides[2], const int32_t *rest_len,

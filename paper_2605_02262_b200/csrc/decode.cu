@@ -436,7 +436,11 @@ WQ_DEV void peer_exchange_merge(const DecodeArgs &a, int tid, int u, int b, int 
     const uint64_t t0 = gtime();
     while ((int32_t)(ld_acquire_sys(my) - want) < 0) {
       __nanosleep(64);
-      if (gtime() - t0 > 10000000000ull) break;
+      if (gtime() - t0 > 10000000000ull) {
+        // error word after the counters: the host checks it (wq_peer_status)
+        atomicExch(const_cast<uint32_t *>(my) - u + a.B * a.H, 1u);
+        break;
+      }
     }
   }
   named_bar_sync(1, NT);
@@ -462,7 +466,8 @@ WQ_DEV void peer_exchange_merge(const DecodeArgs &a, int tid, int u, int b, int 
 }
 
 size_t peer_buffer_bytes(int B, int H, int Hq, int d, int G) {
-  return 2ull * G * B * Hq * (d + 2) * sizeof(float) + (((size_t)B * H * sizeof(uint32_t) + 255) / 256) * 256;
+  // slots, then B*H arrival counters and one error word (a timed-out wait sets it)
+  return 2ull * G * B * Hq * (d + 2) * sizeof(float) + (((size_t)(B * H + 1) * sizeof(uint32_t) + 255) / 256) * 256;
 }
 
 template <int D, int S, bool UR>

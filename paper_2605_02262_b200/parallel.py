@@ -79,6 +79,7 @@ class PeerMerge:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.bytes = wq.wq_peer_buffer_bytes(g, self.G)
+        self.err_off = wq.wq_peer_error_offset(g, self.G)
         rt = _cudart()
         self.local = int(_ck(rt.cudaMalloc(self.bytes)))
         _ck(rt.cudaMemset(self.local, 0, self.bytes))
@@ -102,6 +103,16 @@ class PeerMerge:
         self.epoch = 0
         if self.G > 1:
             dist.barrier(group=group)
+
+    def timed_out(self) -> bool:
+        """True if a wait of this rank's decode kernels for its peers timed out (the
+        outputs of that call are invalid)."""
+        import numpy as np
+        rt = _cudart()
+        v = np.zeros(1, np.uint32)
+        _ck(rt.cudaDeviceSynchronize())
+        _ck(rt.cudaMemcpy(v.ctypes.data, self.local + self.err_off, 4, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost))
+        return bool(v[0])
 
     def next_epoch(self) -> int:
         self.epoch += 1

@@ -76,6 +76,7 @@ def load(build_if_missing: bool = True):
         "wq_dequantize_image": [P, P, P, C.POINTER(Geom), P, P, P],
         "wq_unreordered_layout": [C.POINTER(Geom), P, P, P],
         "wq_peer_buffer_bytes": [C.POINTER(Geom), I32, P],
+        "wq_peer_error_offset": [C.POINTER(Geom), I32, P],
         "wq_decode_attention_peer": [P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, SZ, P, P, I32, I32,
                                      C.c_uint32, P],
         "wq_unreorder_image": [P, P, P, P, C.POINTER(Geom), P, P, P],
@@ -98,7 +99,7 @@ def exported_symbols():
             "wq_packed_bytes", "wq_layer_layout", "wq_reorder_quantize_pack", "wq_decode_workspace",
             "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_dequant_layout", "wq_dequantize_image",
             "wq_unreordered_layout", "wq_unreorder_image", "wq_decode_attention_unreordered",
-            "wq_peer_buffer_bytes", "wq_decode_attention_peer",
+            "wq_peer_buffer_bytes", "wq_peer_error_offset", "wq_decode_attention_peer",
             "wq_last_error", "wq_version"]
 
 
@@ -332,3 +333,9 @@ def wq_decode_attention_peer(q, packed, offs, seg_off_l, g: Geom, k_rest, v_rest
                                            C.c_void_p(local_ptr), int(G), int(rank), C.c_uint32(epoch),
                                            _stream(stream)))
     return out
+
+
+def wq_peer_error_offset(g: Geom, G: int) -> int:
+    n = C.c_size_t(0)
+    _check(load().wq_peer_error_offset(C.byref(g), int(G), C.byref(n)))
+    return n.value

@@ -460,6 +460,7 @@ def test_peer_merge_single_rank(orc):
             torch.cuda.synchronize()
             assert rel_err(o2.float().cpu().numpy(), ref) <= ATTN_TOL
             assert torch.equal(o2, out)
+        assert not pm.timed_out()
         pm.close()
 
 
