@@ -248,17 +248,44 @@ class Workload:
         return n_win * m.H * cfg.S * m.d * 4 + self.packed_bytes[l]
 
 
+def _allreduce_max(t, group=None):
+    """max over ranks of a small device tensor (NCCL), through the host for gloo."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return t
+    c = t.cpu()
+    dist.all_reduce(c, op=dist.ReduceOp.MAX, group=group)
+    return c.to(t.device)
+
+
 def run_wq(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2605_02262_b200 import configs, wq
+    local_rank = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     wq.load(build_if_missing=False)
     cfg = configs.CONFIGS[args.config]
     if args.layers:
         cfg = cfg.with_(layers=args.layers)
-    w = Workload(cfg, dev, rank, world, n_gen=args.n_gen, merge=args.merge)
+    # multi-GPU mode (SURVEY §8(e)): P2 sequence split (long video, C5) with the fused
+    # cross-GPU merge, or P1 batch sharding (C2-C4): rank r takes requests
+    # [B r/N, B (r+1)/N) whole -- independent units, no collective on the data path
+    mode = args.parallel if args.parallel != "auto" else ("seqsplit" if cfg.idx == 5 else "batch")
+    if world > 1 and mode == "batch":
+        from paper_2605_02262_b200.parallel import batch_shard
+        b0, b1 = batch_shard(cfg.B, world, rank)
+        assert b1 > b0, f"batch sharding needs B >= N ({cfg.B} < {world})"
+        cfg_global = cfg
+        cfg = cfg.with_(B=b1 - b0)
+        w = Workload(cfg, dev, 0, 1, n_gen=args.n_gen)
+        w_world = 1
+    else:
+        cfg_global = cfg
+        w = Workload(cfg, dev, rank, world, n_gen=args.n_gen, merge=args.merge)
+        w_world = world
     group = dist.group.WORLD if world > 1 else None
     stream = torch.cuda.current_stream()
 
@@ -274,7 +301,7 @@ def run_wq(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    use_graph = world == 1 and not args.no_graph
+    use_graph = w_world == 1 and not args.no_graph
     if use_graph:
         # the step's ~1.4k launches replayed from two CUDA graphs (search + quantize,
         # decode): no host launch work between kernels; same kernels, same arguments
@@ -327,11 +354,11 @@ def run_wq(args, rank, world, local_rank):
     quant_ms = qe[0].elapsed_time(qe[1])
     t = torch.tensor([total_ms, dec_ms, quant_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = _allreduce_max(t)
     total_ms, dec_ms, quant_ms = t.tolist()
 
     ms_per_step = total_ms / args.steps
-    tokens = cfg.B * w.n_gen
+    tokens = cfg_global.B * w.n_gen                        # whole job: every rank's requests
     value = tokens / (ms_per_step / 1e3)
     n_dec = args.steps * w.n_gen * cfg.layers
     dec_launch_us = dec_ms * 1e3 / n_dec
@@ -352,11 +379,12 @@ def run_wq(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f16",
         "data": "synthetic (seeded; shapes of LLaVA-OneVision-7B / Qwen2-7B video workloads)",
-        "config": {"workload": cfg.name, "model_shape": cfg.model.name, "layers": cfg.layers, "batch": cfg.B,
+        "config": {"workload": cfg_global.name, "model_shape": cfg.model.name, "layers": cfg.layers,
+                   "batch": cfg_global.B, "batch_per_gpu": cfg.B,
                    "visual_tokens": cfg.M, "window": cfg.S, "widths": list(cfg.widths), "gen_tokens": w.n_gen,
-                   "parallelism": f"seqsplit{world}" if world > 1 else "single",
+                   "parallelism": (f"{mode}{world}" if world > 1 else "single"),
                    "merge": (("fused peer-memory LSE merge" if w.peer is not None else (w.merge_note or
-                              "NCCL all-gather + wq_merge_partials")) if world > 1 else None),
+                              "NCCL all-gather + wq_merge_partials")) if w_world > 1 else None),
                    "launch": "cuda-graph replay" if use_graph else "host launches",
                    "l2": f"inputs > L2: {cfg.layers} layers x {w.packed_bytes[0] / 1e6:.0f} MB packed rotated",
                    "window_mix": dict(zip(["2", "4", "8", "16"], [int(x) for x in w.class_windows]))},
@@ -367,7 +395,7 @@ def run_wq(args, rank, world, local_rank):
         "quantize": {"kernel": "wq_reorder_quantize_pack", "GB/s": round(q_gbs, 1),
                      "frac": round(q_gbs / peak, 4), "ms_per_L_layers": round(quant_ms, 3),
                      "bytes_L_layers": round(q_bytes)},
-        "decode_only_tokens_per_s": round(cfg.B / (dec_launch_us * 1e-6 * cfg.layers), 1),
+        "decode_only_tokens_per_s": round(cfg_global.B / (dec_launch_us * 1e-6 * cfg.layers), 1),
         "gpu_launches": w.launches_per_step() * args.steps,
         "clocks": clk.summary(),
     }
@@ -375,8 +403,12 @@ def run_wq(args, rank, world, local_rank):
         result["ablation_unfused_t9"] = run_ablation_unfused(w, stream)
         result["ablation_unreordered_t8"] = run_ablation_unreordered(w, stream)
         result["ablation_similarity_t11"] = run_ablation_similarity(w, stream)
-    if rank == 0 and not args.no_e2e:
-        result["e2e"] = run_e2e(w, args, stream)
+    if not args.no_e2e:
+        # every rank runs the end-to-end steps (the sequence split's decodes are
+        # collective); the time is the max over ranks, the value the whole job's tokens
+        e2e = run_e2e(w, args, stream, tokens=cfg_global.B * w.n_gen, group=group if world > 1 else None)
+        if rank == 0:
+            result["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(cfg, w, args)
     return result
@@ -507,7 +539,7 @@ def imgs_bytes(w, l):
     return n_slots * w.m.H * 4 * w.cfg.S * w.m.d
 
 
-def run_e2e(w, args, stream):
+def run_e2e(w, args, stream, tokens=None, group=None):
     """Same metric through the public API with HOST inputs: every step copies its
     inputs (embeddings, per-layer K/V + rest, queries) from pinned host memory and
     reads all decode outputs back, inside the timed region."""
@@ -538,11 +570,14 @@ def run_e2e(w, args, stream):
         w.q.copy_(hq, non_blocking=True)
         w.search()
         w.quantize()
-        w.decode()
+        w.decode(group)
         hout.copy_(w.out, non_blocking=True)
 
+    import torch.distributed as dist
     step()
     torch.cuda.synchronize()
+    if group is not None:
+        dist.barrier(group=group)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
@@ -550,7 +585,12 @@ def run_e2e(w, args, stream):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    return {"value": round(w.cfg.B * w.n_gen / (ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+    if group is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=w.dev)
+        t = _allreduce_max(t, group)
+        ms = float(t.item())
+    tokens = w.cfg.B * w.n_gen if tokens is None else tokens
+    return {"value": round(tokens / (ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "steps": steps}
 
 
@@ -650,6 +690,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host (no CUDA graphs)")
     ap.add_argument("--no-ablation", action="store_true", help="skip the T8/T9/T11 ablation measurements")
+    ap.add_argument("--parallel", default="auto", choices=["auto", "seqsplit", "batch"],
+                    help="N > 1: sequence split (P2, default for C5) or batch sharding (P1, default otherwise)")
     ap.add_argument("--merge", default="peer", choices=["peer", "nccl"],
                     help="N > 1: fused peer-memory LSE merge in the decode kernel, or NCCL all-gather + merge")
     args = ap.parse_args()
@@ -664,8 +706,15 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        lr = local_rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(lr)
+        # WQ_BENCH_BACKEND=gloo: host-side collectives only (testing the P1 batch-sharded
+        # mode with several ranks on one GPU; the sequence split needs NCCL / peer memory)
+        backend = os.environ.get("WQ_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+        else:
+            dist.init_process_group(backend)
     res = run_wq(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)
