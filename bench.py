@@ -220,12 +220,34 @@ class Workload:
                                                 self.kr[l], self.vr[l], rl, self.sm_scale, self.out[t, l],
                                                 self.peer.ptrs, self.peer.local, self.world, self.rank,
                                                 self.peer.next_epoch(), workspace=self.dws)
+                    if self.peer.epoch == 1 and not self._peer_checked(group):
+                        continue                                 # fell back to NCCL (call redone there)
                 else:
                     wq.wq_decode_attention(self.q[t, l], self.packed[l], self.offs[l], self.seg_r[l], self.g,
                                            self.kr[l], self.vr[l], rl, self.sm_scale, partial=self.part,
                                            workspace=self.dws, flags=flags)
                     torch.distributed.all_gather_into_tensor(self.gathered, self.part, group=group)
                     wq.wq_merge_partials(self.gathered, self.g, out=self.out[t, l])
+
+    def _peer_checked(self, group):
+        """After the first fused call: every rank checks its timeout flag, and if any rank's
+        wait timed out all ranks switch to the NCCL path (decided collectively) and redo
+        the call that way.  Returns True if the fused path stays."""
+        import torch
+        import torch.distributed as dist
+        bad = torch.tensor([1.0 if self.peer.timed_out() else 0.0], device=self.dev)
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX, group=group)
+        if bad.item() == 0.0:
+            return True
+        self.peer = None
+        self.merge_note = "peer-memory exchange timed out at the first call; NCCL all-gather used"
+        wq = self.wq
+        rl = self.rest_len[0] if self.rank == 0 else self.rest_zero
+        wq.wq_decode_attention(self.q[0, 0], self.packed[0], self.offs[0], self.seg_r[0], self.g, self.kr[0],
+                               self.vr[0], rl, self.sm_scale, partial=self.part, workspace=self.dws)
+        torch.distributed.all_gather_into_tensor(self.gathered, self.part, group=group)
+        wq.wq_merge_partials(self.gathered, self.g, out=self.out[0, 0])
+        return False
 
     def launches_per_step(self):
         per_dec = 1 if (self.world == 1 or self.peer is not None) else 2
