@@ -13,6 +13,12 @@
 namespace wq {
 
 constexpr int ST = 128;  // threads per CTA
+#ifndef WQ_SC_RB
+#define WQ_SC_RB 2        // visual rows per block reduction (2 with 3 CTAs/SM: C5 702 -> 560 us)
+#endif
+#ifndef WQ_SC_MINB
+#define WQ_SC_MINB 3      // CTAs per SM the register budget must allow
+#endif
 
 // Deterministic block sum of NV doubles per thread (fixed tree).
 template <int NV>
@@ -83,11 +89,11 @@ __global__ void __launch_bounds__(ST) k_text_pool(const __half *__restrict__ txt
 }
 
 template <int NC, bool CENTER>  // 16-byte chunks per thread per row: ceil(D / 8 / ST); CENTER: Pearson
-__global__ void __launch_bounds__(ST) k_window_scores(const __half *__restrict__ vis, int64_t vrs,
+__global__ void __launch_bounds__(ST, WQ_SC_MINB) k_window_scores(const __half *__restrict__ vis, int64_t vrs,
                                                       int64_t vbs, int M, int N, int D, int S,
                                                       const double *__restrict__ tbar,
                                                       double *__restrict__ scores) {
-  constexpr int RB = 4;  // rows per batch
+  constexpr int RB = WQ_SC_RB;  // rows per batch
   __shared__ double red[4 * RB];
   const int w = blockIdx.x, b = blockIdx.y, W = gridDim.x, tid = threadIdx.x;
   const int nchunk = D / 8;
