@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2605_02262_b200 import configs, synth, wq
 import oracle
-cfg = configs.CONFIGS["C5"]; m = cfg.model
+cfg = configs.CONFIGS[os.environ.get("CFG", "C5")]; m = cfg.model
 dev = "cuda"
 vis, txt = synth.embeddings(cfg.B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, dev)
 g = wq.geom(cfg.B, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
@@ -30,7 +30,7 @@ for mode in [int(x) for x in os.environ.get("DBG", "0,19").split(",")]:
     for it in range(4):
         ws[-nsm * TSB:].zero_()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        e0.record(); wq.wq_decode_attention(q, packed, offs, seg[l].contiguous(), g, kr, vr, rest_len, 1 / math.sqrt(128), out=out, workspace=ws); e1.record()
+        e0.record(); wq.wq_decode_attention(q, packed, offs, seg[l].contiguous(), g, kr, vr, rest_len, 1 / math.sqrt(m.d), out=out, workspace=ws); e1.record()
         torch.cuda.synchronize()
     print(f"=== mode {mode}: event us {e0.elapsed_time(e1) * 1e3:.1f}")
     tsb = ws[-nsm * TSB:].view(torch.int64).view(nsm, TS).cpu().numpy().astype(np.float64)
