@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
 
   // ---- prologue (warp 0): unit cost prefix, then this CTA's share ----
   CtaPlan *cp = reinterpret_cast<CtaPlan *>(sm + SM::plan_off);
-  if (warp == 0) plan_cta<D, S, false>(a, ustart, cp, s_flag, lane);
+  if (warp == 0) plan_cta<D, S, false, (!UR && WQ_DEC_STREAM)>(a, ustart, cp, s_flag, lane);
   if (tid == 32) {
     for (int s = 0; s < NST; s++) {
       mbar_init(&full[s], 1);

@@ -13,6 +13,12 @@ constexpr int MAX_UNITS = 1024;         // B * H
 constexpr int64_t MIN_CTA_BYTES = 49152;
 constexpr uint32_t WQ_DECODE_EARLY_ = 1u;     // = WQ_DECODE_EARLY (include/wq.h)
 constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trace
+#ifndef WQ_DEC_EOV
+#define WQ_DEC_EOV 2000                // per-unit entry overhead in cost units of S*D/100
+#endif
+#ifndef WQ_DEC_STREAM
+#define WQ_DEC_STREAM 0                // 1: cost-stream split when units < CTAs (measured slower)
+#endif
 
 // Compile-time item sizes and costs of a (D, S) instantiation.  Work is partitioned
 // across CTAs in COST space, not bytes: every item costs its bytes plus a per-item
@@ -32,6 +38,9 @@ struct ItemGeo {
   //   8-bit 0.249, FP16 0.251, 16-token rest tile ~0.1; in units of S*D/100.
   //  tcgen05 kernel: the tensor work is asynchronous, an item costs its bytes plus
   //   a per-window dequantization term (same units).
+  // fixed cost of one unit entry of a CTA (its epilogue, ~2 us: ~13 2-bit windows),
+  // charged at the start of every unit in the cost-stream split
+  static constexpr int64_t EOV = WQ_DEC_EOV * (int64_t)S * D / 100;
   static constexpr int64_t cost(int k) {
     if constexpr (TC) {
       return k == 4 ? 40LL * D
@@ -126,7 +135,9 @@ struct Entry {
 // [ua, ub) whole, or one unit split over CTAs [c0, c1) of which this CTA takes
 // items [i0, i1).
 struct CtaPlan {
-  int ua, ub, split, c0, c1, i0, i1;
+  int ua, ub, split, c0, c1, i0, i1;   // split: 0 whole units, 1 one unit over [c0, c1), 2 cost stream
+  double lo, hi;                       // split 2: this CTA's range [lo, hi) of the units' cost stream
+  int G;                               // CTAs that get work
   int geo_ok;                           // geo/img_off of unit ua valid (handed over by the planner)
   int64_t img_off;
   UnitGeo geo;
@@ -134,7 +145,11 @@ struct CtaPlan {
 
 // ---- prologue (one warp): unit cost prefix ustart[U+1], then this CTA's share ----
 // Writes *cp and *s_flag = G (number of CTAs that get work).
-template <int D, int S, bool TC>
+// STREAM (fewer units than CTAs): CTA c takes the cost range [T c/G, T (c+1)/G) of the
+// units laid end to end, each unit's cost preceded by a fixed entry overhead EOV (its
+// epilogue: a CTA that ends one unit and starts the next runs two), so every CTA gets
+// the same cost; a unit-aligned split rounds each unit to a whole number of CTAs.
+template <int D, int S, bool TC, bool STREAM = false>
 WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_flag, int lane) {
   const int U = a.B * a.H;
   int64_t carry = 0;
@@ -146,7 +161,7 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
     if (u < U) {
       ioff = a.offs[u];
       unit_geo<D, S, TC>(a, u, gg);
-      v = unit_cost<D, S, TC>(gg);
+      v = unit_cost<D, S, TC>(gg) + (STREAM ? ItemGeo<D, S, TC>::EOV : 0);
     }
     int64_t x = v;
 #pragma unroll
@@ -178,6 +193,22 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
       ub += __popc(__ballot_sync(0xffffffffu, own <= c));
     }
     if (lane == 0) { cp->ua = ua; cp->ub = ub; cp->split = 0; cp->c0 = c; cp->c1 = c + 1; }
+  } else if (STREAM) {
+    const double Td = (double)T;
+    const double lo = Td * c / G, hi = Td * (c + 1) / G;
+    int ua = 0, ub = 0;
+    for (int base = 0; base < U; base += 32) {
+      const int u = base + lane;
+      bool before = false, starts = false;
+      if (u < U) {
+        const double us = (double)ustart[u], ue = (double)ustart[u + 1];
+        before = ue <= lo;                       // units have cost >= EOV > 0
+        starts = us < hi;
+      }
+      ua += __popc(__ballot_sync(0xffffffffu, before));
+      ub += __popc(__ballot_sync(0xffffffffu, starts));
+    }
+    if (lane == 0) { cp->ua = ua; cp->ub = ub; cp->split = 2; cp->c0 = c; cp->c1 = c + 1; cp->lo = lo; cp->hi = hi; }
   } else {
     // every unit gets 1 + its cost share of the G - U extra CTAs: unit u owns
     // CTAs [c0(u), c0(u+1)), c0(U) = G
@@ -205,7 +236,7 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
     cp->img_off = ioff;
     cp->geo_ok = 1;
   }
-  if (lane == 0) *s_flag = G;
+  if (lane == 0) { *s_flag = G; cp->G = G; }
 }
 
 // ---- producer (one lane): stream the CTA's entries into the ring ----
@@ -221,14 +252,14 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
   if (ts) ts[62] = gtime();
   int sg = 0;                                  // stage number of this CTA
   int uix = 0;                                 // entry number of this CTA
-  auto publish = [&](int u, int n_u, const UnitGeo *gg, const UnitPlan *pl) {
+  auto publish = [&](int u, int n_u, const UnitGeo *gg, const UnitPlan *pl, int ec0, int ec1) {
     while (*reinterpret_cast<volatile int *>(units_done) < uix - (NUS - 1)) {
     }
     Entry &d = ent[uix % NUS];
     d.u = u;
     d.n_u = n_u;
-    d.c0 = P.split ? P.c0 : c;
-    d.c1 = P.split ? P.c1 : c + 1;
+    d.c0 = ec0;
+    d.c1 = ec1;
     d.rl = gg ? gg->rl : 0;
     d.nslots = gg ? gg->nslots : 0;
 #pragma unroll
@@ -253,11 +284,32 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
       unit_geo<D, S, TC>(a, u, gg);
     }
     int i0 = 0, i1 = gg.nslots + gg.ntiles;
-    if (P.split) {
+    int ec0 = P.split == 1 ? P.c0 : c, ec1 = P.split == 1 ? P.c1 : c + 1;
+    if (P.split == 1) {
       const double ucost = (double)(ustart[u + 1] - ustart[u]);
       const int k = c - P.c0, n = P.c1 - P.c0;
       i0 = first_item<D, S, TC>(gg, ucost * k / n);
       if (k < n - 1) i1 = first_item<D, S, TC>(gg, ucost * (k + 1) / n);
+    } else if (P.split == 2) {
+      // this CTA's slice of unit u (items start EOV into the unit's cost range) and the
+      // CTAs [ec0, ec1) sharing the unit; every CTA evaluates the same expressions
+      const double us = (double)ustart[u], ue = (double)ustart[u + 1];
+      const double eov = (double)ItemGeo<D, S, TC>::EOV;
+      const double Td = (double)ustart[a.B * a.H];
+      const int Gp = P.G;
+      auto Bk = [&](int k) { return Td * k / Gp; };
+      if (P.lo > us) i0 = first_item<D, S, TC>(gg, P.lo - us - eov);
+      if (P.hi < ue) i1 = first_item<D, S, TC>(gg, P.hi - us - eov);
+      int k0 = (int)(us * Gp / Td);
+      k0 = k0 < 0 ? 0 : (k0 > Gp - 1 ? Gp - 1 : k0);
+      while (k0 + 1 < Gp && Bk(k0 + 1) <= us) k0++;
+      while (k0 > 0 && Bk(k0) > us) k0--;
+      int k1 = (int)(ue * Gp / Td);
+      k1 = k1 < 0 ? 0 : (k1 > Gp - 1 ? Gp - 1 : k1);
+      while (k1 > 0 && Bk(k1) >= ue) k1--;
+      while (k1 + 1 < Gp && Bk(k1 + 1) < ue) k1++;
+      ec0 = k0;
+      ec1 = k1 + 1;
     }
     UnitPlan pl;
     plan_unit<D, S, TC, STAGE>(gg, i0, i1, pl);
@@ -293,12 +345,12 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
           bulk_g2s_evict_first(dst, kr + (int64_t)r0 * D, nb, &full[slot], pol);
           bulk_g2s_evict_first(dst + cap * 32 * D, vr + (int64_t)r0 * D, nb, &full[slot], pol);
         }
-        if (!published) { publish(u, i1 - i0, &gg, &pl); published = true; }
+        if (!published) { publish(u, i1 - i0, &gg, &pl, ec0, ec1); published = true; }
       }
     }
-    if (!published) publish(u, i1 - i0, &gg, &pl);
+    if (!published) publish(u, i1 - i0, &gg, &pl, ec0, ec1);
   }
-  publish(-1, 0, nullptr, nullptr);           // terminator
+  publish(-1, 0, nullptr, nullptr, c, c + 1);   // terminator
   if (ts) ts[2] = gtime();
 }
 
