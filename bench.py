@@ -270,6 +270,51 @@ class Workload:
         return n_win * m.H * cfg.S * m.d * 4 + self.packed_bytes[l]
 
 
+def build_step(w, group, stream, use_graph: bool, warmup: int):
+    """The timed step of bench.py (also driven by tests/test_gpu_fullsize.py so the
+    parity check runs this exact launch path): search -> quantize -> decode, with
+    `warmup` eager passes first; under use_graph the step's launches are captured in two
+    CUDA graphs (search + quantize, decode) and replayed -- same kernels, same
+    arguments, PDL-chained decodes (WQ_DECODE_EARLY) inside the decode graph.
+    step(ev) records ev[0] / ev[1] around the decode phase."""
+    import torch
+
+    def step(ev=None):
+        w.search()
+        w.quantize()
+        if ev is not None:
+            ev[0].record(stream)
+        w.decode(group)
+        if ev is not None:
+            ev[1].record(stream)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if not use_graph:
+        return step
+    g_sq, g_dec = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_sq):
+        w.search()
+        w.quantize()
+    with torch.cuda.graph(g_dec):
+        w.decode(group)
+    torch.cuda.synchronize()
+    w._graphs = (g_sq, g_dec)                               # keep the graphs alive with the workload
+
+    def gstep(ev=None):
+        g_sq.replay()
+        if ev is not None:
+            ev[0].record(stream)
+        g_dec.replay()
+        if ev is not None:
+            ev[1].record(stream)
+
+    gstep()
+    torch.cuda.synchronize()
+    return gstep
+
+
 def _allreduce_max(t, group=None):
     """max over ranks of a small device tensor (NCCL), through the host for gloo."""
     import torch.distributed as dist
@@ -310,41 +355,8 @@ def run_wq(args, rank, world, local_rank):
         w_world = world
     group = dist.group.WORLD if world > 1 else None
     stream = torch.cuda.current_stream()
-
-    def step(ev=None):
-        w.search()
-        w.quantize()
-        if ev is not None:
-            ev[0].record(stream)
-        w.decode(group)
-        if ev is not None:
-            ev[1].record(stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
     use_graph = w_world == 1 and not args.no_graph
-    if use_graph:
-        # the step's ~1.4k launches replayed from two CUDA graphs (search + quantize,
-        # decode): no host launch work between kernels; same kernels, same arguments
-        g_sq, g_dec = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_sq):
-            w.search()
-            w.quantize()
-        with torch.cuda.graph(g_dec):
-            w.decode(group)
-        torch.cuda.synchronize()
-
-        def step(ev=None):                                   # noqa: F811
-            g_sq.replay()
-            if ev is not None:
-                ev[0].record(stream)
-            g_dec.replay()
-            if ev is not None:
-                ev[1].record(stream)
-
-        step()
-        torch.cuda.synchronize()
+    step = build_step(w, group, stream, use_graph, args.warmup)
     if world > 1:
         dist.barrier()
     ev_all = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -354,6 +366,8 @@ def run_wq(args, rank, world, local_rank):
         ev_all[0].record(stream)
         for s in range(args.steps):
             step(ev_dec[s])
+            if w.peer is not None and w.peer.timed_out():          # fused merge: fail loudly, at once
+                raise RuntimeError(f"fused cross-GPU merge: a peer wait timed out in step {s}")
         ev_all[1].record(stream)
         torch.cuda.synchronize()
     if world > 1:

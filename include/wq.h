@@ -108,7 +108,8 @@ typedef struct {
  *
  * Quantizer (Eq.14-16, reading Q17/Q18/Q21).  Per group x[0..n),
  * q_max = 2^b - 1, all arithmetic IEEE fp32 with one rounding per operation:
- *   mn = min x, mx = max x
+ *   mn = minimum x, mx = maximum x   (IEEE 754-2019 minimum/maximum, sec. 9.6:
+ *        -0 < +0, so mn is -0 iff the smallest value is a zero and a -0 is present)
  *   s  = max(RoundUp_fp16(fl(mx - mn) / q_max), 2^-24)        (stored fp16)
  *   r  = fl(1 / s)
  *   code_i = clamp(rint_half_even(fl(fl(x_i - mn) * r)), 0, q_max)
@@ -220,6 +221,11 @@ wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t s
  *   (m, l, o[d]) with m = max logit, l = sum exp(logit - m), o = sum exp(logit - m) v
  *   (unnormalized; m = -inf, l = 0 for an empty cache), may be NULL.
  * workspace: wq_decode_workspace(g) bytes, zero-filled once.
+ * Numerical domain (fp16 intermediates of the fused dequantization): for every K
+ *   channel group |q_c| * s_c < 2^15 (q*s is carried as an fp16 hi + lo pair) and for
+ *   every V token group s_t < 255 (p * s_t is an fp16 MMA operand with p <= 2^8, the
+ *   lazy-rescale headroom).  Outside it results are undefined.  For b = 2 this allows V
+ *   ranges up to 765 and, with |q| <= 8, K channel ranges up to 12288.
  * Errors: WQ_ESHAPE (unsupported d/S, Hq/H > 8), WQ_EINVAL (both outputs NULL). */
 wq_status wq_decode_workspace(const wq_geom *g, size_t *bytes_host);
 
@@ -321,7 +327,8 @@ wq_status wq_decode_attention_unreordered(const void *q, const uint8_t *uimg, co
  * wq_peer_buffer_bytes: bytes of the symmetric per-rank buffer
  *   [2 parities][G][B][Hq][d+2] fp32 + one u32 counter per (b, h) + one u32 error
  *   word (set when a wait for the peers timed out after 10 s: the output of that call
- *   is invalid; read it with wq_peer_error), 256-B aligned.
+ *   and of every later call is invalid, later waits give up at once; its byte offset is
+ *   wq_peer_error_offset), 256-B aligned.
  *   Every rank allocates one (cudaMalloc, zero-filled ONCE), maps the peers' buffers
  *   (CUDA IPC, peer access over NVLink) and keeps a device array of the G pointers.
  * wq_decode_attention_peer: wq_decode_attention of rank `rank` over its shard
@@ -330,6 +337,9 @@ wq_status wq_decode_attention_unreordered(const void *q, const uint8_t *uimg, co
  *   the same sequence of calls (the kernel waits on its peers' contributions).
  *   peer_bufs: device array [G] of device pointers (entry `rank` = local_buf).
  *   No PDL flag.  With G = 1 it is the ordinary decode through the exchange path.
+ *   Every CTA of the launch must be resident at once (one per SM, grid = SM count):
+ *   the call returns WQ_ECUDA if the occupancy query says otherwise.  The tcgen05
+ *   variant (WQ_DECODE_TC) is never used for this call.
  * Errors: as wq_decode_attention, WQ_EINVAL for rank/G/epoch/NULL. */
 wq_status wq_peer_buffer_bytes(const wq_geom *g, int32_t G, size_t *bytes_host);
 /* Byte offset of the error word inside the symmetric buffer (u32; 0 = no timeout). */
@@ -340,6 +350,24 @@ wq_status wq_decode_attention_peer(const void *q, const uint8_t *packed, const i
                                    const int32_t *rest_len, int32_t R_max, float sm_scale, void *out,
                                    void *workspace, size_t workspace_bytes, void *const *peer_bufs,
                                    void *local_buf, int32_t G, int32_t rank, uint32_t epoch, void *stream);
+
+/* Test entry of the fused merge without a second GPU: G = 2 virtual ranks of
+ * wq_decode_attention_peer run in ONE launch on this device, each on half of the SMs,
+ * rank r with its own q/packed/offs/seg_off/rest/out/workspace (HOST arrays of G device
+ * pointers: q_host[r] etc.) and the symmetric buffer local_bufs_host[r]; peer_bufs is the
+ * device array of the G buffers.  Every exchange step of the cross-GPU protocol runs
+ * (peer stores, system-scope release counters, acquire wait, LSE merge); since all CTAs
+ * of the launch are co-resident, no kernel waits on another launch.
+ * Errors: WQ_EUNSUPPORTED unless G = 2 and (d, S) in {(128, 32), (64, 16)}; as
+ * wq_decode_attention_peer otherwise. */
+wq_status wq_decode_attention_peer_emulated(int32_t G, const void *const *q_host, const uint8_t *const *packed_host,
+                                            const int64_t *const *offs_host, const int32_t *const *seg_off_host,
+                                            const wq_geom *g, const void *const *k_rest_host,
+                                            const void *const *v_rest_host, const int64_t rest_strides[2],
+                                            const int32_t *const *rest_len_host, int32_t R_max, float sm_scale,
+                                            void *const *out_host, void *const *workspace_host,
+                                            size_t workspace_bytes, void *const *peer_bufs,
+                                            void *const *local_bufs_host, uint32_t epoch, void *stream);
 
 /* Thread-local message of the last non-OK status of this thread. */
 const char *wq_last_error(void);

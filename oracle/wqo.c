@@ -314,13 +314,27 @@ void wqo_layer_layout(const wqo_geom *g, const int32_t *seg_off_l, int64_t *offs
 /* ------------------------------------------------------------------------ */
 static float f16f(uint16_t h) { return (float)wqo_f16_to_f64(h); }  /* exact */
 
+/* Q17: mn / mx are the IEEE 754-2019 minimum / maximum operations (section 9.6),
+ * which order -0 below +0: a group whose smallest value is a zero of either sign
+ * stores mn = -0 (0x8000) iff a -0 is present, independent of element order. */
+static float ieee_minimum(float a, float b) {
+  if (a < b) return a;
+  if (b < a) return b;
+  return signbit(a) ? a : b;                             /* equal: -0 wins over +0 */
+}
+static float ieee_maximum(float a, float b) {
+  if (a > b) return a;
+  if (b > a) return b;
+  return signbit(a) ? b : a;                             /* equal: +0 wins over -0 */
+}
+
 void wqo_quantize_group(const uint16_t *x, int32_t n, int64_t stride, int32_t bits,
                         uint16_t *s_out, uint16_t *mn_out, uint8_t *codes) {
   float mn = f16f(x[0]), mx = f16f(x[0]);
   for (int i = 1; i < n; i++) {
     float v = f16f(x[(int64_t)i * stride]);
-    if (v < mn) mn = v;
-    if (v > mx) mx = v;
+    mn = ieee_minimum(mn, v);
+    mx = ieee_maximum(mx, v);
   }
   float qmax = (float)((1 << bits) - 1);
   volatile float range = mx - mn;                        /* exact for fp16 operands */

@@ -214,12 +214,13 @@ struct PeerCfg {
   uint32_t epoch;
 };
 
-static wq_status decode_impl(const void *q, const uint8_t *packed, const int64_t *offs,
+// validated kernel arguments of one decode call (no launch)
+static wq_status decode_args(const void *q, const uint8_t *packed, const int64_t *offs,
                              const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
                              const void *v_rest, const int64_t rest_strides[2], const int32_t *rest_len,
                              int32_t R_max, float sm_scale, void *out, float *partial, void *workspace,
-                             size_t workspace_bytes, uint32_t flags, const int64_t *woff, void *stream,
-                             const PeerCfg *pc = nullptr) {
+                             size_t workspace_bytes, uint32_t flags, const int64_t *woff, const PeerCfg *pc,
+                             wq::DecodeArgs &a) {
   if (flags & ~(uint32_t)WQ_DECODE_EARLY) return fail(WQ_EINVAL, "unknown decode flags 0x%x", flags);
   wq_status s = check_geom(g, true);
   if (s != WQ_OK) return s;
@@ -235,14 +236,13 @@ static wq_status decode_impl(const void *q, const uint8_t *packed, const int64_t
   const int sms = wq::device_sm_count();
   if (workspace_bytes < wq::decode_workspace_bytes(g->B, g->H, g->Hq, g->d, sms))
     return fail(WQ_EINVAL, "workspace too small (see wq_decode_workspace)");
-  wq::DecodeArgs a{};
+  a = wq::DecodeArgs{};
   a.q = (const __half *)q; a.packed = packed; a.offs = offs; a.seg_off = seg_off_l;
   a.k_rest = (const __half *)k_rest; a.v_rest = (const __half *)v_rest;
   a.rs_b = R_max > 0 ? rest_strides[0] : 0; a.rs_h = R_max > 0 ? rest_strides[1] : 0;
   a.rest_len = R_max > 0 ? rest_len : nullptr; a.R_max = R_max;
   a.B = g->B; a.H = g->H; a.Hq = g->Hq; a.grp = g->Hq / g->H; a.d = g->d; a.S = g->S;
   a.scale_log2 = sm_scale * 1.4426950408889634f;
-  { const char *dbg = getenv("WQ_DECODE_DEBUG"); a.debug = dbg ? atoi(dbg) : 0; }
   a.out = (__half *)out; a.partial = partial;
   a.flags = flags;
   a.woff = woff;
@@ -261,9 +261,24 @@ static wq_status decode_impl(const void *q, const uint8_t *packed, const int64_t
   a.ws_part = reinterpret_cast<float *>(workspace);
   a.ws_cnt = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(workspace) + part);
   size_t cntb = ((size_t)g->B * g->H * sizeof(int32_t) + 255) / 256 * 256;
-  a.ws_ts = (a.debug & 8) ? reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(workspace) + part + cntb)
-                          : nullptr;
-  return cuda_status(wq::launch_decode(a, sms, S_(stream)), "decode");
+  // profiling builds only (WQ_DEC_PROFILE / WQ_TC_PROFILE): per-CTA timestamps when
+  // WQ_DECODE_DEBUG has bit 3 set; the environment is read once per process
+  static const int dbg = getenv("WQ_DECODE_DEBUG") ? atoi(getenv("WQ_DECODE_DEBUG")) : 0;
+  a.ws_ts = (dbg & 8) ? reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(workspace) + part + cntb) : nullptr;
+  return WQ_OK;
+}
+
+static wq_status decode_impl(const void *q, const uint8_t *packed, const int64_t *offs,
+                             const int32_t *seg_off_l, const wq_geom *g, const void *k_rest,
+                             const void *v_rest, const int64_t rest_strides[2], const int32_t *rest_len,
+                             int32_t R_max, float sm_scale, void *out, float *partial, void *workspace,
+                             size_t workspace_bytes, uint32_t flags, const int64_t *woff, void *stream,
+                             const PeerCfg *pc = nullptr) {
+  wq::DecodeArgs a;
+  wq_status s = decode_args(q, packed, offs, seg_off_l, g, k_rest, v_rest, rest_strides, rest_len, R_max, sm_scale,
+                            out, partial, workspace, workspace_bytes, flags, woff, pc, a);
+  if (s != WQ_OK) return s;
+  return cuda_status(wq::launch_decode(a, wq::device_sm_count(), S_(stream)), "decode");
 }
 
 wq_status wq_decode_attention_ex(const void *q, const uint8_t *packed, const int64_t *offs,
@@ -305,6 +320,34 @@ wq_status wq_decode_attention_peer(const void *q, const uint8_t *packed, const i
   PeerCfg pc{reinterpret_cast<uint8_t *const *>(peer_bufs), local_buf, G, rank, epoch};
   return decode_impl(q, packed, offs, seg_off_l, g, k_rest, v_rest, rest_strides, rest_len, R_max, sm_scale, out,
                      nullptr, workspace, workspace_bytes, 0u, nullptr, stream, &pc);
+}
+
+wq_status wq_decode_attention_peer_emulated(int32_t G, const void *const *q_host, const uint8_t *const *packed_host,
+                                            const int64_t *const *offs_host, const int32_t *const *seg_off_host,
+                                            const wq_geom *g, const void *const *k_rest_host,
+                                            const void *const *v_rest_host, const int64_t rest_strides[2],
+                                            const int32_t *const *rest_len_host, int32_t R_max, float sm_scale,
+                                            void *const *out_host, void *const *workspace_host,
+                                            size_t workspace_bytes, void *const *peer_bufs,
+                                            void *const *local_bufs_host, uint32_t epoch, void *stream) {
+  if (G != 2) return fail(WQ_EUNSUPPORTED, "emulation runs G = 2 virtual ranks (G=%d)", G);
+  if (!q_host || !packed_host || !offs_host || !seg_off_host || !out_host || !workspace_host || !peer_bufs ||
+      !local_bufs_host || (R_max > 0 && (!k_rest_host || !v_rest_host || !rest_len_host)))
+    return fail(WQ_EINVAL, "NULL pointer array");
+  if (epoch == 0) return fail(WQ_EINVAL, "epoch must start at 1");
+  if (!((g && g->d == 128 && g->S == 32) || (g && g->d == 64 && g->S == 16)))
+    return fail(WQ_EUNSUPPORTED, "emulation built for (d, S) = (128, 32) and (64, 16)");
+  wq::DecodeArgs ra[2];
+  for (int r = 0; r < G; r++) {
+    if (!out_host[r]) return fail(WQ_EINVAL, "NULL out of rank %d", r);
+    PeerCfg pc{reinterpret_cast<uint8_t *const *>(peer_bufs), local_bufs_host[r], G, r, epoch};
+    wq_status s = decode_args(q_host[r], packed_host[r], offs_host[r], seg_off_host[r], g,
+                              R_max > 0 ? k_rest_host[r] : nullptr, R_max > 0 ? v_rest_host[r] : nullptr,
+                              rest_strides, R_max > 0 ? rest_len_host[r] : nullptr, R_max, sm_scale, out_host[r],
+                              nullptr, workspace_host[r], workspace_bytes, 0u, nullptr, &pc, ra[r]);
+    if (s != WQ_OK) return s;
+  }
+  return cuda_status(wq::launch_decode_emu(ra, G, wq::device_sm_count(), S_(stream)), "decode (peer emulation)");
 }
 
 wq_status wq_unreordered_layout(const wq_geom *g, const uint8_t *bits_l, int64_t *woff, void *stream) {

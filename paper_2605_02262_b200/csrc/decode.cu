@@ -309,10 +309,10 @@ struct DecodeSmem {
 // last CTA the FP16 rest tiles.
 template <int D, int S, int STAGE, int NST, int NUS, int TABN>
 WQ_DEV void produce_ur(const DecodeArgs &a, const CtaPlan &P, uint8_t *ring, uint64_t *full, uint64_t *empty,
-                       Entry *ent, int *units_done, int *tab) {
+                       Entry *ent, int *units_done, int *tab, int vc) {
   using IG = ItemGeo<D, S, false>;
   constexpr int MAXI = (TABN - 2) / 2;
-  const int c = blockIdx.x;
+  const int c = vc;
   const uint64_t pol = policy_evict_first();
   int sg = 0, uix = 0;
   auto publish = [&](int u, int n_u, int lo0, int len0, int rl, int nslots, int lo4, int len4, int nst4) {
@@ -432,13 +432,17 @@ WQ_DEV void peer_exchange_merge(const DecodeArgs &a, int tid, int u, int b, int 
     const uint32_t *my = reinterpret_cast<const uint32_t *>(a.peer_bufs[r] + ctr_off) + u;
     const uint32_t want = (uint32_t)G * a.peer_epoch;
     // bounded wait (10 s of globaltimer): a peer that never arrives (a rank that skipped
-    // the call, a broken mapping) must not hang the GPU; the result is then invalid
+    // the call, a broken mapping) must not hang the GPU; the result is then invalid.
+    // The error word after the counters (wq_peer_error_offset) is polled too: once any
+    // wait of this rank timed out, every later wait gives up at once instead of burning
+    // another 10 s per unit and call.
+    uint32_t *err = const_cast<uint32_t *>(my) - u + a.B * a.H;
     const uint64_t t0 = gtime();
     while ((int32_t)(ld_acquire_sys(my) - want) < 0) {
       __nanosleep(64);
+      if (ld_acquire_sys(err) != 0u) break;
       if (gtime() - t0 > 10000000000ull) {
-        // error word after the counters: the host checks it (wq_peer_status)
-        atomicExch(const_cast<uint32_t *>(my) - u + a.B * a.H, 1u);
+        atomicExch(err, 1u);
         break;
       }
     }
@@ -470,8 +474,10 @@ size_t peer_buffer_bytes(int B, int H, int Hq, int d, int G) {
   return 2ull * G * B * Hq * (d + 2) * sizeof(float) + (((size_t)(B * H + 1) * sizeof(uint32_t) + 255) / 256) * 256;
 }
 
+// The kernel body; vc / vn = this CTA's index and the CTA count it plans with
+// (blockIdx.x / gridDim.x, or a virtual rank's share of the grid under emulation).
 template <int D, int S, bool UR>
-__global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
+WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
   using SM = DecodeSmem<D, S>;
   constexpr int KT = D / 16;
   constexpr int NST = SM::NST;
@@ -488,12 +494,12 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int U = a.B * a.H;
   // timestamps only in profiling builds (WQ_DEC_PROFILE=1, tools/dbg_decode_time.py)
-  uint64_t *ts = (WQ_DEC_PROFILE && a.ws_ts) ? a.ws_ts + (size_t)blockIdx.x * TS_PER_CTA : nullptr;
+  uint64_t *ts = (WQ_DEC_PROFILE && a.ws_ts) ? a.ws_ts + (size_t)vc * TS_PER_CTA : nullptr;
   if (ts && tid == 0) ts[0] = gtime();
 
   // ---- prologue (warp 0): unit cost prefix, then this CTA's share ----
   CtaPlan *cp = reinterpret_cast<CtaPlan *>(sm + SM::plan_off);
-  if (warp == 0) plan_cta<D, S, false, (!UR && WQ_DEC_STREAM)>(a, ustart, cp, s_flag, lane);
+  if (warp == 0) plan_cta<D, S, false, (!UR && WQ_DEC_STREAM)>(a, ustart, cp, s_flag, lane, vc, vn);
   if (tid == 32) {
     for (int s = 0; s < NST; s++) {
       mbar_init(&full[s], 1);
@@ -505,21 +511,20 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   }
   __syncthreads();
   const int G = *s_flag;
-  const int c = blockIdx.x;
+  const int c = vc;
   // the next launch on the stream may start its prologue and cache prefetch as soon
   // as SMs free up (it waits for this grid before touching q / outputs: PDL)
   if (tid == 0) griddep_launch_dependents();
   if (c >= G) return;
-  if (a.debug & 32) return;                       // debug: launch + prologue only
   if (ts && tid == 0) { ts[1] = gtime(); ts[70] = clock64(); }
 
   if (warp == NCW) {
     // =========================== producer ===========================
     if constexpr (UR) {
       if (lane == 0) produce_ur<D, S, STAGE, NST, SM::NUS, SM::TABN>(a, *cp, ring, full, empty, ent, units_done,
-                                                                      reinterpret_cast<int *>(sm + SM::tab_off));
+                                                                      reinterpret_cast<int *>(sm + SM::tab_off), vc);
     } else {
-      if (lane == 0) produce<D, S, false, STAGE, NST, SM::NUS>(a, *cp, ustart, ring, full, empty, ent, units_done, ts);
+      if (lane == 0) produce<D, S, false, STAGE, NST, SM::NUS>(a, *cp, ustart, ring, full, empty, ent, units_done, ts, vc);
     }
     return;
   }
@@ -621,9 +626,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
         for (; nxt < kbase + n; nxt += NCW) {
           const int k = nxt - kbase;
           const uint8_t *rec = sbase + (size_t)k * sz;
-          if (a.debug & 1) {
-            st.l[0] += (float)lds32(rec + 16 * lane);
-          } else if (p == 0) {
+          if (p == 0) {
             do_window<D, S, 2>(rec, qs, a.scale_log2, st, o, scratch, lane);
           } else if (p == 1) {
             do_window<D, S, 4>(rec, qs, a.scale_log2, st, o, scratch, lane);
@@ -656,7 +659,7 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
       st.vb[0] += __shfl_xor_sync(0xffffffffu, st.vb[0], off);
       st.vb[1] += __shfl_xor_sync(0xffffffffu, st.vb[1], off);
     }
-    if (!(a.debug & 16)) {
+    {
       float *mine = ep + warp * SM::EPW;
 #pragma unroll
       for (int mt = 0; mt < KT; mt++) {
@@ -673,10 +676,6 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
     }
     named_bar_sync(1, NCW * 32);
     uidx++;
-    if (a.debug & 16) {                           // debug: no epilogue
-      if (tid == 0) atomicAdd(units_done, 1);
-      continue;
-    }
     // (2) CTA merge: per head j, M = max_w m_w, weights f_w = 2^(m_w - M) (written over
     // m_w), L = sum f_w l_w, VB = sum f_w vb_w; then per output (j, cc):
     // O = VB + sum_w f_w o_w[j][cc]
@@ -748,6 +747,29 @@ __global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
   }
 }
 
+template <int D, int S, bool UR>
+__global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
+  decode_body<D, S, UR>(a, (int)blockIdx.x, (int)gridDim.x);
+}
+
+// Fused cross-GPU merge emulated on ONE device in ONE launch (tests): the grid is split
+// into NR equal shares, share r plays rank r with its own arguments (image shard, rest,
+// workspace, out) and exchanges its partials through the NR "peer" buffers exactly as
+// wq_decode_attention_peer does across GPUs: peer stores, system-scope release/acquire
+// counters, the bounded wait and the LSE merge.  All CTAs are co-resident (1 CTA/SM,
+// grid <= SMs), so every wait is satisfied by CTAs of the same launch.
+template <int NR>
+struct DecodeArgsN {
+  DecodeArgs r[NR];
+};
+template <int D, int S, int NR>
+__global__ void __launch_bounds__(DT, 1) k_decode_emu(const __grid_constant__ DecodeArgsN<NR> s) {
+  const int per = (int)gridDim.x / NR;
+  const int rk = (int)blockIdx.x / per;
+  if (rk >= NR) return;
+  decode_body<D, S, false>(s.r[rk], (int)blockIdx.x - rk * per, per);
+}
+
 __global__ void k_merge(const float *__restrict__ parts, int G, int BHq, int d, __half *__restrict__ out) {
   const int row = blockIdx.x;
   for (int cc = threadIdx.x; cc < d; cc += blockDim.x) {
@@ -786,6 +808,15 @@ static cudaError_t launch_decode_t(const DecodeArgs &a, int num_sms, cudaStream_
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  if (a.peer_bufs) {
+    // the exchange waits on partials written by other CTAs of this grid's peers: every CTA
+    // must be resident at once (one per SM) or a waiting CTA could starve one not yet
+    // scheduled on a peer
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode<D, S, UR>, DT, SM::total);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1 || num_sms > device_sm_count()) return cudaErrorCooperativeLaunchTooLarge;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms);
   cfg.blockDim = dim3(DT);
@@ -805,13 +836,43 @@ cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st) {
   // WQ_DECODE_TC=1 (head dim 128): the tcgen05/TMEM kernel of decode_tc.cu instead of
   // this file's mma.sync kernel.  Parity-clean but ~4x slower on C5 (its dequantization
   // warps are issue/latency bound), so it is opt-in.
+  // (The tcgen05 kernel has no peer exchange: the fused-merge path always runs here.)
   static const bool use_tc = getenv("WQ_DECODE_TC") && atoi(getenv("WQ_DECODE_TC")) != 0;
-  if (a.d == 128 && use_tc && !a.woff) return launch_decode_tc(a, num_sms, st);
+  if (a.d == 128 && use_tc && !a.woff && !a.peer_bufs) return launch_decode_tc(a, num_sms, st);
 #define WQ_D(DD, SS) \
   if (a.d == DD && a.S == SS) return a.woff ? launch_decode_t<DD, SS, true>(a, num_sms, st) : launch_decode_t<DD, SS, false>(a, num_sms, st);
   WQ_D(64, 16) WQ_D(64, 32) WQ_D(64, 64) WQ_D(64, 128)
   WQ_D(128, 16) WQ_D(128, 32) WQ_D(128, 64) WQ_D(128, 128)
 #undef WQ_D
+  return cudaErrorInvalidValue;
+}
+
+template <int D, int S>
+static cudaError_t launch_emu_t(const DecodeArgs *ra, int nr, int num_sms, cudaStream_t st) {
+  using SM = DecodeSmem<D, S>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_decode_emu<D, S, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SM::total);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (nr != 2) return cudaErrorInvalidValue;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_emu<D, S, 2>, DT, SM::total);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+  DecodeArgsN<2> s;
+  s.r[0] = ra[0];
+  s.r[1] = ra[1];
+  k_decode_emu<D, S, 2><<<(num_sms / 2) * 2, DT, SM::total, st>>>(s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_emu(const DecodeArgs *ra, int nr, int num_sms, cudaStream_t st) {
+  const DecodeArgs &a = ra[0];
+  if (a.d == 128 && a.S == 32) return launch_emu_t<128, 32>(ra, nr, num_sms, st);
+  if (a.d == 64 && a.S == 16) return launch_emu_t<64, 16>(ra, nr, num_sms, st);
   return cudaErrorInvalidValue;
 }
 

@@ -1,5 +1,6 @@
 // decode_common.cuh -- the split-KV work partition shared by the two decode kernels
-// (decode.cu: mma.sync, d = 64; decode_tc.cu: tcgen05/TMEM, d = 128): item geometry
+// (decode.cu: mma.sync, the default for d = 64 and 128; decode_tc.cu: tcgen05/TMEM,
+// d = 128, opt-in WQ_DECODE_TC=1): item geometry
 // and cost model, the per-CTA plan computed in the prologue, the TMA producer that
 // streams a CTA's items into the shared-memory ring, and the log-sum-exp merge of a
 // split unit's CTA partials (Q24; Eq.12-13 P:462-473 make any split exact).
@@ -149,8 +150,10 @@ struct CtaPlan {
 // units laid end to end, each unit's cost preceded by a fixed entry overhead EOV (its
 // epilogue: a CTA that ends one unit and starts the next runs two), so every CTA gets
 // the same cost; a unit-aligned split rounds each unit to a whole number of CTAs.
+// vc / vn: this CTA's index and the CTA count of the grid it plans over (blockIdx.x /
+// gridDim.x, or a virtual rank's share of one grid in the fused-merge emulation).
 template <int D, int S, bool TC, bool STREAM = false>
-WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_flag, int lane) {
+WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_flag, int lane, int vc, int vn) {
   const int U = a.B * a.H;
   int64_t carry = 0;
   UnitGeo gg;                                   // this lane's unit of the last chunk
@@ -176,8 +179,8 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
   __syncwarp();
   const int64_t T = carry;
   int G = (int)(T / MIN_CTA_BYTES);
-  G = G < 1 ? 1 : (G > (int)gridDim.x ? (int)gridDim.x : G);
-  const int c = blockIdx.x;
+  G = G < 1 ? 1 : (G > vn ? vn : G);
+  const int c = vc;
   if (U >= G || T <= 0) {
     // whole units to the CTA owning their cost midpoint: a contiguous unit range
     int ua = 0, ub = 0;
@@ -244,11 +247,10 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
 // entries published in a ring of NUS Entry slots, released via *units_done.
 template <int D, int S, bool TC, int STAGE, int NST, int NUS>
 WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart, uint8_t *ring,
-                    uint64_t *full, uint64_t *empty, Entry *ent, int *units_done, uint64_t *ts) {
+                    uint64_t *full, uint64_t *empty, Entry *ent, int *units_done, uint64_t *ts, int vc) {
   using IG = ItemGeo<D, S, TC>;
-  const int c = blockIdx.x;
+  const int c = vc;
   const uint64_t pol = policy_evict_first();
-  const bool nocopy = (a.debug & 2) != 0;
   if (ts) ts[62] = gtime();
   int sg = 0;                                  // stage number of this CTA
   int uix = 0;                                 // entry number of this CTA
@@ -328,9 +330,7 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
         mbar_wait_sleep(&empty[slot], (fill & 1) ^ 1, 64);
         if (ts && sg < 64) ts[72 + sg] = clock64();
         uint8_t *dst = ring + (size_t)slot * STAGE;
-        if (nocopy) {
-          mbar_arrive(&full[slot]);
-        } else if (p < 4) {
+        if (p < 4) {
           const uint32_t nb = (uint32_t)(f1 - f0) * IG::sz(p);
           mbar_arrive_expect_tx(&full[slot], nb);
           bulk_g2s_evict_first(dst, img + gg.cs[p] + (int64_t)(f0 - gg.so[p]) * IG::sz(p), nb, &full[slot], pol);

@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(NT, 1) k_decode_tc(DecodeArgs a) {
   auto stamp = [&](int jj, int ev) { if (ts && jj < PROF_G) ts[10 + 5 * jj + ev] = clock64(); };
   if (ts && tid == 0) ts[0] = clock64();
 
-  if (warp == 0) plan_cta<D, S, true>(a, ustart, cp, s_flag, lane);
+  if (warp == 0) plan_cta<D, S, true>(a, ustart, cp, s_flag, lane, (int)blockIdx.x, (int)gridDim.x);
   if (tid == 32) {
     for (int s = 0; s < NST; s++) {
       mbar_init(&full[s], 1);
@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(NT, 1) k_decode_tc(DecodeArgs a) {
   const uint32_t tmem = *s_tmem;
 
   if (warp == W_PROD) {
-    if (lane == 0) produce<D, S, true, STAGE, NST, C::NUS>(a, *cp, ustart, ring, full, empty, ent, units_done, nullptr);
+    if (lane == 0) produce<D, S, true, STAGE, NST, C::NUS>(a, *cp, ustart, ring, full, empty, ent, units_done, nullptr,
+                                                           (int)blockIdx.x);
     return;
   }
 

@@ -44,13 +44,12 @@ struct DecodeArgs {
   int R_max;
   int B, H, Hq, grp, d, S;
   float scale_log2;          // sm_scale * log2(e)
-  int debug;                 // WQ_DECODE_DEBUG: 1 = stream only (no math), profiling aid
   uint32_t flags;            // WQ_DECODE_* flags (include/wq.h)
   __half *out;
   float *partial;
   float *ws_part;            // [(G + B*H)][grp][d + 2]
   int32_t *ws_cnt;           // [B*H]
-  uint64_t *ws_ts;           // [num_sms][8] timestamps when debug & 8, else NULL
+  uint64_t *ws_ts;           // [num_sms][TS_PER_CTA] timestamps (profiling builds, WQ_DECODE_DEBUG & 8), else NULL
   const int64_t *woff;       // non-NULL: unreordered image, window offsets [B][W+1]
   // fused cross-GPU LSE merge; peer_bufs NULL: off
   uint8_t *const *peer_bufs; // device array [G] of the ranks' symmetric buffers (IPC-mapped)
@@ -62,6 +61,8 @@ size_t peer_buffer_bytes(int B, int H, int Hq, int d, int G);
 size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms);
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st);
 cudaError_t launch_decode_tc(const DecodeArgs &a, int num_sms, cudaStream_t st);   // d = 128
+// nr virtual ranks of the fused peer merge in one launch (tests; nr = 2, (d, S) = (128, 32) / (64, 16))
+cudaError_t launch_decode_emu(const DecodeArgs *ra, int nr, int num_sms, cudaStream_t st);
 cudaError_t launch_merge(const float *parts, int G, int BHq, int d, __half *out, cudaStream_t st);
 
 cudaError_t launch_dequant_layout(const int32_t *seg_off, int B, int H, int d, int S, int32_t *seg16, int64_t *offs16,

@@ -79,6 +79,8 @@ def load(build_if_missing: bool = True):
         "wq_peer_error_offset": [C.POINTER(Geom), I32, P],
         "wq_decode_attention_peer": [P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, SZ, P, P, I32, I32,
                                      C.c_uint32, P],
+        "wq_decode_attention_peer_emulated": [I32, P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, SZ, P,
+                                              P, C.c_uint32, P],
         "wq_unreorder_image": [P, P, P, P, C.POINTER(Geom), P, P, P],
         "wq_decode_attention_unreordered": [P, P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, P, SZ, P],
     }
@@ -100,7 +102,7 @@ def exported_symbols():
             "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_dequant_layout", "wq_dequantize_image",
             "wq_unreordered_layout", "wq_unreorder_image", "wq_decode_attention_unreordered",
             "wq_peer_buffer_bytes", "wq_peer_error_offset", "wq_decode_attention_peer",
-            "wq_last_error", "wq_version"]
+            "wq_decode_attention_peer_emulated", "wq_last_error", "wq_version"]
 
 
 def _check(rc: int):
@@ -339,3 +341,20 @@ def wq_peer_error_offset(g: Geom, G: int) -> int:
     n = C.c_size_t(0)
     _check(load().wq_peer_error_offset(C.byref(g), int(G), C.byref(n)))
     return n.value
+
+
+def wq_decode_attention_peer_emulated(ranks, g: Geom, sm_scale: float, peer_ptrs: torch.Tensor, local_ptrs, epoch: int,
+                                      stream=None):
+    """G = 2 virtual ranks of wq_decode_attention_peer in ONE launch on one GPU (tests of
+    the fused cross-GPU merge without a second device).  ranks: list of G dicts with the
+    keys q, packed, offs, seg_off, k_rest, v_rest, rest_len, out, workspace (tensors)."""
+    G = len(ranks)
+    arr = lambda key: (C.c_void_p * G)(*[ranks[r][key].data_ptr() for r in range(G)])
+    kr = ranks[0]["k_rest"]
+    R_max = kr.shape[2]
+    rs = (C.c_int64 * 2)(*(kr.stride(0), kr.stride(1)))
+    loc = (C.c_void_p * G)(*[int(x) for x in local_ptrs])
+    _check(load().wq_decode_attention_peer_emulated(
+        G, arr("q"), arr("packed"), arr("offs"), arr("seg_off"), C.byref(g), arr("k_rest"), arr("v_rest"), rs,
+        arr("rest_len"), R_max, float(sm_scale), arr("out"), arr("workspace"), ranks[0]["workspace"].numel(),
+        _ptr(peer_ptrs), loc, C.c_uint32(epoch), _stream(stream)))

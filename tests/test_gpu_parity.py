@@ -464,6 +464,48 @@ def test_peer_merge_single_rank(orc):
         pm.close()
 
 
+@pytest.mark.parametrize("d,S,W,tail,B,H,Hq", [(128, 32, 40, 7, 2, 4, 28), (64, 16, 30, 5, 3, 2, 14)])
+def test_peer_merge_two_rank_emulation(orc, d, S, W, tail, B, H, Hq):
+    """The G = 2 exchange of the fused cross-GPU merge, executed: two virtual ranks share
+    one launch (half of the SMs each), each decodes its wq_shard_slots shard of the
+    sequence split and exchanges its (m, l, o) rows with the other through the two
+    symmetric buffers (peer stores, red.release.sys counters, ld.acquire.sys wait, LSE
+    merge).  Over several epochs (both buffer parities) both ranks' merged outputs equal
+    each other, stay within 2e-3 of the oracle's unsplit attention, and no wait times out."""
+    c = small_case(600 + d + S, d=d, S=S, W=W, tail=tail, B=B, H=H, Hq=Hq)
+    g = c["g"]
+    sc = wq.wq_window_scores(c["vis"], c["txt"], S)
+    thr = orc.thresholds([0.45], 2.0, 4)
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 1, g)
+    sm = 1 / math.sqrt(d)
+    offs, packed, full, _ = run_layer(g, c["K"], c["V"], c["kr"], c["vr"], c["rest_len"], perm[0], seg[0], c["q"], sm)
+    ref = _decode_ref(orc, c, g, offs, packed, perm[0], seg[0], sm)[0]
+    ranks = []
+    for r in range(2):
+        pr, sr = wq.wq_shard_slots(perm[0], seg[0], 2, r)
+        rl = c["rest_len"] if r == 0 else torch.zeros_like(c["rest_len"])
+        o_r = wq.wq_layer_layout(g, sr)
+        pk = torch.zeros(int(o_r[-1].item()) + 16, dtype=torch.uint8, device="cuda")
+        wq.wq_reorder_quantize_pack(c["K"], c["V"], 0, g, pr, sr, o_r, pk)
+        ranks.append(dict(q=c["q"], packed=pk, offs=o_r, seg_off=sr.contiguous(), k_rest=c["kr"], v_rest=c["vr"],
+                          rest_len=rl, out=torch.zeros_like(full),
+                          workspace=torch.zeros(wq.wq_decode_workspace(g), dtype=torch.uint8, device="cuda")))
+    nb = wq.wq_peer_buffer_bytes(g, 2)
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    err_off = wq.wq_peer_error_offset(g, 2)
+    for epoch in (1, 2, 3, 4):
+        for rk in ranks:
+            rk["out"].zero_()
+        wq.wq_decode_attention_peer_emulated(ranks, g, sm, ptrs, [b.data_ptr() for b in bufs], epoch)
+        torch.cuda.synchronize()
+        for r in range(2):
+            assert int(bufs[r][err_off:err_off + 4].view(torch.int32).item()) == 0, "peer wait timed out"
+        assert torch.equal(ranks[0]["out"], ranks[1]["out"])
+        assert rel_err(ranks[0]["out"].float().cpu().numpy(), ref) <= ATTN_TOL
+        assert rel_err(ranks[0]["out"].float().cpu().numpy(), full.float().cpu().numpy()) <= ATTN_TOL
+
+
 def _peer_ipc_worker(rank, world, port, q):
     import os
     import torch.distributed as dist

@@ -385,6 +385,55 @@ def test_quantizer_scale_values(orc):
     assert np.array([s], np.uint16).view(np.float16)[0] == np.float16(1312 * 2 ** -15)
 
 
+SZ = [
+    # Q17 mn = IEEE 754-2019 minimum (section 9.6: -0 < +0), independent of element order
+    ([0x0000, 0x8000, 0x3C00, 0x4000], 0x8000),       # [+0, -0, 1, 2] -> mn = -0
+    ([0x8000, 0x0000, 0x3C00, 0x4000], 0x8000),       # [-0, +0, 1, 2] -> mn = -0
+    ([0x3C00, 0x0000, 0x4000, 0x8000], 0x8000),       # -0 last
+    ([0x0000, 0x0000, 0x3C00], 0x0000),               # only +0 -> +0
+    ([0x8000, 0x8000, 0x3C00], 0x8000),               # only -0 -> -0
+    ([0x0000, 0x8000, 0xBC00], 0xBC00),               # a negative value below both zeros
+    ([0x8000, 0x0000], 0x8000),                       # all zeros: mn = -0, codes 0
+]
+
+
+@pytest.mark.parametrize("bits16,mn_bits", SZ)
+def test_quantizer_signed_zero_minimum(orc, bits16, mn_bits):
+    """Reading Q17 fixes mn as the IEEE 754-2019 minimum, so a group whose minimum is a
+    zero stores the sign bit of -0 iff a -0 is present (both element orders give the
+    same bytes); zeros of either sign get code 0 and dequantize to a zero."""
+    x = np.array(bits16, np.uint16).view(np.float16)
+    for bits in (2, 4, 8):
+        s, mn, c = orc.quantize_group(x, bits)
+        assert mn == mn_bits, (bits16, hex(mn))
+        for i, v in enumerate(bits16):
+            if v in (0x0000, 0x8000):
+                assert c[i] == (0 if mn_bits in (0x0000, 0x8000) else c[i])
+        sv = float(np.array([s], np.uint16).view(np.float16)[0])
+        mv = float(np.array([mn], np.uint16).view(np.float16)[0])
+        assert np.all(np.abs(x.astype(np.float64) - (mv + sv * c)) <= sv * (0.5 + 2 ** -14))
+
+
+def test_quantizer_degenerate_groups(orc):
+    """Edge groups: a constant group takes the 2^-24 scale floor (Q21) and every code is 0;
+    values at the fp16 extremes +-65504 give s = RU(131008 / q_max) exactly (closed form)
+    and the codes 0 / q_max at the ends; a range of one subnormal step is a subnormal scale."""
+    for bits in (2, 4, 8):
+        qmax = 2 ** bits - 1
+        s, mn, c = orc.quantize_group(np.full(32, -3.25, np.float16), bits)
+        assert s == 0x0001 and np.all(c == 0)
+        x = np.array([65504, -65504, 0, 1, -1], np.float16)
+        s, mn, c = orc.quantize_group(x, bits)
+        sv = float(np.array([s], np.uint16).view(np.float16)[0])
+        exact = 131008.0 / qmax
+        # RU to fp16: the smallest fp16 >= fl32(131008 / q_max)
+        assert sv >= np.float32(exact) and float(np.nextafter(np.float16(sv), np.float16(0))) < np.float32(exact)
+        assert mn == 0xFBFF and c[0] == qmax and c[1] == 0
+        x = np.array([2 ** -24, 0, 2 ** -24, 0], np.float16)     # range = one subnormal step
+        s, mn, c = orc.quantize_group(x, bits)
+        assert s == 0x0001 and list(c) == [1, 0, 1, 0]
+
+
 @pytest.mark.parametrize("bits", [2, 4, 8])
 def test_quantizer_error_bound_and_monotone(orc, bits):
     """North star: |x - x^| <= s/2 (Q17 guarantees s*(1/2 + 2^-14)); codes monotone;

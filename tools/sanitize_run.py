@@ -1,0 +1,73 @@
+"""C1-sized run of every libwq device call, for compute-sanitizer (tests/test_gpu_sanitize.py):
+scores (cosine, Pearson), rank + assign (budget and vote), layout, quantize, decode
+(flags 0, then a PDL-chained WQ_DECODE_EARLY decode, and partials), merge, shard,
+the unfused (T9) and unreordered (T8) baselines and the two-rank fused-merge emulation.
+Exits 0 when every call returned WQ_OK; the sanitizer reports hazards itself."""
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2605_02262_b200 import configs, synth, wq  # noqa: E402
+
+
+def main():
+    wq.load(build_if_missing=False)
+    cfg = configs.CONFIGS["C1"]
+    m = cfg.model
+    dev = "cuda"
+    vis, txt = synth.embeddings(cfg.B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, dev)
+    sc = wq.wq_window_scores(vis, txt, cfg.S)
+    wq.wq_window_scores(vis, txt, cfg.S, metric=wq.WQ_SIM_PEARSON)
+    g = wq.geom(cfg.B, m.H, m.Hq, m.d, cfg.M, cfg.S, (2, 4, 8, 16))
+    thr = wq.wq_thresholds([0.5, 0.3], 2.0, 4)
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 2, g, wq.AssignOpts(4.5, 1, 1))
+    bits, rank, perm, seg = wq.wq_assign_bits(sc, thr, 2, g, wq.AssignOpts(0.0, 1, 0))
+    K, V, kr, vr, rest_len = synth.layer_tensors(cfg, 0, dev)
+    q = synth.queries(cfg.B, m.Hq, m.H, m.d, cfg.seed, 0, device=dev)
+    sm = 1 / math.sqrt(m.d)
+    offs = wq.wq_layer_layout(g, seg[0])
+    packed = torch.zeros(int(offs[-1].item()) + 16, dtype=torch.uint8, device=dev)
+    wq.wq_reorder_quantize_pack(K, V, 0, g, perm[0], seg[0], offs, packed)
+    out = torch.empty((cfg.B, m.Hq, m.d), dtype=torch.float16, device=dev)
+    part = torch.empty((cfg.B, m.Hq, m.d + 2), dtype=torch.float32, device=dev)
+    ws = torch.zeros(wq.wq_decode_workspace(g), dtype=torch.uint8, device=dev)
+    wq.wq_decode_attention(q, packed, offs, seg[0], g, kr, vr, rest_len, sm, out=out, partial=part, workspace=ws)
+    wq.wq_decode_attention(q, packed, offs, seg[0], g, kr, vr, rest_len, sm, out=out, workspace=ws,
+                           flags=wq.WQ_DECODE_EARLY)
+    wq.wq_merge_partials(torch.stack([part, part]), g)
+    pr, sr = wq.wq_shard_slots(perm[0], seg[0], 2, 1)
+    seg16, offs16 = wq.wq_dequant_layout(g, seg[0])
+    img16 = torch.zeros(int(offs16[-1].item()) + 16, dtype=torch.uint8, device=dev)
+    wq.wq_dequantize_image(packed, offs, seg[0], g, offs16, img16)
+    woff = wq.wq_unreordered_layout(g, bits[0].contiguous())
+    uimg = torch.zeros_like(packed)
+    wq.wq_unreorder_image(packed, offs, seg[0], perm[0], g, woff, uimg)
+    wq.wq_decode_attention_unreordered(q, uimg, offs, seg[0], woff, g, kr, vr, rest_len, sm, out=out)
+    # fused merge, two virtual ranks in one launch (d = 64 needs S = 16 here)
+    g16 = wq.geom(cfg.B, m.H, m.Hq, m.d, cfg.M, 16, (2, 4, 8, 16))
+    sc16 = wq.wq_window_scores(vis, txt, 16)
+    _, _, perm16, seg16b = wq.wq_assign_bits(sc16, thr[:1], 1, g16)
+    ranks = []
+    for r in range(2):
+        p_r, s_r = wq.wq_shard_slots(perm16[0], seg16b[0], 2, r)
+        o_r = wq.wq_layer_layout(g16, s_r)
+        pk = torch.zeros(int(o_r[-1].item()) + 16, dtype=torch.uint8, device=dev)
+        wq.wq_reorder_quantize_pack(K, V, 0, g16, p_r, s_r, o_r, pk)
+        ranks.append(dict(q=q, packed=pk, offs=o_r, seg_off=s_r.contiguous(), k_rest=kr, v_rest=vr,
+                          rest_len=rest_len if r == 0 else torch.zeros_like(rest_len), out=torch.zeros_like(out),
+                          workspace=torch.zeros(wq.wq_decode_workspace(g16), dtype=torch.uint8, device=dev)))
+    nb = wq.wq_peer_buffer_bytes(g16, 2)
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=dev)
+    for epoch in (1, 2):
+        wq.wq_decode_attention_peer_emulated(ranks, g16, sm, ptrs, [b.data_ptr() for b in bufs], epoch)
+    torch.cuda.synchronize()
+    print("sanitize_run: ok")
+
+
+if __name__ == "__main__":
+    main()
