@@ -13,8 +13,9 @@
  *  - The caller owns every buffer.  The library never allocates, frees or keeps
  *    a pointer after the call returns.  Scratch space comes from an explicit
  *    `workspace` argument whose size is returned by the matching *_workspace()
- *    query; workspaces must be zero-filled once after allocation (kernels leave
- *    them zeroed again on exit).
+ *    query; workspaces must be zero-filled once after allocation: the kernels
+ *    leave the synchronization counters in them zeroed again on exit (the rest
+ *    is scratch whose contents do not matter between calls).
  *  - Device calls are asynchronous on `stream` (a cudaStream_t passed as void*,
  *    NULL = legacy default stream).  Argument validation is synchronous: a call
  *    that returns anything but WQ_OK launched nothing, and wq_last_error()

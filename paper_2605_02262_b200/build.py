@@ -69,5 +69,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defs: str, force: bool = False) -> str:
+    """Build lib/<name>/libwq.so with extra nvcc defines (a separate process: the
+    variant is chosen by the environment at import).  E.g. the checked build:
+    build_variant("checked", "-DWQ_CHECKS=1") (tests/test_gpu_checked.py)."""
+    env = dict(os.environ, WQ_VARIANT=name, WQ_NVCC_DEFS=defs)
+    args = [sys.executable, "-m", "paper_2605_02262_b200.build"] + (["--force"] if force else [])
+    out = subprocess.check_output(args, env=env, cwd=ROOT, text=True)
+    return out.strip().splitlines()[-1]
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -186,7 +186,7 @@ wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t s
   if (strides[2] < g->d) return fail(WQ_ESHAPE, "token stride %lld < d=%d", (long long)strides[2], g->d);
   if (vis_off < 0) return fail(WQ_EINVAL, "vis_off=%d", vis_off);
   return cuda_status(wq::launch_quant((const __half *)k, (const __half *)v, strides, vis_off, g->B, g->H, g->d,
-                                      g->S, perm_l, perm_stride, seg_off_l, offs, packed, S_(stream)),
+                                      g->S, g->M, perm_l, perm_stride, seg_off_l, offs, packed, S_(stream)),
                      "quantize");
 }
 
@@ -255,16 +255,14 @@ static wq_status decode_args(const void *q, const uint8_t *packed, const int64_t
     a.out = nullptr;
     a.partial = reinterpret_cast<float *>(pc->local) + ((int64_t)(pc->epoch & 1u) * pc->G + pc->rank) * slotf;
   }
-  const int grp = a.grp;
-  size_t part = (size_t)(sms + g->B * g->H) * grp * (g->d + 2) * sizeof(float);
-  part = (part + 255) / 256 * 256;
+  const wq::DecodeWsLayout wl = wq::decode_ws_layout(g->B, g->H, g->d, sms);
   a.ws_part = reinterpret_cast<float *>(workspace);
-  a.ws_cnt = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(workspace) + part);
-  size_t cntb = ((size_t)g->B * g->H * sizeof(int32_t) + 255) / 256 * 256;
+  a.ws_cnt = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(workspace) + wl.part);
   // profiling builds only (WQ_DEC_PROFILE / WQ_TC_PROFILE): per-CTA timestamps when
   // WQ_DECODE_DEBUG has bit 3 set; the environment is read once per process
   static const int dbg = getenv("WQ_DECODE_DEBUG") ? atoi(getenv("WQ_DECODE_DEBUG")) : 0;
-  a.ws_ts = (dbg & 8) ? reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(workspace) + part + cntb) : nullptr;
+  a.ws_ts = (dbg & 8) ? reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(workspace) + wl.part + wl.cnt)
+                      : nullptr;
   return WQ_OK;
 }
 

@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(AT) k_assign(const double *__restrict__ scores
     if (w >= W) break;
     int k = cls_of(bits[w]);
     int slot = run[k]++;
+    WQ_CHECK(slot >= seg[k] && slot < seg[k + 1]);
     for (int bo = 0; bo < nb_out; bo++) {
       int bb = p.vote ? bo : b;
       int64_t row = (int64_t)l * B + bb;

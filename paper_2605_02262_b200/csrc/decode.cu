@@ -36,9 +36,12 @@ namespace wq {
 #define WQ_DEC_RING 163840
 #endif
 constexpr int NCW = WQ_DEC_NCW;                 // consumer warps
-constexpr int DT = (NCW + 1) * 32;      // threads per CTA
+constexpr int DT = (NCW + 1) * 32;      // threads per CTA: consumers + the producer warp
 #ifndef WQ_DEC_QLO
 #define WQ_DEC_QLO 1                     // carry q*s as fp16 hi + lo (0: hi only, experiment)
+#endif
+#ifndef WQ_EXP_NOZP
+#define WQ_EXP_NOZP 0                    // timing experiments only: skip the zero-point MMA (wrong values)
 #endif
 #ifndef WQ_DEC_PROFILE
 #define WQ_DEC_PROFILE 0                 // per-CTA timestamps into the workspace (debug & 8)
@@ -166,7 +169,7 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
         // {mn01, s01, mn89, s89}: the quad is the zero-point term's A fragment as
         // loaded (rows g: mn, rows g+8: don't-care -- only d0/d1 of b0/b1 are used)
         const uint4 pr = lds128(kp + (q * KT + kt) * 16);
-        if (c0 == 0) {
+        if (c0 == 0 && !WQ_EXP_NOZP) {
           const uint32_t am[4] = {pr.x, pr.y, pr.z, pr.w};
           if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
           else mma16816(b0, am, qk.x, qk.y, b0);
@@ -283,7 +286,8 @@ struct DecodeSmem {
   static constexpr int NST = (RING / STAGE) < 2 ? 2 : RING / STAGE;
   static constexpr int KT = D / 16;
   static constexpr int SCRATCH = 2 * 16 * 16;            // P' rows of one 2-tile chunk per warp
-  static constexpr int EPW = 8 * D + 24;                 // per warp: o [8][D], m[8], l[8], vb[8]
+  static constexpr int EPW = 8 * D + 24;                 // per warp: o [KT*32 groups][4], m[8], l[8], vb[8]
+  static constexpr int PSLOT = 16 + 8 * D;               // floats of a CTA partial in the workspace
   static constexpr int NUS = 4;                          // entry ring published by the producer
   static constexpr size_t ring = (size_t)NST * STAGE;
   static constexpr size_t scratch_off = ring;
@@ -297,8 +301,9 @@ struct DecodeSmem {
   // unreordered mode (UR): per ring slot the producer's item table {n, (offset, class) x n}
   static constexpr int MAXI = (int)(STAGE / (S * D / 2 + 4 * D + 4 * S));   // most records per stage
   static constexpr int TABN = 2 + 2 * MAXI;
-  static constexpr size_t tab_off = bar_off + 2 * NST * 8;
+  static constexpr size_t tab_off = bar_off + 2 * NST * 8;                    // full, empty barriers
   static constexpr size_t total = tab_off + (size_t)NST * TABN * 4;
+  static_assert(total <= 232448, "decode shared memory exceeds the 227 KB opt-in limit");
 };
 
 // Producer of the unreordered image (UR): a unit's windows are
@@ -368,6 +373,7 @@ WQ_DEV void produce_ur(const DecodeArgs &a, const CtaPlan &P, uint8_t *ring, uin
         }
       }
       const uint32_t nb = (uint32_t)(o[n] - o[0]);
+      WQ_CHECK(n >= 1 && nb <= (uint32_t)STAGE && a.offs[u] + o[n] <= a.offs[u + 1]);
       mbar_arrive_expect_tx(&full[slot], nb);
       bulk_g2s_evict_first(ring + (size_t)slot * STAGE, img + o[0], nb, &full[slot], pol);
       w += n;
@@ -625,6 +631,7 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
         const uint8_t *sbase = ring + (size_t)slot * STAGE;
         for (; nxt < kbase + n; nxt += NCW) {
           const int k = nxt - kbase;
+          WQ_CHECK(k < n && (k + 1) * sz <= STAGE);
           const uint8_t *rec = sbase + (size_t)k * sz;
           if (p == 0) {
             do_window<D, S, 2>(rec, qs, a.scale_log2, st, o, scratch, lane);
@@ -651,7 +658,9 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
     if (ts) t_loop += t_e0 - t_ls;
 
     // ---------------- entry epilogue ----------------
-    // (1) every warp parks (m, l, vb) per head and its o as [8 heads][D]
+    // (1) every warp parks its (m, l, vb) per head and its o fragments; o goes lane-
+    // interleaved in 16-byte groups (group gi = mt*32 + lane: the lane's o[mt][0..3],
+    // channels 16mt+g (+8), heads 2q, 2q+1), so parking and reading are conflict-free
 #pragma unroll
     for (int off = 4; off <= 16; off <<= 1) {
       st.l[0] += __shfl_xor_sync(0xffffffffu, st.l[0], off);
@@ -662,74 +671,82 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
     {
       float *mine = ep + warp * SM::EPW;
 #pragma unroll
-      for (int mt = 0; mt < KT; mt++) {
-        mine[(2 * q) * D + 16 * mt + g] = o[mt][0];
-        mine[(2 * q + 1) * D + 16 * mt + g] = o[mt][1];
-        mine[(2 * q) * D + 16 * mt + g + 8] = o[mt][2];
-        mine[(2 * q + 1) * D + 16 * mt + g + 8] = o[mt][3];
-      }
+      for (int mt = 0; mt < KT; mt++)
+        sts128(mine + (mt * 32 + lane) * 4, make_uint4(__float_as_uint(o[mt][0]), __float_as_uint(o[mt][1]),
+                                                      __float_as_uint(o[mt][2]), __float_as_uint(o[mt][3])));
       if (g == 0) {
-        mine[8 * D + 2 * q] = st.m[0]; mine[8 * D + 2 * q + 1] = st.m[1];
-        mine[8 * D + 8 + 2 * q] = st.l[0]; mine[8 * D + 8 + 2 * q + 1] = st.l[1];
-        mine[8 * D + 16 + 2 * q] = st.vb[0]; mine[8 * D + 16 + 2 * q + 1] = st.vb[1];
+        float *stt = mine + 8 * D;                 // [3][8]: m, l, vb per head
+        stt[2 * q] = st.m[0]; stt[2 * q + 1] = st.m[1];
+        stt[8 + 2 * q] = st.l[0]; stt[8 + 2 * q + 1] = st.l[1];
+        stt[16 + 2 * q] = st.vb[0]; stt[16 + 2 * q + 1] = st.vb[1];
       }
     }
     named_bar_sync(1, NCW * 32);
     uidx++;
-    // (2) CTA merge: per head j, M = max_w m_w, weights f_w = 2^(m_w - M) (written over
-    // m_w), L = sum f_w l_w, VB = sum f_w vb_w; then per output (j, cc):
-    // O = VB + sum_w f_w o_w[j][cc]
+    // (2) per head j (8 threads): M = max_w m_w, weights f_w = 2^(m_w - M), L = sum f_w l_w,
+    // VB = sum f_w vb_w into hw = [NCW][8] f, then [8] M, [8] L, [8] VB
     const bool split = (c1 - c0) > 1;
-    float *wslot = a.ws_part + (int64_t)(c + u) * grp * (D + 2);
-    float *hML = reinterpret_cast<float *>(sm + SM::scratch_off);      // [8] M, [8] L, [8] VB
-    if (tid < grp) {
+    float *hw = reinterpret_cast<float *>(sm + SM::scratch_off);
+    if (tid < 8) {
       const int j = tid;
+      float mw[NCW];
       float M = -INFINITY;
 #pragma unroll
-      for (int w = 0; w < NCW; w++) M = fmaxf(M, ep[w * SM::EPW + 8 * D + j]);
+      for (int w = 0; w < NCW; w++) {
+        mw[w] = ep[w * SM::EPW + 8 * D + j];
+        M = fmaxf(M, mw[w]);
+      }
       float L = 0.f, VB = 0.f;
 #pragma unroll
       for (int w = 0; w < NCW; w++) {
-        float *pw = ep + w * SM::EPW + 8 * D;
-        const float f = (M == -INFINITY) ? 0.f : exp2f(pw[j] - M);
-        pw[j] = f;
-        L = fmaf(f, pw[8 + j], L);
-        VB = fmaf(f, pw[16 + j], VB);
+        const float f = (M == -INFINITY) ? 0.f : ex2f(mw[w] - M);
+        hw[w * 8 + j] = f;
+        L = fmaf(f, ep[w * SM::EPW + 8 * D + 8 + j], L);
+        VB = fmaf(f, ep[w * SM::EPW + 8 * D + 16 + j], VB);
       }
-      hML[j] = M;
-      hML[8 + j] = L;
-      hML[16 + j] = VB;
+      hw[NCW * 8 + j] = M;
+      hw[NCW * 8 + 8 + j] = L;
+      hw[NCW * 8 + 16 + j] = VB;
     }
     named_bar_sync(1, NCW * 32);
-    for (int idx = tid; idx < grp * D; idx += NCW * 32) {
-      const int j = idx / D, cc = idx - j * D;
-      float O = hML[16 + j];
+    // (3) per 16-byte group: O = VB + sum_w f_w o_w; a split unit's CTA partial goes to
+    // its workspace slot ([8] (M, L) pairs, then the groups), a whole unit's straight out
+    float *wslot = a.ws_part + (int64_t)(c + u) * SM::PSLOT;
+    for (int gi = tid; gi < KT * 32; gi += NCW * 32) {
+      const int jq = 2 * (gi & 3);                 // heads jq, jq + 1
+      float4 O = make_float4(hw[NCW * 8 + 16 + jq], hw[NCW * 8 + 17 + jq], hw[NCW * 8 + 16 + jq],
+                             hw[NCW * 8 + 17 + jq]);
 #pragma unroll
-      for (int w = 0; w < NCW; w++) O = fmaf(ep[w * SM::EPW + 8 * D + j], ep[w * SM::EPW + j * D + cc], O);
-      const float M = hML[j], L = hML[8 + j];
-      if (split) {
-        if (cc == 0) { wslot[j * (D + 2)] = M; wslot[j * (D + 2) + 1] = L; }
-        wslot[j * (D + 2) + 2 + cc] = O;
-      } else {
-        const int64_t row = (int64_t)b * a.Hq + h * grp + j;
-        if (a.out) a.out[row * D + cc] = __float2half_rn(L > 0.f ? O / L : 0.f);
-        if (a.partial) {
-          float *pp = a.partial + row * (D + 2);
-          if (cc == 0) { pp[0] = M * 0.69314718055994530942f; pp[1] = L; }
-          pp[2 + cc] = O;
-        }
+      for (int w = 0; w < NCW; w++) {
+        const uint4 v = lds128(ep + w * SM::EPW + gi * 4);
+        const uint2 f = lds64(hw + w * 8 + jq);
+        O.x = fmaf(__uint_as_float(f.x), __uint_as_float(v.x), O.x);
+        O.y = fmaf(__uint_as_float(f.y), __uint_as_float(v.y), O.y);
+        O.z = fmaf(__uint_as_float(f.x), __uint_as_float(v.z), O.z);
+        O.w = fmaf(__uint_as_float(f.y), __uint_as_float(v.w), O.w);
       }
+      if (split) {
+        *reinterpret_cast<float4 *>(wslot + 16 + gi * 4) = O;
+      } else {
+        const float2 M2 = make_float2(hw[NCW * 8 + jq], hw[NCW * 8 + jq + 1]);
+        const float2 L2 = make_float2(hw[NCW * 8 + 8 + jq], hw[NCW * 8 + 9 + jq]);
+        write_group<D>(a, b, h, gi, O, M2, L2);
+      }
+    }
+    if (split && tid < 8) {
+      wslot[2 * tid] = hw[NCW * 8 + tid];
+      wslot[2 * tid + 1] = hw[NCW * 8 + 8 + tid];
     }
     const uint64_t t_e1 = ts ? clock64() : 0;
     if (split) {
-      // (3) ticket: the last CTA of the unit merges all CTA partials by log-sum-exp
+      // (4) ticket: the last CTA of the unit merges all CTA partials by log-sum-exp
       named_bar_sync(1, NCW * 32);
       // one acq_rel ticket: releases this CTA's partial (written by all threads before
       // the barrier) and, for the last CTA, acquires every other CTA's partial
       if (tid == 0) *s_flag = (atom_add_acq_rel_gpu(a.ws_cnt + u, 1) == c1 - c0 - 1);
       named_bar_sync(1, NCW * 32);
       if (ts && tid == 0) { ts[6] = *s_flag; ts[7] = c - c0; }
-      if (*s_flag) merge_unit<D, NCW * 32>(a, tid, u, b, h, c0, c1);
+      if (*s_flag) merge_unit<D, NCW * 32, SM::PSLOT>(a, tid, u, b, h, c0, c1);
     }
     if (a.peer_bufs && (!split || *s_flag)) peer_exchange_merge<D, NCW * 32>(a, tid, u, b, h);
     if (ts && tid == 0) {
@@ -790,12 +807,20 @@ __global__ void k_merge(const float *__restrict__ parts, int G, int BHq, int d, 
   }
 }
 
+// Workspace layout (wq_decode_workspace): CTA partial slots of 16 + 8d floats (k_decode;
+// >= grp * (d + 2), decode_tc's rows) for num_sms + B*H slots, then B*H ticket counters,
+// then the profiling timestamps; each region 256-byte aligned.
+DecodeWsLayout decode_ws_layout(int B, int H, int d, int num_sms) {
+  DecodeWsLayout L;
+  L.part = ((size_t)(num_sms + B * H) * (16 + 8 * (size_t)d) * sizeof(float) + 255) / 256 * 256;
+  L.cnt = ((size_t)B * H * sizeof(int32_t) + 255) / 256 * 256;
+  L.ts = (size_t)num_sms * TS_PER_CTA * sizeof(uint64_t);
+  return L;
+}
 size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms) {
-  const int grp = Hq / H;
-  size_t part = (size_t)(num_sms + B * H) * grp * (d + 2) * sizeof(float);
-  part = (part + 255) / 256 * 256;
-  size_t cnt = ((size_t)B * H * sizeof(int32_t) + 255) / 256 * 256;
-  return part + cnt + (size_t)num_sms * TS_PER_CTA * sizeof(uint64_t);
+  (void)Hq;
+  const DecodeWsLayout L = decode_ws_layout(B, H, d, num_sms);
+  return L.part + L.cnt + L.ts;
 }
 
 template <int D, int S, bool UR>

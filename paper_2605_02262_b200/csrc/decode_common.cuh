@@ -332,6 +332,9 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
         uint8_t *dst = ring + (size_t)slot * STAGE;
         if (p < 4) {
           const uint32_t nb = (uint32_t)(f1 - f0) * IG::sz(p);
+          WQ_CHECK(f0 >= gg.so[p] && f1 <= gg.so[p + 1] && nb <= (uint32_t)STAGE);
+          WQ_CHECK(img_off + gg.cs[p] + (int64_t)(f1 - gg.so[p]) * IG::sz(p) <= a.offs[a.B * a.H]);
+          WQ_CHECK(img_off + gg.cs[4] <= a.offs[u + 1]);
           mbar_arrive_expect_tx(&full[slot], nb);
           bulk_g2s_evict_first(dst, img + gg.cs[p] + (int64_t)(f0 - gg.so[p]) * IG::sz(p), nb, &full[slot], pol);
         } else {
@@ -341,6 +344,7 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
           const int r0 = 16 * (f0 - gg.nslots);
           const int r1 = min(gg.rl, 16 * (f1 - gg.nslots));
           const uint32_t nb = (uint32_t)(r1 - r0) * 2u * D;
+          WQ_CHECK(r0 >= 0 && r1 <= a.R_max && 2u * (uint32_t)cap * 32u * D <= (uint32_t)STAGE);
           mbar_arrive_expect_tx(&full[slot], 2 * nb);
           bulk_g2s_evict_first(dst, kr + (int64_t)r0 * D, nb, &full[slot], pol);
           bulk_g2s_evict_first(dst + cap * 32 * D, vr + (int64_t)r0 * D, nb, &full[slot], pol);
@@ -354,69 +358,85 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
   if (ts) ts[2] = gtime();
 }
 
-// ---- last-CTA merge of a split unit (NT threads, thread index tid) ----
-// Every output element: the np CTA partials' (m, l, o) in one batch of independent
-// loads, then the log-sum-exp combination in registers; writes out / partial.
-template <int D, int NT>
-WQ_DEV void merge_unit(const DecodeArgs &a, int tid, int u, int b, int h, int c0, int c1) {
-  const int grp = a.grp;
-  const int np = c1 - c0;
-  const int64_t stride = (int64_t)grp * (D + 2);
-  const float *pb = a.ws_part + (int64_t)(c0 + u) * stride;
-  constexpr int EPT = (8 * D + NT - 1) / NT;   // elements per thread (max)
-  float mM[EPT], mL[EPT], mO[EPT];
+// ---- outputs of one 16-byte group of a unit's merged result ----
+// Group gi = mt*32 + L (L = g*4 + q of the consumer fragment): channels 16mt + g, +8,
+// heads 2q, 2q + 1: O = (ch0, j0), (ch0, j1), (ch1, j0), (ch1, j1); M, L per head (log2
+// domain max, sum).  Writes out (fp16 O / L) and the ABI partial (m in natural log, l, o).
+template <int D>
+WQ_DEV void write_group(const DecodeArgs &a, int b, int h, int gi, float4 O, float2 M, float2 L) {
+  const int mt = gi >> 5, ln = gi & 31, gg = ln >> 2, jq = 2 * (ln & 3);
+  const int ch0 = 16 * mt + gg, ch1 = ch0 + 8;
+  const float ov[4] = {O.x, O.y, O.z, O.w};
 #pragma unroll
-  for (int e = 0; e < EPT; e++) { mM[e] = -INFINITY; mL[e] = 0.f; mO[e] = 0.f; }
-  constexpr int CHP = 4;                       // partials per load batch
-  for (int b0 = 0; b0 < np || b0 == 0; b0 += CHP) {
-    // (the common case np <= CHP is one pass with every load of the thread in flight)
-    float mv[EPT][CHP], lv[EPT][CHP], ov[EPT][CHP];
-#pragma unroll
-    for (int e = 0; e < EPT; e++) {
-      const int idx = tid + e * NT;
-      const int j = idx / D, cc = idx - j * D;
-      const bool ie = idx < grp * D;
-      const float *hb = pb + j * (D + 2);
-#pragma unroll
-      for (int i = 0; i < CHP; i++) {
-        const bool ok = ie && b0 + i < np;
-        mv[e][i] = ok ? __ldcg(hb + (b0 + i) * stride) : -INFINITY;
-        lv[e][i] = ok ? __ldcg(hb + (b0 + i) * stride + 1) : 0.f;
-        ov[e][i] = ok ? __ldcg(hb + (b0 + i) * stride + 2 + cc) : 0.f;
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < EPT; e++) {
-      float Mn = mM[e];
-#pragma unroll
-      for (int i = 0; i < CHP; i++) Mn = fmaxf(Mn, lv[e][i] > 0.f ? mv[e][i] : -INFINITY);
-      if (Mn != -INFINITY) {
-        const float r = exp2f(mM[e] - Mn);
-        mL[e] *= r;
-        mO[e] *= r;
-#pragma unroll
-        for (int i = 0; i < CHP; i++) {
-          const float f = lv[e][i] > 0.f ? exp2f(mv[e][i] - Mn) : 0.f;
-          mL[e] = fmaf(f, lv[e][i], mL[e]);
-          mO[e] = fmaf(f, ov[e][i], mO[e]);
-        }
-        mM[e] = Mn;
-      }
-    }
-    if (b0 + CHP >= np) break;
-  }
-#pragma unroll
-  for (int e = 0; e < EPT; e++) {
-    const int idx = tid + e * NT;
-    if (idx >= grp * D) continue;
-    const int j = idx / D, cc = idx - j * D;
-    const int64_t row = (int64_t)b * a.Hq + h * grp + j;
-    if (a.out) a.out[row * D + cc] = __float2half_rn(mL[e] > 0.f ? mO[e] / mL[e] : 0.f);
+  for (int e = 0; e < 4; e++) {
+    const int j = jq + (e & 1), ch = (e & 2) ? ch1 : ch0;
+    if (j >= a.grp) continue;
+    const float Lj = (e & 1) ? L.y : L.x, Mj = (e & 1) ? M.y : M.x;
+    const int64_t row = (int64_t)b * a.Hq + h * a.grp + j;
+    if (a.out) a.out[row * D + ch] = __float2half_rn(Lj > 0.f ? ov[e] / Lj : 0.f);
     if (a.partial) {
       float *pp = a.partial + row * (D + 2);
-      if (cc == 0) { pp[0] = mM[e] * 0.69314718055994530942f; pp[1] = mL[e]; }
-      pp[2 + cc] = mO[e];
+      if (ch == 0) { pp[0] = Mj * 0.69314718055994530942f; pp[1] = Lj; }
+      pp[2 + ch] = ov[e];
     }
+  }
+}
+
+// ---- last-CTA merge of a split unit (NT threads, thread index tid) ----
+// CTA partial slot (PSLOT floats): [8 heads] (M, L) pairs, then the 16-byte o groups.
+// One thread per group: the np partials' (M, L) of its two heads and its o group are
+// loaded 8 partials at a time (every load of a batch in flight at once: one L2 round
+// trip per batch), combined by log-sum-exp in registers, and written out.
+#ifndef WQ_DEC_MB
+#define WQ_DEC_MB 12                 // partials per load batch of the last-CTA merge (A/B: 12 > 8)
+#endif
+template <int D, int NT, int PSLOT>
+WQ_DEV void merge_unit(const DecodeArgs &a, int tid, int u, int b, int h, int c0, int c1) {
+  constexpr int NG = D * 2;                    // groups (KT * 32)
+  constexpr int MB = WQ_DEC_MB;
+  const int np = c1 - c0;
+  const float *pb = a.ws_part + (int64_t)(c0 + u) * PSLOT;
+  for (int gi = tid; gi < NG; gi += NT) {
+    const int jq = 2 * (gi & 3);
+    float2 M = make_float2(-INFINITY, -INFINITY), L = make_float2(0.f, 0.f);
+    float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p0 = 0; p0 < np; p0 += MB) {
+      float4 ml[MB], ov[MB];
+#pragma unroll
+      for (int i = 0; i < MB; i++) {
+        if (p0 + i < np) {
+          const float *ps = pb + (int64_t)(p0 + i) * PSLOT;
+          ml[i] = __ldcg(reinterpret_cast<const float4 *>(ps + 2 * jq));       // (M, L) of jq, jq + 1
+          ov[i] = __ldcg(reinterpret_cast<const float4 *>(ps + 16 + gi * 4));
+        } else {
+          ml[i] = make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
+          ov[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      float2 Mn = M;
+#pragma unroll
+      for (int i = 0; i < MB; i++) {
+        if (ml[i].y > 0.f) Mn.x = fmaxf(Mn.x, ml[i].x);
+        if (ml[i].w > 0.f) Mn.y = fmaxf(Mn.y, ml[i].z);
+      }
+      const float r0 = Mn.x == -INFINITY ? 0.f : ex2f(M.x - Mn.x);
+      const float r1 = Mn.y == -INFINITY ? 0.f : ex2f(M.y - Mn.y);
+      L.x *= r0; O.x *= r0; O.z *= r0;
+      L.y *= r1; O.y *= r1; O.w *= r1;
+#pragma unroll
+      for (int i = 0; i < MB; i++) {
+        const float f0 = ml[i].y > 0.f ? ex2f(ml[i].x - Mn.x) : 0.f;
+        const float f1 = ml[i].w > 0.f ? ex2f(ml[i].z - Mn.y) : 0.f;
+        L.x = fmaf(f0, ml[i].y, L.x);
+        L.y = fmaf(f1, ml[i].w, L.y);
+        O.x = fmaf(f0, ov[i].x, O.x);
+        O.y = fmaf(f1, ov[i].y, O.y);
+        O.z = fmaf(f0, ov[i].z, O.z);
+        O.w = fmaf(f1, ov[i].w, O.w);
+      }
+      M = Mn;
+    }
+    write_group<D>(a, b, h, gi, O, M, L);
   }
   if (tid == 0) a.ws_cnt[u] = 0;
 }

@@ -40,7 +40,7 @@ struct QuantArgs {
   const __half *k, *v;
   int64_t sb, sh, st;     // strides in elements (b, h, t); channel stride 1
   int vis_off;
-  int B, H, d, S;
+  int B, H, d, S, M;
   const int32_t *perm;
   int perm_stride;
   const int32_t *seg_off;
@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
       return;
     }
     const int w = a.perm[(int64_t)b * a.perm_stride + slot];
+    WQ_CHECK(w >= 0 && (int64_t)(w + 1) * S <= a.M && slot < a.perm_stride);
     // class of the slot and its record offset (branch-free: no local arrays)
     const int cls = (slot >= so_[1]) + (slot >= so_[2]) + (slot >= so_[3]);
     const int bits = class_bits(cls);
@@ -398,6 +399,7 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
       if (kk < cls) roff += (int64_t)(so_[kk + 1] - so_[kk]) * record_bytes(class_bits(kk), D, S);
     const int sbase = cls == 0 ? so_[0] : cls == 1 ? so_[1] : cls == 2 ? so_[2] : so_[3];
     roff += (int64_t)(slot - sbase) * record_bytes(bits, D, S);
+    WQ_CHECK(roff >= a.offs[(int64_t)b * a.H + h] && roff + record_bytes(bits, D, S) <= a.offs[(int64_t)b * a.H + h + 1]);
     wdesc[sl].roff = roff;
     wdesc[sl].bits = bits;
     const int64_t ro = b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
@@ -478,8 +480,10 @@ __global__ void k_shard_slots(const int32_t *__restrict__ perm, const int32_t *_
     start[k + 1] = start[k] + cnt[k];
   }
   for (int k = 0; k < 4; k++)
-    for (int i = threadIdx.x; i < cnt[k]; i += blockDim.x)
+    for (int i = threadIdx.x; i < cnt[k]; i += blockDim.x) {
+      WQ_CHECK(start[k] + i < W && lo[k] + i < so[k + 1]);
       perm_r[(int64_t)b * W + start[k] + i] = perm[(int64_t)b * W + lo[k] + i];
+    }
   if (threadIdx.x < 5) seg_r[5 * b + threadIdx.x] = start[threadIdx.x];
 }
 
@@ -497,10 +501,10 @@ cudaError_t launch_layer_layout(const int32_t *seg_off, int B, int H, int d, int
 }
 
 cudaError_t launch_quant(const __half *k, const __half *v, const int64_t strides[3], int vis_off,
-                         int B, int H, int d, int S, const int32_t *perm, int perm_stride,
+                         int B, int H, int d, int S, int M, const int32_t *perm, int perm_stride,
                          const int32_t *seg_off, const int64_t *offs, uint8_t *packed,
                          cudaStream_t st) {
-  QuantArgs a{k, v, strides[0], strides[1], strides[2], vis_off, B, H, d, S, perm, perm_stride,
+  QuantArgs a{k, v, strides[0], strides[1], strides[2], vis_off, B, H, d, S, M, perm, perm_stride,
               seg_off, offs, packed};
 #define WQ_Q(DD, SS) \
   if (d == DD && S == SS) return launch_quant_t<DD, SS>(a, st);

@@ -9,6 +9,27 @@
 
 #define WQ_DEV __device__ __forceinline__
 
+// Checked builds (-DWQ_CHECKS=1, tests/test_gpu_checked.py): device-side bounds checks on
+// every bulk copy, record write and permutation index of the path; a failed check prints
+// its condition and traps (the call then fails with a CUDA error).  Product builds compile
+// the checks out.
+#ifndef WQ_CHECKS
+#define WQ_CHECKS 0
+#endif
+#if WQ_CHECKS
+#include <cstdio>
+#define WQ_CHECK(cond)                                                                   \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("WQ_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,       \
+             (int)blockIdx.x, (int)threadIdx.x, #cond);                                  \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define WQ_CHECK(cond) do { } while (0)
+#endif
+
 namespace wq {
 
 // bits of width class k (segment order of a packed image, Alg.2)
@@ -300,6 +321,9 @@ WQ_DEV uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t magic) {
 // exactly; subtracting 2^(10-p) leaves the code (CENTER: subtracting
 // 2^(10-p) + 2^(BITS-1) leaves code - 2^(BITS-1), also exact).  Positions
 // p + BITS <= 10 only; higher slots use the word shifted right by 8.
+#ifndef WQ_EXP_NOSUB
+#define WQ_EXP_NOSUB 0     // timing experiments only (tools/ubench_window.cu): skip the HSUB2 of the
+#endif                     // dequantization on the K side (1), the V side (2) or both (3): wrong values
 template <int BITS, int J, bool CENTER = false>
 WQ_DEV uint32_t dq_pair(uint32_t w, uint32_t w8) {
   constexpr int SLOT_BITS = BITS * J;
@@ -312,6 +336,7 @@ WQ_DEV uint32_t dq_pair(uint32_t w, uint32_t w8) {
   constexpr uint32_t SUB1 = MAG1 | (CENTER ? (1u << (BITS - 1)) << P : 0u);
   constexpr uint32_t SUB = SUB1 | (SUB1 << 16);
   uint32_t x = lop3_and_or(HI ? w8 : w, MASK, MAG);
+  if constexpr ((WQ_EXP_NOSUB & (CENTER ? 2 : 1)) != 0) return x;
   return h2u(__hsub2(u2h(x), u2h(SUB)));
 }
 // 8-bit codes: bytes 0/2 (J = 0) or 1/3 (J = 1) under the exponent byte 0x64 -> 1024 + code
@@ -320,6 +345,7 @@ WQ_DEV uint32_t dq_pair8(uint32_t w) {
   uint32_t x;
   if constexpr (J == 0) asm("prmt.b32 %0, %1, %2, 0x7250;" : "=r"(x) : "r"(w), "r"(0x64646464u));
   else asm("prmt.b32 %0, %1, %2, 0x7351;" : "=r"(x) : "r"(w), "r"(0x64646464u));
+  if constexpr ((WQ_EXP_NOSUB & (CENTER ? 2 : 1)) != 0) return x;
   return h2u(__hsub2(u2h(x), u2h(CENTER ? 0x64806480u : 0x64006400u)));
 }
 

@@ -29,7 +29,7 @@ cudaError_t launch_layer_layout(const int32_t *seg_off, int B, int H, int d, int
 cudaError_t launch_shard_slots(const int32_t *perm, const int32_t *seg, int B, int W, int G, int r,
                                int32_t *perm_r, int32_t *seg_r, cudaStream_t st);
 cudaError_t launch_quant(const __half *k, const __half *v, const int64_t strides[3], int vis_off,
-                         int B, int H, int d, int S, const int32_t *perm, int perm_stride,
+                         int B, int H, int d, int S, int M, const int32_t *perm, int perm_stride,
                          const int32_t *seg_off, const int64_t *offs, uint8_t *packed,
                          cudaStream_t st);
 
@@ -58,6 +58,10 @@ struct DecodeArgs {
   __half *peer_out;          // out [B][Hq][d] of the merged result
 };
 size_t peer_buffer_bytes(int B, int H, int Hq, int d, int G);
+struct DecodeWsLayout {
+  size_t part, cnt, ts;      // bytes of the partial slots, the counters, the timestamps
+};
+DecodeWsLayout decode_ws_layout(int B, int H, int d, int num_sms);
 size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms);
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st);
 cudaError_t launch_decode_tc(const DecodeArgs &a, int num_sms, cudaStream_t st);   // d = 128

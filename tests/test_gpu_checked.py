@@ -1,0 +1,118 @@
+"""Memory-safety checks of the CUDA path without compute-sanitizer (closed on this pool):
+
+* the checked build (lib/checked/libwq.so, -DWQ_CHECKS=1) runs every device call of the
+  path on C1-sized inputs (tools/checked_run.py); every bulk copy, record write,
+  permutation index and shard index is bounds-checked on the device and a failed check
+  traps -- the run must finish cleanly;
+* guard zones: with the product library, every output buffer of the path is embedded
+  between 4 KiB canaries; after scores, assign, layout, quantize, decode (out + partial),
+  merge, shard, the T8/T9 baselines the canaries are intact and the decode workspace is
+  left ready for the next call (its counters re-zeroed, include/wq.h): repeated decodes
+  through the same workspace give identical outputs."""
+import math
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+from paper_2605_02262_b200 import build, configs, synth, wq
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GUARD = 4096
+PAT = 0xA5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    wq.load()
+
+
+def test_checked_build_runs_clean():
+    lib = os.path.join(ROOT, "paper_2605_02262_b200", "lib", "checked", "libwq.so")
+    if not os.path.exists(lib):
+        build.build_variant("checked", "-DWQ_CHECKS=1")
+    env = dict(os.environ, WQ_VARIANT="checked")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "checked_run.py")], capture_output=True,
+                       text=True, timeout=900, env=env, cwd=ROOT)
+    log = r.stdout[-4000:] + r.stderr[-4000:]
+    assert r.returncode == 0, log
+    assert "checked_run: ok" in r.stdout and "WQ_CHECK failed" not in log, log
+
+
+class Guarded:
+    """Device buffers embedded between canary zones."""
+
+    def __init__(self):
+        self.bufs = []
+
+    def empty(self, shape, dtype, fill=None):
+        n = int(torch.Size(shape).numel()) * torch.empty((), dtype=dtype).element_size()
+        raw = torch.full((n + 2 * GUARD + 16,), PAT, dtype=torch.uint8, device="cuda")
+        inner = raw[GUARD:GUARD + n]
+        t = inner.view(dtype).view(shape)
+        if fill is not None:
+            t.fill_(fill)
+        self.bufs.append((raw, n))
+        return t
+
+    def check(self):
+        torch.cuda.synchronize()
+        for raw, n in self.bufs:
+            assert bool((raw[:GUARD] == PAT).all()), "front guard overwritten"
+            assert bool((raw[GUARD + n:] == PAT).all()), "back guard overwritten"
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_guard_zones(name):
+    cfg = configs.CONFIGS[name]
+    m = cfg.model
+    G = Guarded()
+    vis, txt = synth.embeddings(cfg.B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, "cuda")
+    g = wq.geom(cfg.B, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
+    W, L = cfg.W, min(cfg.layers, 3)
+    scores = G.empty((cfg.B, W), torch.float64)
+    sws = G.empty((wq.wq_window_scores_workspace(cfg.B, m.D),), torch.uint8)
+    wq.wq_window_scores(vis, txt, cfg.S, scores=scores, workspace=sws)
+    thr = wq.wq_thresholds(cfg.sensitivities()[:L], cfg.alpha, len(cfg.widths))
+    bits, rank = G.empty((L, cfg.B, W), torch.uint8), G.empty((cfg.B, W), torch.int32)
+    perm, seg = G.empty((L, cfg.B, W), torch.int32), G.empty((L, cfg.B, 5), torch.int32)
+    wq.wq_assign_bits(scores, thr, L, g, wq.AssignOpts(cfg.budget, 1, 0), bits, rank, perm, seg)
+    G.check()
+    K, V, kr, vr, rest_len = synth.layer_tensors(cfg, 0, "cuda")
+    q = synth.queries(cfg.B, m.Hq, m.H, m.d, cfg.seed, 0, device="cuda")
+    offs = G.empty((cfg.B * m.H + 1,), torch.int64)
+    wq.wq_layer_layout(g, seg[0], offs)
+    torch.cuda.synchronize()
+    packed = G.empty((int(offs[-1].item()),), torch.uint8, fill=0)
+    wq.wq_reorder_quantize_pack(K, V, 0, g, perm[0], seg[0], offs, packed)
+    out = G.empty((cfg.B, m.Hq, m.d), torch.float16)
+    part = G.empty((cfg.B, m.Hq, m.d + 2), torch.float32)
+    ws = G.empty((wq.wq_decode_workspace(g),), torch.uint8, fill=0)
+    sm = 1 / math.sqrt(m.d)
+    outs = []
+    for flags in (0, wq.WQ_DECODE_EARLY, wq.WQ_DECODE_EARLY):
+        wq.wq_decode_attention(q, packed, offs, seg[0], g, kr, vr, rest_len, sm, out=out, partial=part,
+                               workspace=ws, flags=flags)
+        outs.append(out.clone())
+    G.check()
+    assert all(torch.equal(outs[0], o) for o in outs[1:]), "workspace state leaked between calls"
+    merged = G.empty((cfg.B, m.Hq, m.d), torch.float16)
+    wq.wq_merge_partials(torch.stack([part, part]), g, out=merged)
+    pr, sr = G.empty((cfg.B, W), torch.int32), G.empty((cfg.B, 5), torch.int32)
+    wq.wq_shard_slots(perm[0], seg[0], 3, 2, pr, sr)
+    seg16, offs16 = wq.wq_dequant_layout(g, seg[0])
+    torch.cuda.synchronize()
+    img16 = G.empty((int(offs16[-1].item()),), torch.uint8, fill=0)
+    wq.wq_dequantize_image(packed, offs, seg[0], g, offs16, img16)
+    woff = G.empty((cfg.B, W + 1), torch.int64)
+    wq.wq_unreordered_layout(g, bits[0].contiguous(), woff)
+    uimg = G.empty((int(offs[-1].item()),), torch.uint8, fill=0)
+    wq.wq_unreorder_image(packed, offs, seg[0], perm[0], g, woff, uimg)
+    wq.wq_decode_attention_unreordered(q, uimg, offs, seg[0], woff, g, kr, vr, rest_len, sm, out=out,
+                                       workspace=ws)
+    G.check()

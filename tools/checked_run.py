@@ -1,8 +1,9 @@
-"""C1-sized run of every libwq device call, for compute-sanitizer (tests/test_gpu_sanitize.py):
+"""C1-sized run of every libwq device call, for the checked build (tests/test_gpu_checked.py):
 scores (cosine, Pearson), rank + assign (budget and vote), layout, quantize, decode
 (flags 0, then a PDL-chained WQ_DECODE_EARLY decode, and partials), merge, shard,
 the unfused (T9) and unreordered (T8) baselines and the two-rank fused-merge emulation.
-Exits 0 when every call returned WQ_OK; the sanitizer reports hazards itself."""
+Exits 0 when every call returned WQ_OK; under WQ_VARIANT=checked (-DWQ_CHECKS=1) every
+device-side bounds check of the path ran."""
 import math
 import os
 import sys
@@ -66,7 +67,7 @@ def main():
     for epoch in (1, 2):
         wq.wq_decode_attention_peer_emulated(ranks, g16, sm, ptrs, [b.data_ptr() for b in bufs], epoch)
     torch.cuda.synchronize()
-    print("sanitize_run: ok")
+    print("checked_run: ok")
 
 
 if __name__ == "__main__":

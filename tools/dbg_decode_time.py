@@ -25,7 +25,7 @@ nsm = torch.cuda.get_device_properties(0).multi_processor_count
 NW = int(os.environ.get("NW", "11"))
 TS = 200
 TSB = TS * 8
-for mode in [int(x) for x in os.environ.get("DBG", "0,19").split(",")]:
+for mode in [int(x) for x in os.environ.get("DBG", "0").split(",")]:
     os.environ["WQ_DECODE_DEBUG"] = str(8 | mode)
     for it in range(4):
         ws[-nsm * TSB:].zero_()
@@ -60,7 +60,9 @@ for mode in [int(x) for x in os.environ.get("DBG", "0,19").split(",")]:
     ok = np.isfinite(dur_loop)
     sol, *_ = np.linalg.lstsq(A[ok], dur_loop[ok], rcond=None)
     print("fit us/item (2,4,8,16,rest) + const:", np.round(sol, 4), " resid rms", round(float(np.sqrt(np.mean((A[ok] @ sol - dur_loop[ok]) ** 2))), 3))
-    for cta in (0, 77):
+    slow = int(np.nanargmax(st[:, 3]))
+    print("slowest CTA", slow)
+    for cta in (0, slow):
         ref = tsb[cta, 70]
         pi = tsb[cta, 72:136]; fd = tsb[cta, 136:200]
         n = int((pi > 0).sum())

@@ -7,6 +7,9 @@
 #include <cstdio>
 
 using namespace wq;
+// (the launchers of decode.cu are not used here)
+int wq::device_sm_count() { return 148; }
+cudaError_t wq::launch_decode_tc(const DecodeArgs &, int, cudaStream_t) { return cudaErrorNotSupported; }
 
 template <int BITS>
 __global__ void __launch_bounds__(512, 1) kbench(int iters, unsigned long long *cyc, float *sink) {
@@ -56,7 +59,7 @@ void run(int sms, unsigned long long *dc, float *ds) {
   const size_t smem = 4 * REC + 16 * 512 + 2048;
   cudaFuncSetAttribute(kbench<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int iters = 200;
-  for (int nw : {1, 2, 4, 8, 11, 12, 16}) {
+  for (int nw : {1, 11, 16}) {
     kbench<BITS><<<sms, nw * 32, smem>>>(iters, dc, ds);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
