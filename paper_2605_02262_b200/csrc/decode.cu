@@ -40,6 +40,9 @@ constexpr int DT = (NCW + 1) * 32;      // threads per CTA: consumers + the prod
 #ifndef WQ_DEC_QLO
 #define WQ_DEC_QLO 1                     // carry q*s as fp16 hi + lo (0: hi only, experiment)
 #endif
+#ifndef WQ_DEC_PAIR
+#define WQ_DEC_PAIR 0                    // 1: 2-bit windows in pairs (do_window2), S <= 32 (A/B: slower)
+#endif
 #ifndef WQ_EXP_NOZP
 #define WQ_EXP_NOZP 0                    // timing experiments only: skip the zero-point MMA (wrong values)
 #endif
@@ -235,6 +238,95 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
   }
 }
 
+// Two windows A and B of the same b-bit class (S <= 32) in one pass: their 2*S/16 tiles
+// share the k-tile loop (one q fragment load per k-tile, four independent K-side MMA
+// chains for S = 32), ONE zero-point MMA per k-tile serves both (A rows g = window A's
+// minima, rows g + 8 = window B's: the rows the single-window path leaves unused), and one
+// softmax pass covers the pair.  Same products and accumulations per window as do_window.
+template <int D, int S, int BITS>
+WQ_DEV void do_window2(const uint8_t *recA, const uint8_t *recB, const uint8_t *qs, float scale2,
+                       WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane) {
+  constexpr int NTT = S / 16;                 // tiles per window (1 or 2)
+  constexpr int T = 2 * NTT;                  // tiles of the pair: A's, then B's
+  constexpr int KT = D / 16;
+  constexpr int WPL = D * BITS / 64;
+  constexpr int TILE = 2 * D * BITS;
+  constexpr int KB = S * D * BITS / 8;        // K (or V) code bytes of a window
+  static_assert(BITS < 16 && NTT >= 1 && NTT <= 2, "pairs of b-bit windows with S <= 32");
+  const uint8_t *kpA = recA + 2 * KB, *kpB = recB + 2 * KB;
+  const int g = lane >> 2, q = lane & 3;
+  uint32_t wk[T][WPL];
+#pragma unroll
+  for (int t = 0; t < NTT; t++) {
+    load_chunk<D, BITS>(wk[t], recA + t * TILE, lane);
+    load_chunk<D, BITS>(wk[NTT + t], recB + t * TILE, lane);
+  }
+  float ah[T][4], al[T][4];
+  float b0[4] = {0.f, 0.f, 0.f, 0.f}, b1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int t = 0; t < T; t++)
+#pragma unroll
+    for (int i = 0; i < 4; i++) { ah[t][i] = 0.f; al[t][i] = 0.f; }
+#pragma unroll
+  for (int kt = 0; kt < KT; kt++) {
+    const uint2 qk = lds64(qs + (kt * 32 + lane) * 8);
+    const uint4 pa = lds128(kpA + (q * KT + kt) * 16);     // {mn01, s01, mn89, s89} of A
+    const uint4 pb = lds128(kpB + (q * KT + kt) * 16);     // ... of B
+    {
+      const uint32_t am[4] = {pa.x, pb.x, pa.z, pb.z};     // rows g: A's minima, rows g + 8: B's
+      if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
+      else mma16816(b0, am, qk.x, qk.y, b0);
+    }
+    const uint32_t hA0 = hmul2u(qk.x, pa.y), hA1 = hmul2u(qk.y, pa.w);
+    const uint32_t lA0 = h2u(__hfma2(u2h(qk.x), u2h(pa.y), __hneg2(u2h(hA0))));
+    const uint32_t lA1 = h2u(__hfma2(u2h(qk.y), u2h(pa.w), __hneg2(u2h(hA1))));
+    const uint32_t hB0 = hmul2u(qk.x, pb.y), hB1 = hmul2u(qk.y, pb.w);
+    const uint32_t lB0 = h2u(__hfma2(u2h(qk.x), u2h(pb.y), __hneg2(u2h(hB0))));
+    const uint32_t lB1 = h2u(__hfma2(u2h(qk.y), u2h(pb.w), __hneg2(u2h(hB1))));
+#pragma unroll
+    for (int t = 0; t < T; t++) {
+      uint32_t a[4];
+#pragma unroll
+      for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS>(wk[t], 4 * kt + r);
+      if (t < NTT) {
+        mma16816(ah[t], a, hA0, hA1, ah[t]);
+        mma16816(al[t], a, lA0, lA1, al[t]);
+      } else {
+        mma16816(ah[t], a, hB0, hB1, ah[t]);
+        mma16816(al[t], a, lB0, lB1, al[t]);
+      }
+    }
+  }
+  float sc[T][4];
+#pragma unroll
+  for (int t = 0; t < T; t++)
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      sc[t][i] = (ah[t][i] + al[t][i]) + (b0[(t < NTT ? 0 : 2) + (i & 1)] + b1[(t < NTT ? 0 : 2) + (i & 1)]);
+  float vs[T][2], vm[T][2];
+#pragma unroll
+  for (int t = 0; t < T; t++) {
+    const uint8_t *vp = (t < NTT ? kpA : kpB) + 4 * D;
+    const uint4 pr = lds128(vp + (4 * (t % NTT) + (g >> 1)) * 16);
+    const uint32_t sh = (g & 1) * 16;
+    vs[t][0] = __half2float(__ushort_as_half((unsigned short)(pr.x >> sh)));
+    vs[t][1] = __half2float(__ushort_as_half((unsigned short)(pr.y >> sh)));
+    constexpr float HALF = (float)(1 << (BITS - 1));
+    vm[t][0] = fmaf(vs[t][0], HALF, __half2float(__ushort_as_half((unsigned short)(pr.z >> sh))));
+    vm[t][1] = fmaf(vs[t][1], HALF, __half2float(__ushort_as_half((unsigned short)(pr.w >> sh))));
+  }
+  softmax_tiles<T, KT>(sc, scale2, st, o, vs, vm, true, scratch, lane);
+#pragma unroll
+  for (int t = 0; t < T; t++) {
+    uint32_t pbv[2];
+    ldsm_x2_t(pbv, scratch + (16 * t + (lane & 15)) * 16);
+    uint32_t wv[WPL];
+    load_chunk<D, BITS>(wv, (t < NTT ? recA : recB) + KB + (t % NTT) * TILE, lane);
+    tile_pv<D, BITS>(wv, pbv[0], pbv[1], o);
+  }
+  __syncwarp();
+}
+
 // FP16 rest tile: K rows [16][D] at Kb, V rows [16][D] at Vb (unpadded rows as the
 // bulk copies land them; rows past ntok hold stale bytes and are masked)
 template <int D>
@@ -285,13 +377,14 @@ struct DecodeSmem {
   static constexpr int RING = WQ_DEC_RING;
   static constexpr int NST = (RING / STAGE) < 2 ? 2 : RING / STAGE;
   static constexpr int KT = D / 16;
-  static constexpr int SCRATCH = 2 * 16 * 16;            // P' rows of one 2-tile chunk per warp
+  static constexpr int SCRATCH = 4 * 16 * 16;            // P' rows of up to 4 tiles per warp
   static constexpr int EPW = 8 * D + 24;                 // per warp: o [KT*32 groups][4], m[8], l[8], vb[8]
+  static_assert(SCRATCH <= EPW * 4, "a warp's P' scratch lives in its own epilogue slot");
   static constexpr int PSLOT = 16 + 8 * D;               // floats of a CTA partial in the workspace
   static constexpr int NUS = 4;                          // entry ring published by the producer
   static constexpr size_t ring = (size_t)NST * STAGE;
-  static constexpr size_t scratch_off = ring;
-  static constexpr size_t q_off = scratch_off + (size_t)NCW * SCRATCH;     // q fragments [KT][32][2]
+  static constexpr size_t hw_off = ring;                                       // epilogue head weights
+  static constexpr size_t q_off = hw_off + ((size_t)(NCW * 8 + 24) * 4 + 15) / 16 * 16;   // q fragments [KT][32][2]
   static constexpr size_t ep_off = q_off + (size_t)KT * 32 * 8;
   static constexpr size_t units_off = ep_off + (size_t)NCW * EPW * 4;
   static constexpr size_t ent_off = units_off + (size_t)(MAX_UNITS + 1) * 8;
@@ -536,8 +629,9 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
   }
 
   // =========================== consumers ===========================
-  uint8_t *scratch = sm + SM::scratch_off + warp * SM::SCRATCH;
   float *ep = reinterpret_cast<float *>(sm + SM::ep_off);
+  // the warp's P' scratch: the head of its own epilogue slot (dead until it parks there)
+  uint8_t *scratch = reinterpret_cast<uint8_t *>(ep + warp * SM::EPW);
   const int g = lane >> 2, q = lane & 3;
   const int grp = a.grp;
   uint8_t *qs = sm + SM::q_off;
@@ -617,13 +711,17 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
 #pragma unroll
     for (int p = UR ? 4 : 0; p < 5; p++) {
       using IG = ItemGeo<D, S, false>;
-      constexpr int SZ_[5] = {IG::sz(0), IG::sz(1), IG::sz(2), IG::sz(3), IG::sz(4)};
-      const int sz = SZ_[p];
+      // item bytes of class p, computed (a table indexed by p would live in local memory)
+      const int sz = p == 4 ? IG::REST_SZ : (p == 3 ? 4 * S * D : S * D * (2 << p) / 4 + 4 * D + 4 * S);
       const int cap = STAGE / sz;
       const int len = E.len[p], nst = E.nst[p], lo = E.lo[p];
+      // 2-bit stages (S <= 32) are consumed in PAIRS of windows (do_window2): a stage of n
+      // records is ceil(n/2) work items, handed out round robin like single items
+      constexpr bool PAIRS = WQ_DEC_PAIR && S <= 32;
       for (int t = 0; t < nst; t++, sg++) {
         const int slot = sg % NST;
-        const int n = min(cap, len - t * cap);
+        const int nrec = min(cap, len - t * cap);
+        const int n = (PAIRS && p == 0) ? (nrec + 1) / 2 : nrec;
         const uint64_t t0 = ts ? clock64() : 0;
         mbar_wait(&full[slot], (uint32_t)(sg / NST) & 1u);
         const uint64_t t1 = ts ? clock64() : 0;
@@ -634,7 +732,13 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
           WQ_CHECK(k < n && (k + 1) * sz <= STAGE);
           const uint8_t *rec = sbase + (size_t)k * sz;
           if (p == 0) {
-            do_window<D, S, 2>(rec, qs, a.scale_log2, st, o, scratch, lane);
+            if constexpr (PAIRS) {
+              const uint8_t *r0 = sbase + (size_t)(2 * k) * sz;
+              if (2 * k + 1 < nrec) do_window2<D, S, 2>(r0, r0 + sz, qs, a.scale_log2, st, o, scratch, lane);
+              else do_window<D, S, 2>(r0, qs, a.scale_log2, st, o, scratch, lane);
+            } else {
+              do_window<D, S, 2>(rec, qs, a.scale_log2, st, o, scratch, lane);
+            }
           } else if (p == 1) {
             do_window<D, S, 4>(rec, qs, a.scale_log2, st, o, scratch, lane);
           } else if (p == 2) {
@@ -686,7 +790,7 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
     // (2) per head j (8 threads): M = max_w m_w, weights f_w = 2^(m_w - M), L = sum f_w l_w,
     // VB = sum f_w vb_w into hw = [NCW][8] f, then [8] M, [8] L, [8] VB
     const bool split = (c1 - c0) > 1;
-    float *hw = reinterpret_cast<float *>(sm + SM::scratch_off);
+    float *hw = reinterpret_cast<float *>(sm + SM::hw_off);
     if (tid < 8) {
       const int j = tid;
       float mw[NCW];

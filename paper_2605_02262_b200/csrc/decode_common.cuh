@@ -17,6 +17,15 @@ constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trac
 #ifndef WQ_DEC_EOV
 #define WQ_DEC_EOV 2000                // per-unit entry overhead in cost units of S*D/100
 #endif
+#ifndef WQ_DEC_C16
+#define WQ_DEC_C16 235                 // FP16 window cost, units of S*D/100 (2-bit: 156)
+#endif
+#ifndef WQ_DEC_CR
+#define WQ_DEC_CR 40                   // FP16 rest tile (16 tokens) cost, units of D
+#endif
+#ifndef WQ_DEC_LOV
+#define WQ_DEC_LOV 0                   // merge allowance of a split unit's last CTA, units of S*D/100
+#endif
 #ifndef WQ_DEC_STREAM
 #define WQ_DEC_STREAM 0                // 1: cost-stream split when units < CTAs (measured slower)
 #endif
@@ -47,7 +56,8 @@ struct ItemGeo {
       return k == 4 ? 40LL * D
                     : (int64_t)(k == 0 ? 100 : k == 1 ? 140 : k == 2 ? 220 : 300) * S * D / 100;
     } else {
-      return k == 4 ? 40LL * D : (int64_t)(k == 0 ? 156 : k == 1 ? 170 : k == 2 ? 233 : 235) * S * D / 100;
+      return k == 4 ? (int64_t)WQ_DEC_CR * D
+                    : (int64_t)(k == 0 ? 156 : k == 1 ? 170 : k == 2 ? 233 : WQ_DEC_C16) * S * D / 100;
     }
   }
 };
@@ -288,7 +298,11 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
     int i0 = 0, i1 = gg.nslots + gg.ntiles;
     int ec0 = P.split == 1 ? P.c0 : c, ec1 = P.split == 1 ? P.c1 : c + 1;
     if (P.split == 1) {
-      const double ucost = (double)(ustart[u + 1] - ustart[u]);
+      // the unit's cost plus the last CTA's merge allowance, cut into n equal shares: the
+      // last CTA (the merger: it ends with the unit's FP16 windows and rest tiles, then
+      // merges every partial) gets LOV less item cost than the others
+      const double lov = (double)WQ_DEC_LOV * S * D / 100;
+      const double ucost = (double)(ustart[u + 1] - ustart[u]) + lov;
       const int k = c - P.c0, n = P.c1 - P.c0;
       i0 = first_item<D, S, TC>(gg, ucost * k / n);
       if (k < n - 1) i1 = first_item<D, S, TC>(gg, ucost * (k + 1) / n);
