@@ -1,13 +1,16 @@
 // quant.cu -- wq_layer_layout and wq_reorder_quantize_pack (Alg.2 prefill
 // branch P:420-446, Eq.14-16, group = window P:508, readings Q17-Q22).
 //
-// One CTA per (slot, kv-head, request).  The window's fp16 K and V rows are pulled
-// into shared memory by the TMA bulk-copy engine (one cp.async.bulk per tensor when
-// rows are contiguous), per-channel K and per-token V (min, max) are reduced with
+// Persistent teams of 4 warps.  A window's fp16 K and V rows are pulled into shared
+// memory by tensor-map TMA copies (128-byte swizzled boxes), per-channel K and per-token
+// V (min, max) are reduced with
 // fp16x2 min/max, the fp32 quantizer contract (Q17) runs per element with explicit
 // round-to-nearest intrinsics (no FMA contraction), and the record is written in
 // D-1 fragment order with 16-byte stores at the window's REORDERED slot (so the
 // reorder of Alg.2 is an address remap, not a copy).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "wq_device.cuh"
 #include "wq_internal.h"
 
@@ -92,14 +95,16 @@ WQ_DEV void qwait(uint64_t *b, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------------------------
-// k_quant: persistent.  A CTA runs TEAMS teams of 4 warps; a team owns two window
-// slots in shared memory (double buffering) and quantizes windows gt, gt + nteams, ...
-// of the flattened (request, kv head, slot) space.  A window's K and V rows land by
-// two 1-D bulk copies (TMA engine); its work splits into independent warp tasks --
-// the two channel halves of K (per-channel parameters) and the 16-token tiles of V
+// k_quant: persistent.  A CTA runs TEAMS teams of 4 warps; a team owns NSL window slots
+// in shared memory and quantizes windows gt, gt + nteams, ... of the flattened (request,
+// kv head, slot) space.  A window's K and V rows land by tensor-map TMA copies
+// (cp.async.bulk.tensor, one box of S tokens x 64 channels per 128-byte row, 128-byte
+// swizzle: 16-byte chunk j of token row r sits at chunk j ^ (r mod 8)), so the fragment-
+// order reads below are bank-conflict free straight from the landed tile -- no re-layout
+// buffer.  A window's work splits into independent warp tasks -- the two channel halves of
+// K (per-channel parameters need only their channels) and the 16-token tiles of V
 // (per-token parameters) -- so no CTA barrier is ever needed: the slot is released
-// through an mbarrier once the team's 4 warps are done with it.  Fragment-order reads
-// go through a per-warp work buffer with rows padded by 16 bytes (bank-conflict free).
+// through an mbarrier once the team's 4 warps are done with it.
 // ---------------------------------------------------------------------------------
 // what a team slot holds, written by the issuing lane with the copy (so the consumer
 // warps never wait on the metadata loads): record offset and width, bits = 0 if empty
@@ -110,18 +115,18 @@ struct WinDesc {
 
 template <int D, int S>
 struct QuantGeo {
-  static constexpr int WIN = 4 * S * D;                 // K + V rows of a window, as landed
-  static constexpr int WRB = 2 * D + 16;                // padded row bytes, work buffer
-  static constexpr int WORK = 16 * WRB;                 // one 16-row tile
+  static constexpr int KH = D / 64;                     // 64-channel boxes per K (and V) window
+  static constexpr int BOX = S * 128;                   // bytes of one box: S token rows x 128 B
+  static constexpr int WIN = 2 * KH * BOX;              // K boxes, then V boxes (= 4*S*D)
   static constexpr int SCR = (D > S ? D : S) * 8;       // float2 params scratch per warp
 #ifndef WQ_Q_NSL
 #define WQ_Q_NSL 0                                      // 0: by window size (below)
 #endif
-  // window slots per team: double buffering pays while it leaves room for 4 teams; for
-  // S >= 64 (32-64 KB windows) one slot per team and more teams per SM win (C4 shape:
-  // S = 64 716 -> 583 us, S = 128 992 -> 662 us; S = 32 needs two: 493 vs 641 us)
-  static constexpr int NSL = WQ_Q_NSL > 0 ? WQ_Q_NSL : (S >= 64 ? 1 : 2);
-  static constexpr int PER_TEAM = NSL * WIN + 4 * (WORK + SCR);
+  // window slots per team: small windows buffer 3-4 deep (bytes in flight: the copy latency
+  // under load is ~3 us); for S >= 64 (32-64 KB windows) one slot per team and more teams
+  static constexpr int NSL0 = S >= 64 ? 1 : ((50 * 1024) / WIN > 4 ? 4 : (50 * 1024) / WIN);
+  static constexpr int NSL = WQ_Q_NSL > 0 ? WQ_Q_NSL : (NSL0 < 2 && S < 64 ? 2 : NSL0);
+  static constexpr int PER_TEAM = ((NSL * WIN + 4 * SCR) + 1023) / 1024 * 1024;   // slots 1024-B aligned
   static constexpr int T0 = (216 * 1024) / PER_TEAM;
   static constexpr int TEAMS = T0 > 4 ? 4 : (T0 < 1 ? 1 : T0);
   static constexpr int NT = S / 16 + 2;                 // tasks per window: 2 K halves + S/16 V tiles
@@ -130,29 +135,48 @@ struct QuantGeo {
   static constexpr size_t total = desc_off + TEAMS * NSL * 16;
 };
 
+// byte offset of (token row, byte b of the 64-channel box row) in a 128-byte-swizzled box
+WQ_DEV uint32_t swz(int row, int b) { return (uint32_t)(row * 128 + ((((b >> 4) ^ row) & 7) << 4) + (b & 15)); }
+// the 4 bytes of channels (c, c+1) of token row t of a window (boxes of 64 channels)
+WQ_DEV uint32_t pair_at(const uint8_t *boxes, int t, int c, int box_bytes) {
+  return lds32(boxes + (c >> 6) * box_bytes + swz(t, 2 * (c & 63)));
+}
+WQ_DEV uint32_t half_at(const uint8_t *boxes, int t, int c, int box_bytes) {
+  return *reinterpret_cast<const uint16_t *>(boxes + (c >> 6) * box_bytes + swz(t, 2 * (c & 63)));
+}
+
 // K channel half hf (channels [hf*D/2, (hf+1)*D/2)) of a window: per-channel min/max
 // over the S rows, parameters, then codes tile by tile (the fragment lane's words whose
 // channels fall in this half).
 template <int D, int S, int BITS>
-WQ_DEV void quant_k_half(const uint8_t *krows, uint8_t *work, float2 *kp, uint8_t *rec, int hf, int lane) {
+WQ_DEV void quant_k_half(const uint8_t *kbox, float2 *kp, uint8_t *rec, int hf, int lane) {
   using QG = QuantGeo<D, S>;
-  constexpr int WRB = QG::WRB;
   constexpr float QMAX = (float)((1 << BITS) - 1);
-  constexpr uint32_t MASK = (1u << BITS) - 1u;
   constexpr int PPW = 16 / BITS;
   constexpr int CW = D * BITS / 64;                     // chunk words per lane per tile
   constexpr int TILE = 2 * D * BITS;                    // bytes per 16-token tile
   constexpr int KBYTES = S * D * BITS / 8;
   constexpr int HP = D / 4;                             // channel pairs per half
-  // (1) min/max: lane = channel pair (rows read straight from the landed copy)
+  // (1) min/max (IEEE minimum/maximum, Q17): lane = channel pair, rows from the landed box
   if (lane < HP) {
     const int cp = hf * HP + lane;
     __half2 mn2 = __float2half2_rn(65504.f), mx2 = __float2half2_rn(-65504.f);
-#pragma unroll 8
-    for (int t = 0; t < S; t++) {
-      const __half2 x = *reinterpret_cast<const __half2 *>(krows + t * 2 * D + 4 * cp);
-      mn2 = __hmin2(mn2, x);
-      mx2 = __hmax2(mx2, x);
+    // channel pair cp: box cp/32, byte 4*(cp%32) = chunk c0, word cp%4; row t at t*128 with
+    // chunk c0 ^ (t mod 8) (the XOR term is a constant of each unrolled row)
+    const uint8_t *cb = kbox + (cp >> 5) * QG::BOX + 4 * (cp & 3);
+    const int c0 = (cp & 31) >> 2;
+    int xo[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) xo[u] = u * 128 + ((c0 ^ u) << 4);
+#pragma unroll 1
+    for (int t0 = 0; t0 < S; t0 += 8) {
+      const uint8_t *rb = cb + t0 * 128;
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const __half2 x = u2h(lds32(rb + xo[u]));
+        mn2 = __hmin2(mn2, x);
+        mx2 = __hmax2(mx2, x);
+      }
     }
     const float mn0 = __low2float(mn2), mn1 = __high2float(mn2);
     const __half s0 = q17_scale(mn0, __low2float(mx2), QMAX), s1 = q17_scale(mn1, __high2float(mx2), QMAX);
@@ -165,24 +189,19 @@ WQ_DEV void quant_k_half(const uint8_t *krows, uint8_t *work, float2 *kp, uint8_
     pv.y = (uint32_t)__half_as_ushort(s0) | ((uint32_t)__half_as_ushort(s1) << 16);
     *reinterpret_cast<uint2 *>(rec + 2 * KBYTES + (q * (D / 16) + m) * 16 + hh * 8) = pv;
   }
+  __syncwarp();
   // (2) codes: words of fragment lane L = lane whose pairs lie in this channel half
   //     (pair P -> m = P/4; m < D/32 is half 0).  WH words per tile per half.
   constexpr int WH = CW / 2 > 0 ? CW / 2 : 1;          // CW >= 2 always (d >= 64, b >= 2)
   const int g = lane >> 2, q = lane & 3;
+  // row mod 8 = g for every code word of the lane: the swizzle term of chunk cc is gx[cc]
+  int gx[8];
+#pragma unroll
+  for (int cc = 0; cc < 8; cc++) gx[cc] = (cc ^ g) << 4;
+  const uint8_t *lb = kbox + g * 128 + 4 * q;
 #pragma unroll 1
   for (int tile = 0; tile < S / 16; tile++) {
-    // re-lay the tile's 16 half rows (D bytes each) into padded rows
-    __syncwarp();
-    {
-      constexpr int CPR = D / 16;                       // 16-byte chunks per half row
-#pragma unroll
-      for (int i = lane; i < 16 * CPR; i += 32) {
-        const int t = i / CPR, cc = i - t * CPR;
-        *reinterpret_cast<uint4 *>(work + t * WRB + 16 * cc) =
-            *reinterpret_cast<const uint4 *>(krows + (tile * 16 + t) * 2 * D + hf * D + 16 * cc);
-      }
-    }
-    __syncwarp();
+    const uint8_t *tb0 = lb + tile * 16 * 128;
     uint32_t wv[WH];
 #pragma unroll
     for (int e = 0; e < WH; e++) {
@@ -191,8 +210,10 @@ WQ_DEV void quant_k_half(const uint8_t *krows, uint8_t *work, float2 *kp, uint8_
 #pragma unroll
       for (int j = 0; j < PPW; j++) {
         const int P = wl * PPW + j, m = P >> 2, r = P & 3;
-        const int row = g + 8 * (r & 1), col = 16 * m + 8 * (r >> 1) + 2 * q;     // col in [hf*D/2, ...)
-        const float2 x = __half22float2(*reinterpret_cast<const __half2 *>(work + row * WRB + 2 * (col - hf * D / 2)));
+        const int col = 16 * m + 8 * (r >> 1) + 2 * q;
+        // row = tile*16 + g + 8(r&1) (row mod 8 = g); byte 2*(col%64) = chunk cc, word q
+        const int cc = (2 * m + (r >> 1)) & 7;
+        const float2 x = __half22float2(u2h(lds32(tb0 + (m >> 2) * QG::BOX + 8 * (r & 1) * 128 + gx[cc])));
         const float4 pr = *reinterpret_cast<const float4 *>(kp + col);
         acc += q17_big(x.x, pr.x, pr.y) * (1u << (BITS * j));
         acc += q17_big(x.y, pr.z, pr.w) * (1u << (16 + BITS * j));
@@ -219,35 +240,30 @@ WQ_DEV void quant_k_half(const uint8_t *krows, uint8_t *work, float2 *kp, uint8_
 // V tile vt (tokens [16vt, 16vt+16)): per-token min/max over D channels, parameters,
 // codes of the fragment lane L = lane for this tile.
 template <int D, int S, int BITS>
-WQ_DEV void quant_v_tile(const uint8_t *vrows, uint8_t *work, float2 *vp, uint8_t *rec, int vt, int lane) {
+WQ_DEV void quant_v_tile(const uint8_t *vbox, float2 *vp, uint8_t *rec, int vt, int lane) {
   using QG = QuantGeo<D, S>;
-  constexpr int WRB = QG::WRB;
   constexpr float QMAX = (float)((1 << BITS) - 1);
-  constexpr uint32_t MASK = (1u << BITS) - 1u;
   constexpr int PPW = 16 / BITS;
   constexpr int CW = D * BITS / 64;
   constexpr int TILE = 2 * D * BITS;
   constexpr int KBYTES = S * D * BITS / 8;
-  // re-lay the tile's 16 rows into padded rows
-  __syncwarp();
-  {
-    constexpr int CPR = 2 * D / 16;
-#pragma unroll
-    for (int i = lane; i < 16 * CPR; i += 32) {
-      const int t = i / CPR, cc = i - t * CPR;
-      *reinterpret_cast<uint4 *>(work + t * WRB + 16 * cc) = *reinterpret_cast<const uint4 *>(vrows + (vt * 16 + t) * 2 * D + 16 * cc);
-    }
-  }
-  __syncwarp();
-  // (1) min/max: two lanes per token (each half of the channels), combined by a shuffle
+  // (1) min/max: two lanes per token (each half of the channels), combined by a shuffle;
+  // the pair order is rotated per lane so rows t and t + 8 and the two halves hit
+  // different bank groups
   {
     const int t = lane >> 1, hc = lane & 1;
+    // the lane's half of token row t, 16-byte chunk by chunk; the second half starts 4
+    // chunks later so a phase's 8 lanes read 8 different bank groups
+    constexpr int NC = D / 16;                          // 16-byte chunks per half (8 channels each)
     __half2 mn2 = __float2half2_rn(65504.f), mx2 = __float2half2_rn(-65504.f);
-#pragma unroll 8
-    for (int i = 0; i < D / 4; i++) {
-      const __half2 x = *reinterpret_cast<const __half2 *>(work + t * WRB + 2 * D / 2 * hc + 4 * i);
-      mn2 = __hmin2(mn2, x);
-      mx2 = __hmax2(mx2, x);
+    const int row = vt * 16 + t;
+#pragma unroll
+    for (int i = 0; i < NC; i++) {
+      const int c = hc * (D / 2) / 8 + ((i + 4 * hc) % NC);          // chunk of 8 channels
+      const uint4 v = lds128(vbox + (c >> 3) * QG::BOX + row * 128 + ((((c & 7) ^ row) & 7) << 4));
+      const __half2 x0 = u2h(v.x), x1 = u2h(v.y), x2 = u2h(v.z), x3 = u2h(v.w);
+      mn2 = __hmin2(mn2, __hmin2(__hmin2(x0, x1), __hmin2(x2, x3)));
+      mx2 = __hmax2(mx2, __hmax2(__hmax2(x0, x1), __hmax2(x2, x3)));
     }
     __half mn = __hmin(__low2half(mn2), __high2half(mn2));
     __half mx = __hmax(__low2half(mx2), __high2half(mx2));
@@ -268,6 +284,11 @@ WQ_DEV void quant_v_tile(const uint8_t *vrows, uint8_t *work, float2 *vp, uint8_
   const int g = lane >> 2, q = lane & 3;
   uint8_t *tb = rec + KBYTES + vt * TILE;
   constexpr int NG = CW >= 4 ? CW / 4 : 1;
+  // tokens 2q + 8(r>>1) (+1): row mod 8 = 2q (2q + 1); swizzle terms of chunk cc
+  int qx0[8], qx1[8];
+#pragma unroll
+  for (int cc = 0; cc < 8; cc++) { qx0[cc] = (cc ^ (2 * q)) << 4; qx1[cc] = 128 + ((cc ^ (2 * q + 1)) << 4); }
+  const uint8_t *lb = vbox + (vt * 16 + 2 * q) * 128 + 2 * g;
 #pragma unroll
   for (int gi = 0; gi < NG; gi++) {
     uint32_t wv[4] = {0u, 0u, 0u, 0u};
@@ -278,10 +299,13 @@ WQ_DEV void quant_v_tile(const uint8_t *vrows, uint8_t *work, float2 *vp, uint8_
 #pragma unroll
       for (int j = 0; j < PPW; j++) {
         const int P = wl * PPW + j, m = P >> 2, r = P & 3;
-        const int ch = 16 * m + g + 8 * (r & 1), t = 2 * q + 8 * (r >> 1);
+        const int t = 2 * q + 8 * (r >> 1);
         const float4 pr = *reinterpret_cast<const float4 *>(vp + t);      // {mn, r} of t, t+1
-        const float x0 = __half2float(*reinterpret_cast<const __half *>(work + t * WRB + 2 * ch));
-        const float x1 = __half2float(*reinterpret_cast<const __half *>(work + (t + 1) * WRB + 2 * ch));
+        // channel 16m + g + 8(r&1): box m/4, chunk cc, byte 2g; tokens t, t+1 (row mod 8 = 2q, 2q+1)
+        const int cc = (2 * m + (r & 1)) & 7;
+        const uint8_t *rb = lb + (m >> 2) * QG::BOX + 8 * (r >> 1) * 128;
+        const float x0 = __half2float(*reinterpret_cast<const __half *>(rb + qx0[cc]));
+        const float x1 = __half2float(*reinterpret_cast<const __half *>(rb + qx1[cc]));
         acc += q17_big(x0, pr.x, pr.y) * (1u << (BITS * j));
         acc += q17_big(x1, pr.z, pr.w) * (1u << (16 + BITS * j));
       }
@@ -296,48 +320,35 @@ WQ_DEV void quant_v_tile(const uint8_t *vrows, uint8_t *work, float2 *vp, uint8_
 
 // FP16 window, task tk: K halves / V tiles copied into fragment order.
 template <int D, int S>
-WQ_DEV void copy_task_fp16(const uint8_t *krows, const uint8_t *vrows, uint8_t *work, uint8_t *rec, int tk, int lane) {
+WQ_DEV void copy_task_fp16(const uint8_t *kbox, const uint8_t *vbox, uint8_t *rec, int tk, int lane) {
   using QG = QuantGeo<D, S>;
-  constexpr int WRB = QG::WRB;
   constexpr int TILE = 2 * D * 16;
   const int g = lane >> 2, q = lane & 3;
   if (tk < 2) {
     // K half tk: groups gi (4 words, m = gi) with 16m in this half, every tile
 #pragma unroll 1
     for (int tile = 0; tile < S / 16; tile++) {
-      __syncwarp();
-      for (int i = lane; i < 16 * (2 * D / 16); i += 32) {
-        const int t = i / (2 * D / 16), cc = i - t * (2 * D / 16);
-        *reinterpret_cast<uint4 *>(work + t * WRB + 16 * cc) = *reinterpret_cast<const uint4 *>(krows + (tile * 16 + t) * 2 * D + 16 * cc);
-      }
-      __syncwarp();
       for (int gi = tk * (D / 32); gi < (tk + 1) * (D / 32); gi++) {
         uint32_t wv[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) {
           const int P = 4 * gi + e, m = P >> 2, r = P & 3;
-          const int row = g + 8 * (r & 1), col = 16 * m + 2 * q + 8 * (r >> 1);
-          wv[e] = *reinterpret_cast<const uint32_t *>(work + row * WRB + 2 * col);
+          const int row = tile * 16 + g + 8 * (r & 1), col = 16 * m + 2 * q + 8 * (r >> 1);
+          wv[e] = pair_at(kbox, row, col, QG::BOX);
         }
         *reinterpret_cast<uint4 *>(rec + tile * TILE + gi * 512 + lane * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       }
     }
   } else {
     const int vt = tk - 2;
-    __syncwarp();
-    for (int i = lane; i < 16 * (2 * D / 16); i += 32) {
-      const int t = i / (2 * D / 16), cc = i - t * (2 * D / 16);
-      *reinterpret_cast<uint4 *>(work + t * WRB + 16 * cc) = *reinterpret_cast<const uint4 *>(vrows + (vt * 16 + t) * 2 * D + 16 * cc);
-    }
-    __syncwarp();
     for (int gi = 0; gi < D / 16; gi++) {
       uint32_t wv[4];
 #pragma unroll
       for (int e = 0; e < 4; e++) {
         const int P = 4 * gi + e, m = P >> 2, r = P & 3;
         const int ch = 16 * m + g + 8 * (r & 1), t = 2 * q + 8 * (r >> 1);
-        const uint32_t lo = *reinterpret_cast<const uint16_t *>(work + t * WRB + 2 * ch);
-        const uint32_t hi = *reinterpret_cast<const uint16_t *>(work + (t + 1) * WRB + 2 * ch);
+        const uint32_t lo = half_at(vbox, vt * 16 + t, ch, QG::BOX);
+        const uint32_t hi = half_at(vbox, vt * 16 + t + 1, ch, QG::BOX);
         wv[e] = lo | (hi << 16);
       }
       *reinterpret_cast<uint4 *>(rec + S * D * 2 + vt * TILE + gi * 512 + lane * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
@@ -345,16 +356,26 @@ WQ_DEV void copy_task_fp16(const uint8_t *krows, const uint8_t *vrows, uint8_t *
   }
 }
 
+// 4-D tensor-map TMA load of one box into shared memory, completes on mbarrier b
+WQ_DEV void tma_load_4d(void *dst, const CUtensorMap *tm, int c0, int c1, int c2, int c3, uint64_t *b,
+                        uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(b)), "l"(policy)
+      : "memory");
+}
+
 template <int D, int S>
-__global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantArgs a) {
+__global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1)
+    k_quant(QuantArgs a, const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
   using QG = QuantGeo<D, S>;
-  extern __shared__ __align__(128) uint8_t sm[];
+  extern __shared__ __align__(1024) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int team = warp >> 2, tw = warp & 3;
   uint8_t *tbase = sm + (size_t)team * QG::PER_TEAM;
   constexpr int NSL = QG::NSL;
-  uint8_t *work = tbase + NSL * QG::WIN + tw * (QG::WORK + QG::SCR);
-  float2 *scr = reinterpret_cast<float2 *>(work + QG::WORK);
+  float2 *scr = reinterpret_cast<float2 *>(tbase + NSL * QG::WIN + tw * QG::SCR);
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + QG::bar_off) + team * 2 * NSL;   // [NSL] full, [NSL] empty
   uint64_t *empty = full + NSL;
   WinDesc *wdesc = reinterpret_cast<WinDesc *>(sm + QG::desc_off) + team * NSL;
@@ -364,6 +385,7 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
     for (int i = 0; i < NSL; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 4); }
     fence_mbar_init();
   }
+  WQ_CHECK((smem_u32(sm) & 1023u) == 0u);        // 128-byte swizzle atoms need 1024-B aligned boxes
   __syncthreads();
   auto locate = [&](int64_t wi, int &b, int &h, int &slot) {
     slot = (int)(wi % a.perm_stride);
@@ -373,8 +395,8 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
   };
   // Window metadata (seg_off, perm, offs) of team window k, loaded by the issuing lane one
   // window AHEAD of its copy: the three loads are independent (issued together, before any
-  // branch on their values) and complete while the warp quantizes, so the bulk copy of a
-  // window never waits on a global round trip (ncu r01: 75% long_sb on the issue path).
+  // branch on their values) and complete while the warp quantizes, so the copy of a window
+  // never waits on a global round trip (ncu r01: 75% long_sb on the issue path).
   struct Meta {
     int b, h, slot, w, so[5];
     int64_t base;
@@ -416,18 +438,15 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
     WQ_CHECK(roff >= a.offs[(int64_t)b * a.H + h] && roff + record_bytes(bits, D, S) <= a.offs[(int64_t)b * a.H + h + 1]);
     wdesc[sl].roff = roff;
     wdesc[sl].bits = bits;
-    const int64_t ro = b * a.sb + h * a.sh + (int64_t)(a.vis_off + w * S) * a.st;
     uint8_t *dst = tbase + (size_t)sl * QG::WIN;
     const uint64_t pol = policy_evict_first();
-    mbar_arrive_expect_tx(&full[sl], (uint32_t)(4 * S * D));
-    if (a.st == D) {
-      bulk_g2s_evict_first(dst, a.k + ro, S * 2 * D, &full[sl], pol);
-      bulk_g2s_evict_first(dst + S * 2 * D, a.v + ro, S * 2 * D, &full[sl], pol);
-    } else {
-      for (int t = 0; t < S; t++) {
-        bulk_g2s_evict_first(dst + t * 2 * D, a.k + ro + t * a.st, 2 * D, &full[sl], pol);
-        bulk_g2s_evict_first(dst + S * 2 * D + t * 2 * D, a.v + ro + t * a.st, 2 * D, &full[sl], pol);
-      }
+    mbar_arrive_expect_tx(&full[sl], (uint32_t)QG::WIN);
+    const int t0 = a.vis_off + w * S;
+    // a window = d/64 boxes of [S tokens][64 channels] per tensor (rows of 128 B)
+#pragma unroll
+    for (int hb = 0; hb < QG::KH; hb++) {
+      tma_load_4d(dst + hb * QG::BOX, &tmk, 64 * hb, t0, h, b, &full[sl], pol);
+      tma_load_4d(dst + (QG::KH + hb) * QG::BOX, &tmv, 64 * hb, t0, h, b, &full[sl], pol);
     }
   };
   const bool issuer = tw == 0 && lane == 0;
@@ -452,24 +471,51 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1) k_quant(QuantA
     const int bits = wdesc[sl].bits;
     if (bits) {
       uint8_t *rec = a.packed + wdesc[sl].roff;
-      const uint8_t *krows = tbase + (size_t)sl * QG::WIN, *vrows = krows + S * 2 * D;
+      const uint8_t *kbox = tbase + (size_t)sl * QG::WIN, *vbox = kbox + QG::KH * QG::BOX;
       for (int tk = tw; tk < QG::NT; tk += 4) {
         if (bits == 16) {
-          copy_task_fp16<D, S>(krows, vrows, work, rec, tk, lane);
+          copy_task_fp16<D, S>(kbox, vbox, rec, tk, lane);
         } else if (tk < 2) {
-          if (bits == 2) quant_k_half<D, S, 2>(krows, work, scr, rec, tk, lane);
-          else if (bits == 4) quant_k_half<D, S, 4>(krows, work, scr, rec, tk, lane);
-          else quant_k_half<D, S, 8>(krows, work, scr, rec, tk, lane);
+          if (bits == 2) quant_k_half<D, S, 2>(kbox, scr, rec, tk, lane);
+          else if (bits == 4) quant_k_half<D, S, 4>(kbox, scr, rec, tk, lane);
+          else quant_k_half<D, S, 8>(kbox, scr, rec, tk, lane);
         } else {
-          if (bits == 2) quant_v_tile<D, S, 2>(vrows, work, scr, rec, tk - 2, lane);
-          else if (bits == 4) quant_v_tile<D, S, 4>(vrows, work, scr, rec, tk - 2, lane);
-          else quant_v_tile<D, S, 8>(vrows, work, scr, rec, tk - 2, lane);
+          if (bits == 2) quant_v_tile<D, S, 2>(vbox, scr, rec, tk - 2, lane);
+          else if (bits == 4) quant_v_tile<D, S, 4>(vbox, scr, rec, tk - 2, lane);
+          else quant_v_tile<D, S, 8>(vbox, scr, rec, tk - 2, lane);
         }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[sl]);       // this warp is done with the slot
   }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+// [B][H][T][d] fp16 (strides in elements) as a 4-D tensor, boxes of 64 channels x S tokens
+// (rows of 128 B), 128-byte swizzle
+static bool encode_kv_map(CUtensorMap *tm, const __half *base, int B, int H, int T, int d, int S,
+                          int64_t sb, int64_t sh, int64_t st) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t gdim[4] = {(cuuint64_t)d, (cuuint64_t)T, (cuuint64_t)H, (cuuint64_t)B};
+  const cuuint64_t gstr[3] = {(cuuint64_t)st * 2, (cuuint64_t)sh * 2, (cuuint64_t)sb * 2};
+  const cuuint32_t box[4] = {64, (cuuint32_t)S, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half *>(base), gdim, gstr, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int D, int S>
@@ -487,7 +533,13 @@ static cudaError_t launch_quant_t(const QuantArgs &a, cudaStream_t st) {
   const int64_t need = (nwin + QG::TEAMS - 1) / QG::TEAMS;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  k_quant<D, S><<<(unsigned)grid, QG::TEAMS * 128, QG::total, st>>>(a);
+  // tokens read: [vis_off, vis_off + M)
+  const int T = a.vis_off + a.M;
+  CUtensorMap tmk, tmv;
+  if (!encode_kv_map(&tmk, a.k, a.B, a.H, T, D, S, a.sb, a.sh, a.st) ||
+      !encode_kv_map(&tmv, a.v, a.B, a.H, T, D, S, a.sb, a.sh, a.st))
+    return cudaErrorInvalidValue;
+  k_quant<D, S><<<(unsigned)grid, QG::TEAMS * 128, QG::total, st>>>(a, tmk, tmv);
   return cudaGetLastError();
 }
 
