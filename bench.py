@@ -29,6 +29,8 @@ import sys
 import threading
 import time
 
+from dataclasses import replace
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -114,12 +116,19 @@ class Workload:
     scratch buffers of the path.  Under a sequence split each rank quantizes and
     decodes its share of every width segment (wq_shard_slots)."""
 
-    def __init__(self, cfg, device, rank=0, world=1, n_gen=None, merge="peer"):
+    def __init__(self, cfg, device, rank=0, world=1, n_gen=None, merge="peer", heads=None):
         import torch
         from paper_2605_02262_b200 import synth, wq
         self.torch, self.wq = torch, wq
         self.cfg, self.dev, self.rank, self.world = cfg, device, rank, world
         m = cfg.model
+        # P1 head sharding: this rank's kv heads [h0, h1) of every request (the inputs are
+        # generated for the full model shape and sliced, so the data is the full job's)
+        h0, h1 = heads if heads is not None else (0, m.H)
+        if (h0, h1) != (0, m.H):
+            grp = m.Hq // m.H
+            m = replace(m, H=h1 - h0, Hq=(h1 - h0) * grp)
+        self.heads = (h0, h1)
         self.m = m
         self.L = cfg.layers
         self.n_gen = cfg.n_gen if n_gen is None else n_gen
@@ -131,14 +140,19 @@ class Workload:
         # inputs
         self.vis, self.txt = synth.embeddings(B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, device)
         self.K, self.V, self.kr, self.vr = [], [], [], []
+        hs = slice(h0, h1)
+        qs = slice(h0 * (m.Hq // m.H), h1 * (m.Hq // m.H))
         for l in range(self.L):
             K, V, kr, vr, rest_len = synth.layer_tensors(cfg, l, device)
+            if (h0, h1) != (0, cfg.model.H):
+                K, V, kr, vr = (x[:, hs].contiguous() for x in (K, V, kr, vr))
             self.K.append(K); self.V.append(V); self.kr.append(kr); self.vr.append(vr)
         base = int(rest_len[0].item())
         steps = [[base + t + 1] * B for t in range(self.n_gen)]
         self.rest_len = torch.tensor(steps, dtype=torch.int32, device=device)       # [n_gen][B]
         self.rest_zero = torch.zeros((B,), dtype=torch.int32, device=device)
-        self.q = torch.stack([torch.stack([synth.queries(B, m.Hq, m.H, m.d, cfg.seed, l, t, device)
+        self.q = torch.stack([torch.stack([synth.queries(B, cfg.model.Hq, cfg.model.H, m.d, cfg.seed, l, t,
+                                                         device)[:, qs].contiguous()
                                            for l in range(self.L)]) for t in range(self.n_gen)])
         # path buffers
         W = cfg.W
@@ -338,16 +352,17 @@ def run_wq(args, rank, world, local_rank):
     if args.layers:
         cfg = cfg.with_(layers=args.layers)
     # multi-GPU mode: P2 sequence split (long video, C5) with the fused
-    # cross-GPU merge, or P1 batch sharding (C2-C4): rank r takes requests
-    # [B r/N, B (r+1)/N) whole -- independent units, no collective on the data path
-    mode = args.parallel if args.parallel != "auto" else ("seqsplit" if cfg.idx == 5 else "batch")
-    if world > 1 and mode == "batch":
-        from paper_2605_02262_b200.parallel import batch_shard
-        b0, b1 = batch_shard(cfg.B, world, rank)
-        assert b1 > b0, f"batch sharding needs B >= N ({cfg.B} < {world})"
+    # cross-GPU merge, or P1 over (request, kv-head) units (C2-C4, or --parallel units):
+    # rank r takes whole requests, or kv heads of one request when ranks outnumber
+    # requests -- independent units, no collective on the data path
+    mode = args.parallel if args.parallel != "auto" else ("seqsplit" if cfg.idx == 5 else "units")
+    if world > 1 and mode in ("batch", "units"):
+        from paper_2605_02262_b200.parallel import unit_shard
+        b0, b1, h0, h1 = unit_shard(cfg.B, cfg.model.H, world, rank)
         cfg_global = cfg
         cfg = cfg.with_(B=b1 - b0)
-        w = Workload(cfg, dev, 0, 1, n_gen=args.n_gen)
+        w = Workload(cfg, dev, 0, 1, n_gen=args.n_gen, heads=(h0, h1))
+        mode = "batch" if (h0, h1) == (0, cfg.model.H) else "heads"
         w_world = 1
     else:
         cfg_global = cfg
@@ -726,8 +741,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host (no CUDA graphs)")
     ap.add_argument("--no-ablation", action="store_true", help="skip the T8/T9/T11 ablation measurements")
-    ap.add_argument("--parallel", default="auto", choices=["auto", "seqsplit", "batch"],
-                    help="N > 1: sequence split (P2, default for C5) or batch sharding (P1, default otherwise)")
+    ap.add_argument("--parallel", default="auto", choices=["auto", "seqsplit", "batch", "units"],
+                    help="N > 1: sequence split (P2, default for C5) or (request, kv-head) unit sharding "
+                         "(P1: whole requests, or kv heads of one request; default otherwise)")
     ap.add_argument("--merge", default="peer", choices=["peer", "nccl"],
                     help="N > 1: fused peer-memory LSE merge in the decode kernel, or NCCL all-gather + merge")
     args = ap.parse_args()

@@ -1,7 +1,8 @@
 """Multi-GPU plumbing of the hot path.
 
-* P1 -- independent units: requests (and kv heads) are sharded across ranks with
-  no collective on the data path (batch_shard).
+* P1 -- independent units: (request, kv-head) units are sharded across ranks with
+  no collective on the data path (unit_shard: whole requests = batch_shard, or kv heads of
+  one request when there are more ranks than requests).
 * P2 -- long-video sequence split: rank r of G keeps chunk r of every width
   segment of the reordered slot list (``wq_shard_slots`` on the device; the same
   bounds as ``segment_chunk`` here), decodes it into (m, l, o) partials, and the
@@ -40,6 +41,25 @@ def shard_plan(seg_off_b, G: int, r: int):
 def batch_shard(B: int, G: int, r: int) -> tuple[int, int]:
     """Contiguous request range of rank r under P1 (requests are independent units)."""
     return (B * r) // G, (B * (r + 1)) // G
+
+
+def unit_shard(B: int, H: int, G: int, r: int) -> tuple[int, int, int, int]:
+    """P1 over (request, kv-head) units (north star: "partitioned ... by KV head and batch"):
+    rank r takes the b-major unit range [U r/G, U (r+1)/G), U = B*H, returned as
+    (b0, b1, h0, h1) = requests [b0, b1) x kv heads [h0, h1).  Supported when every rank's
+    range is whole requests (then h0, h1 = 0, H: batch sharding) or kv heads of ONE request
+    (head sharding, e.g. B = 4, H = 4 on 8 GPUs: two heads each) -- the ranges a [B][H]
+    geometry slice can express.  Units are independent: no collective on the data path."""
+    U = B * H
+    u0, u1 = (U * r) // G, (U * (r + 1)) // G
+    if u1 <= u0:
+        raise ValueError(f"rank {r} of {G} gets no (request, head) unit (B*H = {U})")
+    if u0 % H == 0 and u1 % H == 0:
+        return u0 // H, u1 // H, 0, H
+    if u0 // H == (u1 - 1) // H:
+        b = u0 // H
+        return b, b + 1, u0 - b * H, u1 - b * H
+    raise ValueError(f"units [{u0}, {u1}) of rank {r} span partial requests (B={B}, H={H}, G={G})")
 
 
 def all_gather_partials(part: torch.Tensor, group=None) -> torch.Tensor:

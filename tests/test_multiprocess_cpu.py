@@ -99,3 +99,21 @@ def test_batch_shard_covers_requests():
                 a, e = parallel.batch_shard(B, G, r)
                 got += list(range(a, e))
             assert got == list(range(B))
+
+
+def test_unit_shard_partitions_request_head_units():
+    """P1 over (request, kv-head) units: the ranks' (b, h) ranges partition the B*H units
+    (C3 at 2/4/8 GPUs = whole requests; C5 (B=4, H=4) at 8 GPUs = two heads of one request)."""
+    for B, H, G in [(16, 4, 2), (16, 4, 4), (16, 4, 8), (4, 4, 8), (4, 4, 16), (8, 2, 16), (64, 4, 8), (1, 4, 2),
+                    (2, 4, 8)]:
+        seen = []
+        for r in range(G):
+            b0, b1, h0, h1 = parallel.unit_shard(B, H, G, r)
+            assert 0 <= b0 < b1 <= B and 0 <= h0 < h1 <= H
+            if b1 - b0 > 1:
+                assert (h0, h1) == (0, H)
+            seen += [(b, h) for b in range(b0, b1) for h in range(h0, h1)]
+        assert sorted(seen) == [(b, h) for b in range(B) for h in range(H)], (B, H, G)
+        assert len(seen) == len(set(seen))
+    with pytest.raises(ValueError):
+        parallel.unit_shard(3, 4, 5, 3)          # units [7, 9) straddle requests 1 and 2
