@@ -1,3 +1,1 @@
-export WQ_BENCH_BACKEND=gloo
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29611 bench.py --gpus 8 --config C5 --parallel units --layers 2 --n-gen 2 --steps 2 --warmup 1 --no-e2e --no-cpu --no-ablation > gpurun_out/p1_heads.log 2>&1; echo h=$? > gpurun_out/rc15.txt
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29612 bench.py --gpus 2 --config C3 --layers 2 --n-gen 2 --steps 2 --warmup 1 --no-e2e --no-cpu --no-ablation > gpurun_out/p1_batch.log 2>&1; echo b=$? >> gpurun_out/rc15.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "layer_scores or scores_parity or pearson" > gpurun_out/t17.log 2>&1; echo t17=$? > gpurun_out/rc16.txt

@@ -157,6 +157,22 @@ wq_status wq_window_scores_ex(const void *vis, int64_t vis_row_stride, int64_t v
                               int32_t B, int32_t M, int32_t N, int32_t D, int32_t S, int32_t metric,
                               double *scores, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Per-layer scorer (the "visual keys x text queries" wording of
+ * P:274 and Alg.1 line 11's E_w^i with a layer index; reading Q36).  For layer i:
+ *   scores[b][w] = 1/(S*N) * sum_{j<N} sum_{k<S} cos(t_j, v_{w*S+k})
+ * with v_t = concat over kv heads h of K[b][h][vis_off + t][:] (post-RoPE keys, D = H*d)
+ * and t_j = concat over h of (1/g) sum_{g'<g} Q[b][h*g + g'][j][:] (the text tokens'
+ * queries averaged over each GQA group, g = Hq/H), evaluated like wq_window_scores (pooled
+ * identity, fp64).  k: fp16, element (b, h, t, c) at k[b*k_strides[0] + h*k_strides[1] +
+ * t*k_strides[2] + c] (rows 16-byte aligned); q_text: fp16, element (b, hq, j, c) at
+ * q_text[b*q_strides[0] + hq*q_strides[1] + j*q_strides[2] + c].  scores fp64 [B][W].
+ * workspace: wq_window_scores_workspace(B, H*d) bytes.
+ * Errors: WQ_ESHAPE (S, M < S, H*d > 4096, Hq % H), WQ_EUNSUPPORTED (d not 64/128). */
+wq_status wq_window_scores_layer(const void *k, const int64_t k_strides[3], int32_t vis_off, const void *q_text,
+                                 const int64_t q_strides[3], int32_t B, int32_t H, int32_t Hq, int32_t d,
+                                 int32_t M, int32_t N, int32_t S, double *scores, void *workspace,
+                                 size_t workspace_bytes, void *stream);
+
 /* Bit assignment + permutation (Alg.1 lines 8-16, P:313, P:316-322, P:395;
  * Alg.2 lines 2-13).  For each layer l and request b:
  *   1. rank[b][w]: position of window w in (-score, w) order (0 = most similar, Q7)

@@ -71,6 +71,7 @@ def lib():
                 "wqo_window_score": (F64, [P, I64, P, I64, I32, I32, I32, I32]),
                 "wqo_window_scores": (None, [P, I64, I64, P, I64, I64, I32, I32, I32, I32, I32, P]),
                 "wqo_window_scores_pearson": (None, [P, I64, I64, P, I64, I64, I32, I32, I32, I32, I32, P]),
+                "wqo_window_scores_layer": (None, [P, P, I32, P, P, I32, I32, I32, I32, I32, I32, I32, P]),
                 "wqo_assign_bits": (C.c_int, [P, P, I32, C.POINTER(Geom), F64, I32, I32, P, P, P, P]),
                 "wqo_record_bytes": (I64, [I32, I32, I32]),
                 "wqo_packed_bytes": (I64, [C.POINTER(Geom), P, I32]),
@@ -158,6 +159,18 @@ def window_scores_pearson(vis: np.ndarray, txt: np.ndarray, S: int) -> np.ndarra
     N = txt.shape[1]
     out = np.zeros((B, M // S), np.float64)
     lib().wqo_window_scores_pearson(_p(vis), D, M * D, _p(txt), D, N * D, B, M, N, D, S, _p(out))
+    return out
+
+
+def window_scores_layer(k: np.ndarray, vis_off: int, q_text: np.ndarray, M: int, S: int) -> np.ndarray:
+    """Per-layer scorer (reading Q36): k fp16 [B][H][T][d], q_text fp16 [B][Hq][N][d] -> [B][M//S]."""
+    k, q_text = _u16(k), _u16(q_text)
+    B, H, T, d = k.shape
+    Hq, N = q_text.shape[1], q_text.shape[2]
+    ks = np.array([H * T * d, T * d, d], np.int64)
+    qs = np.array([Hq * N * d, N * d, d], np.int64)
+    out = np.zeros((B, M // S), np.float64)
+    lib().wqo_window_scores_layer(_p(k), _p(ks), vis_off, _p(q_text), _p(qs), B, H, Hq, d, M, N, S, _p(out))
     return out
 
 

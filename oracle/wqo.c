@@ -736,3 +736,45 @@ void wqo_window_scores_pearson(const uint16_t *vis, int64_t vrs, int64_t vbs,
       scores[(int64_t)b * W + w] = sum / ((double)S * (double)N);
     }
 }
+
+/* Per-layer scorer (reading Q36): Eq.8 where the visual vector of
+ * token t is the concatenation over the H kv heads of its post-RoPE key, K[b][h][vis_off+t][:],
+ * and the text vector of text token j the concatenation over h of the mean of the GQA
+ * group's queries, (1/g) sum_{g'} Q[b][h g + g'][j][:].  Literal double sum over the S*N
+ * pairs, every vector built in fp64, zero-norm vectors contribute 0 (Q5). */
+void wqo_window_scores_layer(const uint16_t *k, const int64_t ks[3], int32_t vis_off, const uint16_t *qt,
+                             const int64_t qs[3], int32_t B, int32_t H, int32_t Hq, int32_t d, int32_t M,
+                             int32_t N, int32_t S, double *scores) {
+  int W = M / S, D = H * d, grp = Hq / H;
+#pragma omp parallel for collapse(2) schedule(dynamic)
+  for (int b = 0; b < B; b++)
+    for (int w = 0; w < W; w++) {
+      double *tv = (double *)malloc(sizeof(double) * (size_t)D);
+      double *vv = (double *)malloc(sizeof(double) * (size_t)D);
+      double sum = 0.0;
+      for (int j = 0; j < N; j++) {
+        for (int c = 0; c < D; c++) {
+          int h = c / d, cc = c % d;
+          double acc = 0.0;
+          for (int gq = 0; gq < grp; gq++)
+            acc += wqo_f16_to_f64(qt[b * qs[0] + (int64_t)(h * grp + gq) * qs[1] + (int64_t)j * qs[2] + cc]);
+          tv[c] = acc / (double)grp;
+        }
+        double nt = 0.0;
+        for (int c = 0; c < D; c++) nt += tv[c] * tv[c];
+        nt = sqrt(nt);
+        for (int kk = 0; kk < S; kk++) {
+          int t = vis_off + w * S + kk;
+          for (int c = 0; c < D; c++)
+            vv[c] = wqo_f16_to_f64(k[b * ks[0] + (int64_t)(c / d) * ks[1] + (int64_t)t * ks[2] + c % d]);
+          double nv = 0.0, dot = 0.0;
+          for (int c = 0; c < D; c++) { nv += vv[c] * vv[c]; dot += tv[c] * vv[c]; }
+          nv = sqrt(nv);
+          if (nt == 0.0 || nv == 0.0) continue;
+          sum += dot / (nt * nv);
+        }
+      }
+      scores[(int64_t)b * W + w] = sum / ((double)S * (double)N);
+      free(tv); free(vv);
+    }
+}

@@ -57,6 +57,13 @@ void   wqo_window_scores_pearson(const uint16_t *vis, int64_t vrs, int64_t vbs,
                                  int32_t B, int32_t M, int32_t N, int32_t D, int32_t S,
                                  double *scores);
 
+/* Per-layer scorer (reading Q36): Eq.8 on the layer's post-RoPE
+ * visual keys (kv heads concatenated) against the text tokens' queries averaged over each
+ * GQA group; k [B][H][T][d] and q_text [B][Hq][N][d] with element strides ks / qs (b, h, t). */
+void wqo_window_scores_layer(const uint16_t *k, const int64_t ks[3], int32_t vis_off, const uint16_t *qt,
+                             const int64_t qs[3], int32_t B, int32_t H, int32_t Hq, int32_t d, int32_t M,
+                             int32_t N, int32_t S, double *scores);
+
 /* Alg.1 band/pin/vote + budget + Alg.2 partition.  Returns 0, or 3 if the
  * budget is infeasible. */
 int wqo_assign_bits(const double *scores, const double *thr, int32_t L,

@@ -123,6 +123,32 @@ wq_status wq_window_scores(const void *vis, int64_t vrs, int64_t vbs, const void
                              workspace_bytes, stream);
 }
 
+wq_status wq_window_scores_layer(const void *k, const int64_t k_strides[3], int32_t vis_off, const void *q_text,
+                                 const int64_t q_strides[3], int32_t B, int32_t H, int32_t Hq, int32_t d, int32_t M,
+                                 int32_t N, int32_t S, double *scores, void *workspace, size_t workspace_bytes,
+                                 void *stream) {
+  if (!k || !k_strides || !q_text || !q_strides || !scores || !workspace) return fail(WQ_EINVAL, "NULL pointer");
+  if (!(S == 16 || S == 32 || S == 64 || S == 128)) return fail(WQ_ESHAPE, "S=%d not in {16,32,64,128}", S);
+  if (B < 1 || N < 1 || M < S || vis_off < 0) return fail(WQ_ESHAPE, "B=%d N=%d M=%d vis_off=%d (need M >= S=%d)",
+                                                       B, N, M, vis_off, S);
+  if (!(d == 64 || d == 128)) return fail(WQ_EUNSUPPORTED, "head dim d=%d not in {64,128}", d);
+  if (H < 1 || Hq < H || Hq % H) return fail(WQ_ESHAPE, "Hq=%d not a multiple of H=%d", Hq, H);
+  const int D = H * d;
+  if (D > 4096) return fail(WQ_ESHAPE, "H*d=%d > 4096", D);
+  if (k_strides[0] % 8 || k_strides[1] % 8 || k_strides[2] % 8 || !aligned16(k))
+    return fail(WQ_EINVAL, "K rows must be 16-byte aligned (strides multiple of 8 elements)");
+  if (workspace_bytes < (size_t)B * D * sizeof(double)) return fail(WQ_EINVAL, "workspace too small");
+  double *tbar = reinterpret_cast<double *>(workspace);
+  wq_status s = cuda_status(wq::launch_text_pool_q((const __half *)q_text, q_strides[0], q_strides[1], q_strides[2],
+                                                   B, N, H, Hq / H, d, tbar, S_(stream)),
+                            "text query pool");
+  if (s != WQ_OK) return s;
+  const __half *vis = (const __half *)k + (int64_t)vis_off * k_strides[2];
+  return cuda_status(wq::launch_window_scores(vis, k_strides[2], k_strides[0], B, M, N, D, S, tbar, scores, 0,
+                                              S_(stream), d, k_strides[1]),
+                     "layer window scores");
+}
+
 wq_status wq_assign_bits(const double *scores, const double *thr_host, int32_t L, const wq_geom *g,
                          const wq_assign_opts *opts, uint8_t *bits, int32_t *rank, int32_t *perm,
                          int32_t *seg_off, void *stream) {

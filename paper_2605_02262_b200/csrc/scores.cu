@@ -88,11 +88,13 @@ __global__ void __launch_bounds__(ST) k_text_pool(const __half *__restrict__ txt
   for (int c = threadIdx.x; c < D; c += ST) tbar[(int64_t)b * D + c] = pooled[c];
 }
 
+// A visual "row" is D elements; with head-split rows (the per-layer scorer) element c lives
+// at row + (c / dh) * hs + c % dh (dh = head dim, hs = head stride); dh = D, hs = 0 otherwise.
 template <int NC, bool CENTER>  // 16-byte chunks per thread per row: ceil(D / 8 / ST); CENTER: Pearson
 __global__ void __launch_bounds__(ST, WQ_SC_MINB) k_window_scores(const __half *__restrict__ vis, int64_t vrs,
                                                       int64_t vbs, int M, int N, int D, int S,
                                                       const double *__restrict__ tbar,
-                                                      double *__restrict__ scores) {
+                                                      double *__restrict__ scores, int dh, int64_t hs) {
   constexpr int RB = WQ_SC_RB;  // rows per batch
   __shared__ double red[4 * RB];
   const int w = blockIdx.x, b = blockIdx.y, W = gridDim.x, tid = threadIdx.x;
@@ -110,7 +112,9 @@ __global__ void __launch_bounds__(ST, WQ_SC_MINB) k_window_scores(const __half *
 #pragma unroll
       for (int i = 0; i < NC; i++) {
         int k = tid + ST * i;
-        raw[r][i] = k < nchunk ? __ldcs(reinterpret_cast<const uint4 *>(base + (int64_t)(r0 + r) * vrs) + k)
+        const int c = 8 * k;                                // first element of the chunk
+        raw[r][i] = k < nchunk ? __ldcs(reinterpret_cast<const uint4 *>(base + (int64_t)(r0 + r) * vrs +
+                                                                      (int64_t)(c / dh) * hs + c % dh))
                                : make_uint4(0, 0, 0, 0);
       }
     double mu[RB];
@@ -180,6 +184,45 @@ __global__ void __launch_bounds__(ST, WQ_SC_MINB) k_window_scores(const __half *
   if (tid == 0) scores[(int64_t)b * W + w] = dot[0] / ((double)S * (double)N);
 }
 
+// Per-layer scorer text side (reading Q36): text row j of request b is the concatenation
+// over kv heads h of the mean of its GQA group's queries, (1/g) sum_{g'} Q[b][h g + g'][j][:]
+// (D = H d, fp64); tbar[b][:] = sum_j row_j / ||row_j|| (a zero row contributes 0).
+__global__ void __launch_bounds__(ST) k_text_pool_q(const __half *__restrict__ qt, int64_t qsb, int64_t qsh,
+                                                    int64_t qsj, int N, int H, int grp, int d,
+                                                    double *__restrict__ tbar) {
+  extern __shared__ double sh[];                 // pooled [D], row [D]
+  __shared__ double red[4];
+  const int b = blockIdx.x, D = H * d;
+  double *pooled = sh, *row = sh + D;
+  for (int c = threadIdx.x; c < D; c += ST) pooled[c] = 0.0;
+  for (int j = 0; j < N; j++) {
+    double ss[1] = {0.0};
+    for (int c = threadIdx.x; c < D; c += ST) {
+      const int h = c / d, cc = c - h * d;
+      double acc = 0.0;
+      for (int gq = 0; gq < grp; gq++)
+        acc += (double)__half2float(qt[b * qsb + (int64_t)(h * grp + gq) * qsh + (int64_t)j * qsj + cc]);
+      const double x = acc / (double)grp;
+      row[c] = x;
+      ss[0] = fma(x, x, ss[0]);
+    }
+    block_sum<1>(ss, red);
+    const double inv = ss[0] > 0.0 ? 1.0 / sqrt(ss[0]) : 0.0;
+    for (int c = threadIdx.x; c < D; c += ST) pooled[c] = fma(row[c], inv, pooled[c]);
+    __syncthreads();
+  }
+  for (int c = threadIdx.x; c < D; c += ST) tbar[(int64_t)b * D + c] = pooled[c];
+}
+
+cudaError_t launch_text_pool_q(const __half *qt, int64_t qsb, int64_t qsh, int64_t qsj, int B, int N, int H,
+                               int grp, int d, double *tbar, cudaStream_t st) {
+  const size_t smem = (size_t)2 * H * d * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_text_pool_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_text_pool_q<<<B, ST, smem, st>>>(qt, qsb, qsh, qsj, N, H, grp, d, tbar);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_text_pool(const __half *txt, int64_t trs, int64_t tbs, int B, int N, int D,
                              double *tbar, int metric, cudaStream_t st) {
   size_t smem = (size_t)D * sizeof(double);
@@ -191,14 +234,16 @@ cudaError_t launch_text_pool(const __half *txt, int64_t trs, int64_t tbs, int B,
 }
 
 cudaError_t launch_window_scores(const __half *vis, int64_t vrs, int64_t vbs, int B, int M, int N,
-                                 int D, int S, const double *tbar, double *scores, int metric, cudaStream_t st) {
+                                 int D, int S, const double *tbar, double *scores, int metric, cudaStream_t st,
+                                 int dh, int64_t hs) {
   int W = M / S;
   int nc = (D / 8 + ST - 1) / ST;
   dim3 grid(W, B);
+  if (dh <= 0) { dh = D; hs = 0; }
 #define WQ_WS(NCV)                                                                                   \
   case NCV:                                                                                          \
-    if (metric == 1) k_window_scores<NCV, true><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores); \
-    else k_window_scores<NCV, false><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores);          \
+    if (metric == 1) k_window_scores<NCV, true><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores, dh, hs); \
+    else k_window_scores<NCV, false><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores, dh, hs);          \
     break;
   switch (nc) {
     WQ_WS(1) WQ_WS(2) WQ_WS(3) WQ_WS(4)

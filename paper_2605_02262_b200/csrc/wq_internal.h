@@ -18,7 +18,10 @@ struct AssignParams {
 cudaError_t launch_text_pool(const __half *txt, int64_t trs, int64_t tbs, int B, int N, int D,
                              double *tbar, int metric, cudaStream_t st);
 cudaError_t launch_window_scores(const __half *vis, int64_t vrs, int64_t vbs, int B, int M, int N,
-                                 int D, int S, const double *tbar, double *scores, int metric, cudaStream_t st);
+                                 int D, int S, const double *tbar, double *scores, int metric, cudaStream_t st,
+                                 int dh = 0, int64_t hs = 0);
+cudaError_t launch_text_pool_q(const __half *qt, int64_t qsb, int64_t qsh, int64_t qsj, int B, int N, int H,
+                               int grp, int d, double *tbar, cudaStream_t st);
 
 cudaError_t launch_rank(const double *scores, int B, int W, int32_t *rank, cudaStream_t st);
 cudaError_t launch_assign(const double *scores, const AssignParams &p, uint8_t *bits, int32_t *perm,

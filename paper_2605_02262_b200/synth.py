@@ -139,3 +139,12 @@ def layer_tensors(cfg, layer: int, device="cpu", B=None):
         vr[:, :, :t] = V[:, :, cfg.M - t:]
     rest_len = torch.full((B,), t + cfg.n_text, dtype=torch.int32, device=device)
     return K, V, kr, vr, rest_len
+
+
+def text_queries(B: int, Hq: int, N: int, d: int, seed: int, layer: int, device="cpu"):
+    """Query states of the N text tokens of one layer, [B][Hq][N][d] fp16 (the per-layer
+    scorer's text side, include/wq.h wq_window_scores_layer): N(0, 1) plus a common
+    per-request direction so that text and visual keys correlate like the embeddings."""
+    g = _gen(seed * 1009 + 31 * layer + 13, device)
+    u = _randn((B, 1, 1, d), g, device)
+    return (0.7 * _randn((B, Hq, N, d), g, device) + u).half().contiguous()

@@ -63,6 +63,7 @@ def load(build_if_missing: bool = True):
         "wq_window_scores_workspace": [I32, I32, P],
         "wq_window_scores": [P, I64, I64, P, I64, I64, I32, I32, I32, I32, I32, P, P, SZ, P],
         "wq_window_scores_ex": [P, I64, I64, P, I64, I64, I32, I32, I32, I32, I32, I32, P, P, SZ, P],
+        "wq_window_scores_layer": [P, P, I32, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, SZ, P],
         "wq_assign_bits": [P, P, I32, C.POINTER(Geom), C.POINTER(AssignOpts), P, P, P, P, P],
         "wq_packed_bytes": [C.POINTER(Geom), P, I32, P],
         "wq_layer_layout": [C.POINTER(Geom), P, P, P],
@@ -97,7 +98,8 @@ def load(build_if_missing: bool = True):
 
 
 def exported_symbols():
-    return ["wq_thresholds", "wq_window_scores_workspace", "wq_window_scores", "wq_window_scores_ex", "wq_assign_bits",
+    return ["wq_thresholds", "wq_window_scores_workspace", "wq_window_scores", "wq_window_scores_ex",
+            "wq_window_scores_layer", "wq_assign_bits",
             "wq_packed_bytes", "wq_layer_layout", "wq_reorder_quantize_pack", "wq_decode_workspace",
             "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_dequant_layout", "wq_dequantize_image",
             "wq_unreordered_layout", "wq_unreorder_image", "wq_decode_attention_unreordered",
@@ -358,3 +360,20 @@ def wq_decode_attention_peer_emulated(ranks, g: Geom, sm_scale: float, peer_ptrs
         G, arr("q"), arr("packed"), arr("offs"), arr("seg_off"), C.byref(g), arr("k_rest"), arr("v_rest"), rs,
         arr("rest_len"), R_max, float(sm_scale), arr("out"), arr("workspace"), ranks[0]["workspace"].numel(),
         _ptr(peer_ptrs), loc, C.c_uint32(epoch), _stream(stream)))
+
+
+def wq_window_scores_layer(k: torch.Tensor, vis_off: int, q_text: torch.Tensor, M: int, S: int, scores=None,
+                           workspace=None, stream=None) -> torch.Tensor:
+    """Per-layer scorer (include/wq.h): k fp16 [B][H][T][d] (any strides, rows contiguous),
+    q_text fp16 [B][Hq][N][d] -> scores fp64 [B][M // S]."""
+    B, H, T, d = k.shape
+    Hq, N = q_text.shape[1], q_text.shape[2]
+    if scores is None:
+        scores = torch.empty((B, M // S), dtype=torch.float64, device=k.device)
+    if workspace is None:
+        workspace = torch.empty(wq_window_scores_workspace(B, H * d), dtype=torch.uint8, device=k.device)
+    ks = (C.c_int64 * 3)(k.stride(0), k.stride(1), k.stride(2))
+    qs = (C.c_int64 * 3)(q_text.stride(0), q_text.stride(1), q_text.stride(2))
+    _check(load().wq_window_scores_layer(_ptr(k), ks, int(vis_off), _ptr(q_text), qs, B, H, Hq, d, int(M), N, int(S),
+                                         _ptr(scores), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return scores

@@ -607,3 +607,38 @@ def test_ablation_paths_full_size_c5(orc):
     assert np.array_equal(pk16.cpu().numpy(), rimg[:int(roffs16[-1])])
     r16 = _decode_ref(orc, sub, gb, ob16, pk16, perm[b:b + 1], seg16[b:b + 1], sm)[0]
     assert rel_err(out_16[b:b + 1].float().cpu().numpy(), r16) <= ATTN_TOL
+
+
+@pytest.mark.parametrize("B,H,Hq,d,S,W,tail,N,vis_off", [(2, 2, 14, 64, 16, 9, 5, 8, 3), (1, 4, 28, 128, 32, 12, 7, 32, 0),
+                                                      (3, 4, 8, 128, 64, 4, 0, 5, 16)])
+def test_layer_scores_parity(orc, B, H, Hq, d, S, W, tail, N, vis_off):
+    """Per-layer scorer (§8(f) row 4, reading Q36): post-RoPE visual keys (kv heads
+    concatenated, read in place through the head stride) against the GQA-averaged text
+    queries, 1e-12 absolute against the literal oracle."""
+    M = W * S + tail
+    K, _ = synth.kv_layer(B, H, vis_off + M, d, S, 70 + d, 1, "cuda")
+    qt = synth.text_queries(B, Hq, N, d, 70 + d, 1, "cuda")
+    got = wq.wq_window_scores_layer(K, vis_off, qt, M, S)
+    torch.cuda.synchronize()
+    ref = orc.window_scores_layer(K.cpu().numpy(), vis_off, qt.cpu().numpy(), M, S)
+    assert np.max(np.abs(got.cpu().numpy() - ref)) <= 1e-12
+
+
+def test_layer_scores_c5_geometry(orc):
+    """The layer scorer at the full C5 layer shape (B = 4, H = 4, d = 128, 50,176 visual
+    tokens, N = 32): request 1 against the oracle (every window), bit-exact assignment
+    from those scores."""
+    cfg = configs.CONFIGS["C5"]
+    m = cfg.model
+    K, V, kr, vr, rest_len = synth.layer_tensors(cfg, 3, "cuda")
+    del V, kr, vr
+    qt = synth.text_queries(cfg.B, m.Hq, cfg.n_text, m.d, cfg.seed, 3, "cuda")
+    got = wq.wq_window_scores_layer(K, 0, qt, cfg.M, cfg.S)
+    torch.cuda.synchronize()
+    ref = orc.window_scores_layer(K[1:2].cpu().numpy(), 0, qt[1:2].cpu().numpy(), cfg.M, cfg.S)
+    assert np.max(np.abs(got[1:2].cpu().numpy() - ref)) <= 1e-12
+    thr = orc.thresholds([0.5], cfg.alpha, 4)
+    g = wq.geom(cfg.B, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
+    gpu, oref = _assign_both(orc, got, thr, g)
+    for a_, b_ in zip(gpu, oref):
+        assert np.array_equal(a_, b_)

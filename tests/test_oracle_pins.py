@@ -753,3 +753,45 @@ def test_alpha_sweep_trend(orc):
             assert n[0] <= prev[0] and n[2] <= prev[2] and n[1] >= prev[1]
         prev = n
     assert prev[1] > prev[0] and prev[1] > prev[2]
+
+
+# --------------------------------------------------------------------------------------
+# Per-layer scorer (reading Q36)
+# --------------------------------------------------------------------------------------
+def test_layer_scorer_reduces_to_embedding_scorer(orc):
+    """H = Hq = 1: the per-layer scorer IS Eq.8 on the key rows and the query rows (the
+    pinned embedding scorer); with H kv heads and identical queries inside each GQA group,
+    it equals the embedding scorer on the head-concatenated rows (group mean of equal rows)."""
+    rng = np.random.default_rng(21)
+    B, T, d, N, S, vis_off = 2, 7 + 5 * 16, 64, 6, 16, 7
+    M = T - vis_off
+    k = rng.standard_normal((B, 1, T, d)).astype(np.float16)
+    q = rng.standard_normal((B, 1, N, d)).astype(np.float16)
+    got = orc.window_scores_layer(k, vis_off, q, M, S)
+    ref = orc.window_scores(np.ascontiguousarray(k[:, 0, vis_off:]), np.ascontiguousarray(q[:, 0]), S)
+    assert np.max(np.abs(got - ref)) <= 1e-13
+    H, grp = 3, 4
+    k = rng.standard_normal((B, H, T, d)).astype(np.float16)
+    qh = rng.standard_normal((B, H, N, d)).astype(np.float16)
+    q = np.repeat(qh, grp, axis=1)                                  # identical queries in a group
+    got = orc.window_scores_layer(k, vis_off, q, M, S)
+    vis = np.ascontiguousarray(k[:, :, vis_off:].transpose(0, 2, 1, 3).reshape(B, M, H * d))
+    txt = np.ascontiguousarray(qh.transpose(0, 2, 1, 3).reshape(B, N, H * d))
+    assert np.max(np.abs(got - orc.window_scores(vis, txt, S))) <= 1e-12
+
+
+def test_layer_scorer_invariants(orc):
+    """Permuting the kv heads (keys and their query groups together) and scaling a key
+    row by c > 0 leave the scores unchanged; a query group and its mean give one score."""
+    rng = np.random.default_rng(22)
+    B, H, grp, T, d, N, S = 1, 4, 2, 4 * 32, 128, 5, 32
+    k = rng.standard_normal((B, H, T, d)).astype(np.float16)
+    q = rng.standard_normal((B, H * grp, N, d)).astype(np.float16)
+    base = orc.window_scores_layer(k, 0, q, T, S)
+    perm = [2, 0, 3, 1]
+    qperm = np.concatenate([q[:, h * grp:(h + 1) * grp] for h in perm], axis=1)
+    assert np.max(np.abs(orc.window_scores_layer(np.ascontiguousarray(k[:, perm]), 0, np.ascontiguousarray(qperm),
+                                                 T, S) - base)) <= 1e-12
+    k2 = k.copy()
+    k2[:, :, 5] = (k2[:, :, 5].astype(np.float32) * 2).astype(np.float16)     # whole token row x2 (exact)
+    assert np.max(np.abs(orc.window_scores_layer(k2, 0, q, T, S) - base)) <= 1e-12
