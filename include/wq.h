@@ -195,6 +195,25 @@ wq_status wq_assign_bits(const double *scores, const double *thr_host, int32_t L
                          uint8_t *bits, int32_t *rank, int32_t *perm, int32_t *seg_off,
                          void *stream);
 
+/* The whole search module in ONE launch (the fused scorer -> assign
+ * kernel): wq_window_scores_ex (metric WQ_SIM_COSINE / WQ_SIM_PEARSON) over vis/txt of
+ * request geometry g (B, M, S; widths), then wq_assign_bits for L layers -- the same
+ * results (scores within rounding order: identical code, identical fixed reduction trees;
+ * ranks, bits, perms, seg_off bit-identical).  A cooperative persistent grid: phases
+ * (text pool, window scores, one rank sort per request, assignment) separated by grid-wide
+ * barriers; the per-(layer, request) assignment reuses its request's single sort.
+ * vis: fp16 rows as wq_window_scores (D channels, row/batch strides), txt likewise with N
+ * rows.  Outputs as wq_window_scores / wq_assign_bits (rank may be NULL).
+ * workspace: wq_search_workspace(B, D, W = M/S) bytes (pooled text + rank orders).
+ * Errors: as wq_window_scores and wq_assign_bits; WQ_ECUDA if the cooperative grid cannot
+ * be made co-resident. */
+wq_status wq_search_workspace(int32_t B, int32_t D, int32_t W, size_t *bytes_host);
+wq_status wq_search(const void *vis, int64_t vis_row_stride, int64_t vis_batch_stride, const void *txt,
+                    int64_t txt_row_stride, int64_t txt_batch_stride, int32_t N, int32_t D, int32_t metric,
+                    const double *thr_host, int32_t L, const wq_geom *g, const wq_assign_opts *opts,
+                    double *scores, uint8_t *bits, int32_t *rank, int32_t *perm, int32_t *seg_off,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
 /* Bytes of one (b, h) image holding n_per_class_host[k] windows of class k
  * ({2,4,8,16}[k]) under contract D-1.  HOST.  With code_bytes_only = 1 the
  * params are not counted and the result is the paper's accounting. */

@@ -15,7 +15,7 @@ VARIANT = os.environ.get("WQ_VARIANT", "")
 EXTRA_DEFS = os.environ.get("WQ_NVCC_DEFS", "").split()
 LIBDIR = os.path.join(HERE, "lib", VARIANT) if VARIANT else os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libwq.so")
-SOURCES = ["abi.cu", "scores.cu", "assign.cu", "quant.cu", "decode.cu", "decode_tc.cu", "dequant.cu", "unreordered.cu"]
+SOURCES = ["abi.cu", "scores.cu", "assign.cu", "search.cu", "quant.cu", "decode.cu", "decode_tc.cu", "dequant.cu", "unreordered.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",

@@ -178,6 +178,53 @@ wq_status wq_assign_bits(const double *scores, const double *thr_host, int32_t L
   return cuda_status(wq::launch_assign(scores, p, bits, perm, seg_off, S_(stream)), "assign");
 }
 
+wq_status wq_search_workspace(int32_t B, int32_t D, int32_t W, size_t *bytes_host) {
+  if (!bytes_host) return fail(WQ_EINVAL, "bytes_host is NULL");
+  if (B < 1 || D < 8 || W < 1) return fail(WQ_ESHAPE, "B=%d D=%d W=%d", B, D, W);
+  const size_t tb = ((size_t)B * D * sizeof(double) + 255) / 256 * 256;
+  *bytes_host = tb + (size_t)(B + 1) * W * sizeof(int32_t);
+  return WQ_OK;
+}
+
+wq_status wq_search(const void *vis, int64_t vrs, int64_t vbs, const void *txt, int64_t trs, int64_t tbs, int32_t N,
+                    int32_t D, int32_t metric, const double *thr_host, int32_t L, const wq_geom *g,
+                    const wq_assign_opts *opts, double *scores, uint8_t *bits, int32_t *rank, int32_t *perm,
+                    int32_t *seg_off, void *workspace, size_t workspace_bytes, void *stream) {
+  wq_status s = check_geom(g, false);
+  if (s != WQ_OK) return s;
+  if (!vis || !txt || !scores || !bits || !perm || !seg_off || !workspace || (g->n_widths > 1 && !thr_host))
+    return fail(WQ_EINVAL, "NULL pointer");
+  if (metric != WQ_SIM_COSINE && metric != WQ_SIM_PEARSON) return fail(WQ_EINVAL, "metric=%d", metric);
+  if (L < 1 || L > wq::MAX_LAYERS) return fail(WQ_EINVAL, "L=%d not in 1..%d", L, wq::MAX_LAYERS);
+  const int W = g->M / g->S;
+  if (W < 1 || W > 4096) return fail(WQ_ESHAPE, "W=M/S=%d not in 1..4096", W);
+  if (N < 1) return fail(WQ_ESHAPE, "N=%d", N);
+  if (D % 8 || D < 8 || D > 4096) return fail(WQ_ESHAPE, "D=%d must be a multiple of 8 in [8, 4096]", D);
+  if (vrs % 8 || vbs % 8 || trs % 8 || tbs % 8 || !aligned16(vis) || !aligned16(txt))
+    return fail(WQ_EINVAL, "rows must be 16-byte aligned (strides multiple of 8 elements)");
+  size_t need = 0;
+  wq_search_workspace(g->B, D, W, &need);
+  if (workspace_bytes < need) return fail(WQ_EINVAL, "workspace too small (see wq_search_workspace)");
+  wq::AssignParams p{};
+  p.L = L; p.B = g->B; p.W = W; p.n_widths = g->n_widths;
+  for (int i = 0; i < 4; i++) p.widths[i] = i < g->n_widths ? g->widths[i] : 0;
+  p.pin = opts ? opts->pin_first : 1;
+  p.vote = opts ? opts->batch_vote : 0;
+  p.budget = opts ? opts->budget_avg_bits : 0.0;
+  const int np = p.pin ? 1 : 0;
+  if (p.budget > 0.0 && (double)(16 * np + g->widths[0] * (W - np)) > p.budget * (double)W)
+    return fail(WQ_EBUDGET, "budget %.4f bits infeasible: pinned window + %d x %d-bit windows exceed it",
+                p.budget, W - np, g->widths[0]);
+  for (int l = 0; l < L; l++)
+    for (int j = 0; j < g->n_widths - 1; j++) p.thr[l * 3 + j] = thr_host[(int64_t)l * (g->n_widths - 1) + j];
+  double *tbar = reinterpret_cast<double *>(workspace);
+  int32_t *order = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(workspace) +
+                                               ((size_t)g->B * D * sizeof(double) + 255) / 256 * 256);
+  return cuda_status(wq::launch_search((const __half *)vis, vrs, vbs, (const __half *)txt, trs, tbs, g->B, g->M, N, D,
+                                       g->S, metric, p, tbar, scores, order, bits, rank, perm, seg_off, S_(stream)),
+                     "search");
+}
+
 wq_status wq_packed_bytes(const wq_geom *g, const int32_t n_per_class_host[4], int32_t code_bytes_only,
                           int64_t *bytes_host) {
   if (!g || !n_per_class_host || !bytes_host) return fail(WQ_EINVAL, "NULL pointer");

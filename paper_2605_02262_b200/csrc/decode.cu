@@ -868,8 +868,11 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
   }
 }
 
+#ifndef WQ_DEC_LBT
+#define WQ_DEC_LBT DT                    // launch-bounds thread count (> DT: a lower register cap; experiments)
+#endif
 template <int D, int S, bool UR>
-__global__ void __launch_bounds__(DT, 1) k_decode(DecodeArgs a) {
+__global__ void __launch_bounds__(WQ_DEC_LBT, 1) k_decode(DecodeArgs a) {
   decode_body<D, S, UR>(a, (int)blockIdx.x, (int)gridDim.x);
 }
 

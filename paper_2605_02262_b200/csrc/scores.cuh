@@ -1,0 +1,202 @@
+// scores.cuh -- device side of wq_window_scores (scores.cu) shared with the fused search
+// kernel (search.cu): deterministic block sums, the text pool and the window-score
+// kernels' bodies.
+#pragma once
+#include "wq_device.cuh"
+#include "wq_internal.h"
+
+namespace wq {
+
+
+constexpr int ST = 128;  // threads per CTA
+#ifndef WQ_SC_RB
+#define WQ_SC_RB 2        // visual rows per block reduction (2 with 3 CTAs/SM: C5 702 -> 560 us)
+#endif
+#ifndef WQ_SC_MINB
+#define WQ_SC_MINB 3      // CTAs per SM the register budget must allow
+#endif
+
+// Deterministic block sum of NV doubles per thread (fixed tree).
+template <int NV>
+WQ_DEV void block_sum(double (&v)[NV], double *red /* [4][NV] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; i++)
+    for (int o = 16; o >= 1; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; i++) red[warp * NV + i] = v[i];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; i++) v[i] = ((red[i] + red[NV + i]) + red[2 * NV + i]) + red[3 * NV + i];
+  __syncthreads();
+}
+
+WQ_DEV void load8(const __half *p, double (&x)[8]) {
+  uint4 u = *reinterpret_cast<const uint4 *>(p);
+  const __half2 *h = reinterpret_cast<const __half2 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    float2 f = __half22float2(h[i]);
+    x[2 * i] = (double)f.x;
+    x[2 * i + 1] = (double)f.y;
+  }
+}
+
+// tbar[b] of request b by one CTA of ST threads; pooled: shared [D], red: shared [4]
+template <bool CENTER>
+WQ_DEV void text_pool_body(const __half *__restrict__ txt, int64_t trs, int64_t tbs, int N, int D,
+                           double *__restrict__ tbar, int b, double *pooled, double *red) {
+  const int nchunk = D / 8;
+  for (int c = threadIdx.x; c < D; c += ST) pooled[c] = 0.0;
+  for (int j = 0; j < N; j++) {
+    const __half *row = txt + b * tbs + (int64_t)j * trs;
+    double mu = 0.0;
+    if (CENTER) {                                  // Pearson: centre the row first (T11)
+      double sm[1] = {0.0};
+      for (int k = threadIdx.x; k < nchunk; k += ST) {
+        double x[8];
+        load8(row + 8 * k, x);
+#pragma unroll
+        for (int i = 0; i < 8; i++) sm[0] += x[i];
+      }
+      block_sum<1>(sm, red);
+      mu = sm[0] / (double)D;
+    }
+    double ss[1] = {0.0};
+    for (int k = threadIdx.x; k < nchunk; k += ST) {
+      double x[8];
+      load8(row + 8 * k, x);
+#pragma unroll
+      for (int i = 0; i < 8; i++) ss[0] = fma(x[i] - mu, x[i] - mu, ss[0]);
+    }
+    block_sum<1>(ss, red);
+    double inv = ss[0] > 0.0 ? 1.0 / sqrt(ss[0]) : 0.0;
+    for (int k = threadIdx.x; k < nchunk; k += ST) {
+      double x[8];
+      load8(row + 8 * k, x);
+#pragma unroll
+      for (int i = 0; i < 8; i++) pooled[8 * k + i] = fma(x[i] - mu, inv, pooled[8 * k + i]);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += ST) tbar[(int64_t)b * D + c] = pooled[c];
+  __syncthreads();
+}
+
+// A visual "row" is D elements; with head-split rows (the per-layer scorer) element c lives
+// at row + (c / dh) * hs + c % dh (dh = head dim, hs = head stride); dh = D, hs = 0 otherwise.
+// score of window w of request b by one CTA of ST threads; red: shared [4 * WQ_SC_RB]
+template <int NC, bool CENTER>  // 16-byte chunks per thread per row: ceil(D / 8 / ST); CENTER: Pearson
+WQ_DEV void window_score_body(const __half *__restrict__ vis, int64_t vrs, int64_t vbs, int M, int N, int D, int S,
+                              const double *__restrict__ tbar, double *__restrict__ scores, int dh, int64_t hs,
+                              int w, int b, int W, double *red) {
+  constexpr int RB = WQ_SC_RB;  // rows per batch
+  const int tid = threadIdx.x;
+  const int nchunk = D / 8;
+  double pool[NC][8];
+#pragma unroll
+  for (int i = 0; i < NC; i++)
+#pragma unroll
+    for (int e = 0; e < 8; e++) pool[i][e] = 0.0;
+  const __half *base = vis + b * vbs + (int64_t)w * S * vrs;
+  for (int r0 = 0; r0 < S; r0 += RB) {
+    uint4 raw[RB][NC];
+#pragma unroll
+    for (int r = 0; r < RB; r++)
+#pragma unroll
+      for (int i = 0; i < NC; i++) {
+        int k = tid + ST * i;
+        const int c = 8 * k;                                // first element of the chunk
+        raw[r][i] = k < nchunk ? __ldcs(reinterpret_cast<const uint4 *>(base + (int64_t)(r0 + r) * vrs +
+                                                                      (int64_t)(c / dh) * hs + c % dh))
+                               : make_uint4(0, 0, 0, 0);
+      }
+    double mu[RB];
+#pragma unroll
+    for (int r = 0; r < RB; r++) mu[r] = 0.0;
+    if constexpr (CENTER) {                        // Pearson: row means first (T11)
+#pragma unroll
+      for (int r = 0; r < RB; r++) {
+#pragma unroll
+        for (int i = 0; i < NC; i++) {
+          const __half2 *h = reinterpret_cast<const __half2 *>(&raw[r][i]);
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            float2 f = __half22float2(h[e]);
+            mu[r] += (double)f.x;
+            mu[r] += (double)f.y;
+          }
+        }
+      }
+      block_sum<RB>(mu, red);
+#pragma unroll
+      for (int r = 0; r < RB; r++) mu[r] /= (double)D;
+    }
+    double ss[RB];
+#pragma unroll
+    for (int r = 0; r < RB; r++) {
+      ss[r] = 0.0;
+#pragma unroll
+      for (int i = 0; i < NC; i++) {
+        const __half2 *h = reinterpret_cast<const __half2 *>(&raw[r][i]);
+        const bool in = tid + ST * i < nchunk;     // padding chunks are zeros, not (0 - mu)
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          float2 f = __half22float2(h[e]);
+          const double x0 = in ? (double)f.x - mu[r] : 0.0, x1 = in ? (double)f.y - mu[r] : 0.0;
+          ss[r] = fma(x0, x0, ss[r]);
+          ss[r] = fma(x1, x1, ss[r]);
+        }
+      }
+    }
+    block_sum<RB>(ss, red);
+#pragma unroll
+    for (int r = 0; r < RB; r++) {
+      double inv = ss[r] > 0.0 ? 1.0 / sqrt(ss[r]) : 0.0;
+#pragma unroll
+      for (int i = 0; i < NC; i++) {
+        const __half2 *h = reinterpret_cast<const __half2 *>(&raw[r][i]);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          float2 f = __half22float2(h[e]);
+          pool[i][2 * e] = fma((double)f.x - mu[r], inv, pool[i][2 * e]);
+          pool[i][2 * e + 1] = fma((double)f.y - mu[r], inv, pool[i][2 * e + 1]);
+        }
+      }
+    }
+  }
+  double dot[1] = {0.0};
+  const double *tb = tbar + (int64_t)b * D;
+#pragma unroll
+  for (int i = 0; i < NC; i++) {
+    int k = tid + ST * i;
+    if (k < nchunk)
+#pragma unroll
+      for (int e = 0; e < 8; e++) dot[0] = fma(pool[i][e], tb[8 * k + e], dot[0]);
+  }
+  block_sum<1>(dot, red);
+  if (tid == 0) scores[(int64_t)b * W + w] = dot[0] / ((double)S * (double)N);
+}
+
+}  // namespace wq
+
+namespace wq {
+template <bool CENTER>
+__global__ void __launch_bounds__(ST) k_text_pool(const __half *__restrict__ txt, int64_t trs,
+                                                  int64_t tbs, int N, int D, double *__restrict__ tbar) {
+  extern __shared__ double pooled[];  // [D]
+  __shared__ double red[4];
+  text_pool_body<CENTER>(txt, trs, tbs, N, D, tbar, blockIdx.x, pooled, red);
+}
+
+template <int NC, bool CENTER>
+__global__ void __launch_bounds__(ST, WQ_SC_MINB) k_window_scores(const __half *__restrict__ vis, int64_t vrs,
+                                                      int64_t vbs, int M, int N, int D, int S,
+                                                      const double *__restrict__ tbar,
+                                                      double *__restrict__ scores, int dh, int64_t hs) {
+  __shared__ double red[4 * WQ_SC_RB];
+  window_score_body<NC, CENTER>(vis, vrs, vbs, M, N, D, S, tbar, scores, dh, hs, blockIdx.x, blockIdx.y, gridDim.x,
+                                red);
+}
+}  // namespace wq

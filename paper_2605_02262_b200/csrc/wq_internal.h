@@ -27,6 +27,13 @@ cudaError_t launch_rank(const double *scores, int B, int W, int32_t *rank, cudaS
 cudaError_t launch_assign(const double *scores, const AssignParams &p, uint8_t *bits, int32_t *perm,
                           int32_t *seg_off, cudaStream_t st);
 
+// the fused search (search.cu): scores + rank + assign of every layer in one launch
+size_t search_smem(int W, int D);
+cudaError_t launch_search(const __half *vis, int64_t vrs, int64_t vbs, const __half *txt, int64_t trs, int64_t tbs,
+                          int B, int M, int N, int D, int S, int metric, const AssignParams &p, double *tbar,
+                          double *scores, int32_t *order, uint8_t *bits, int32_t *rank, int32_t *perm, int32_t *seg,
+                          cudaStream_t st);
+
 cudaError_t launch_layer_layout(const int32_t *seg_off, int B, int H, int d, int S, int64_t *offs,
                                 cudaStream_t st);
 cudaError_t launch_shard_slots(const int32_t *perm, const int32_t *seg, int B, int W, int G, int r,

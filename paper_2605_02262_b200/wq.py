@@ -65,6 +65,9 @@ def load(build_if_missing: bool = True):
         "wq_window_scores_ex": [P, I64, I64, P, I64, I64, I32, I32, I32, I32, I32, I32, P, P, SZ, P],
         "wq_window_scores_layer": [P, P, I32, P, P, I32, I32, I32, I32, I32, I32, I32, P, P, SZ, P],
         "wq_assign_bits": [P, P, I32, C.POINTER(Geom), C.POINTER(AssignOpts), P, P, P, P, P],
+        "wq_search_workspace": [I32, I32, I32, P],
+        "wq_search": [P, I64, I64, P, I64, I64, I32, I32, I32, P, I32, C.POINTER(Geom), C.POINTER(AssignOpts), P, P,
+                      P, P, P, P, SZ, P],
         "wq_packed_bytes": [C.POINTER(Geom), P, I32, P],
         "wq_layer_layout": [C.POINTER(Geom), P, P, P],
         "wq_reorder_quantize_pack": [P, P, P, I32, C.POINTER(Geom), P, I32, P, P, P, P],
@@ -99,7 +102,7 @@ def load(build_if_missing: bool = True):
 
 def exported_symbols():
     return ["wq_thresholds", "wq_window_scores_workspace", "wq_window_scores", "wq_window_scores_ex",
-            "wq_window_scores_layer", "wq_assign_bits",
+            "wq_window_scores_layer", "wq_assign_bits", "wq_search_workspace", "wq_search",
             "wq_packed_bytes", "wq_layer_layout", "wq_reorder_quantize_pack", "wq_decode_workspace",
             "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_dequant_layout", "wq_dequantize_image",
             "wq_unreordered_layout", "wq_unreorder_image", "wq_decode_attention_unreordered",
@@ -377,3 +380,29 @@ def wq_window_scores_layer(k: torch.Tensor, vis_off: int, q_text: torch.Tensor, 
     _check(load().wq_window_scores_layer(_ptr(k), ks, int(vis_off), _ptr(q_text), qs, B, H, Hq, d, int(M), N, int(S),
                                          _ptr(scores), _ptr(workspace), workspace.numel(), _stream(stream)))
     return scores
+
+
+def wq_search(vis: torch.Tensor, txt: torch.Tensor, thr, L: int, g: Geom, opts: AssignOpts | None = None,
+              metric: int = 0, outs=None, workspace=None, stream=None):
+    """The fused search (include/wq.h wq_search): scores + rank + assignment of L layers in one
+    launch.  Returns (scores, bits, rank, perm, seg_off)."""
+    import numpy as np
+    B, M, D = vis.shape
+    N = txt.shape[1]
+    W = M // g.S
+    dev = vis.device
+    if outs is None:
+        outs = (torch.empty((B, W), dtype=torch.float64, device=dev), torch.empty((L, B, W), dtype=torch.uint8, device=dev),
+                torch.empty((B, W), dtype=torch.int32, device=dev), torch.empty((L, B, W), dtype=torch.int32, device=dev),
+                torch.empty((L, B, 5), dtype=torch.int32, device=dev))
+    scores, bits, rank, perm, seg = outs
+    if workspace is None:
+        n = C.c_size_t(0)
+        _check(load().wq_search_workspace(B, D, W, C.byref(n)))
+        workspace = torch.empty(n.value, dtype=torch.uint8, device=dev)
+    thr = np.ascontiguousarray(thr, np.float64)
+    _check(load().wq_search(_ptr(vis), vis.stride(1), vis.stride(0), _ptr(txt), txt.stride(1), txt.stride(0), N, D,
+                            int(metric), _host_ptr(thr) if thr.size else None, int(L), C.byref(g),
+                            C.byref(opts) if opts is not None else None, _ptr(scores), _ptr(bits), _ptr(rank),
+                            _ptr(perm), _ptr(seg), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return scores, bits, rank, perm, seg

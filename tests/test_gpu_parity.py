@@ -642,3 +642,45 @@ def test_layer_scores_c5_geometry(orc):
     gpu, oref = _assign_both(orc, got, thr, g)
     for a_, b_ in zip(gpu, oref):
         assert np.array_equal(a_, b_)
+
+
+@pytest.mark.parametrize("B,M,N,D,S,widths,budget,vote,metric,L", [
+    (2, 16 * 9 + 5, 8, 64, 16, (2, 4, 8, 16), 0.0, 0, 0, 3), (3, 32 * 40, 5, 896, 32, (2, 4, 8, 16), 4.0, 0, 0, 5),
+    (4, 32 * 50, 7, 3584, 32, (2, 4, 16), 3.5, 1, 0, 2), (2, 64 * 20 + 7, 6, 256, 64, (2, 4, 8), 0.0, 1, 1, 4),
+    (2, 16 * 300, 32, 512, 16, (4, 8), 5.0, 0, 1, 2)])
+def test_fused_search_equals_chain(orc, B, M, N, D, S, widths, budget, vote, metric, L):
+    """wq_search (scores + rank + assign of L layers in one cooperative launch, one rank
+    sort per request) gives bit-identical scores, ranks, bits, perms and seg_off to the
+    unfused chain, and matches the oracle's assignment."""
+    vis, txt = synth.embeddings(B, M, N, D, S, 900 + D, "cuda")
+    g = wq.geom(B, 2, 14, 64, M, S, widths)
+    s_prof = [0.5, 0.3, 0.9, 0.05, 0.6][:L]
+    thr = orc.thresholds(s_prof, 2.0, len(widths))
+    opts = wq.AssignOpts(budget, 1, vote)
+    sc0 = wq.wq_window_scores(vis, txt, S, metric=metric)
+    bits0, rank0, perm0, seg0 = wq.wq_assign_bits(sc0, thr, L, g, opts)
+    sc1, bits1, rank1, perm1, seg1 = wq.wq_search(vis, txt, thr, L, g, opts, metric=metric)
+    torch.cuda.synchronize()
+    assert torch.equal(sc0, sc1)
+    for x, y in ((bits0, bits1), (rank0, rank1), (perm0, perm1), (seg0, seg1)):
+        assert torch.equal(x, y)
+    ob, orank, operm, oseg = orc.assign_bits(sc1.cpu().numpy(), thr, ogeom(orc, g), budget, 1, vote)
+    assert np.array_equal(bits1.cpu().numpy(), ob) and np.array_equal(perm1.cpu().numpy(), operm)
+
+
+def test_fused_search_c5(orc):
+    """The fused search at the full C5 size (B = 4, 50,176 visual tokens, D = 3584, 28
+    layers, budget 3.5): bit-identical to the chain."""
+    cfg = configs.CONFIGS["C5"]
+    m = cfg.model
+    vis, txt = synth.embeddings(cfg.B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, "cuda")
+    thr = orc.thresholds(cfg.sensitivities(), cfg.alpha, len(cfg.widths))
+    g = wq.geom(cfg.B, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
+    opts = wq.AssignOpts(3.5, 1, 0)
+    sc0 = wq.wq_window_scores(vis, txt, cfg.S)
+    chain = wq.wq_assign_bits(sc0, thr, cfg.layers, g, opts)
+    fused = wq.wq_search(vis, txt, thr, cfg.layers, g, opts)
+    torch.cuda.synchronize()
+    assert torch.equal(sc0, fused[0])
+    for x, y in zip(chain, fused[1:]):
+        assert torch.equal(x, y)
