@@ -89,6 +89,11 @@ def lib():
                 "wqo_merge": (None, [P, I32, I32, I32, P]),
                 "wqo_f64_to_f16_rn": (C.c_uint16, [F64]),
                 "wqo_dequantize_image": (None, [P, P, P, C.POINTER(Geom), P, P]),
+                "wqo_record_bytes_g": (I64, [I32, I32, I32, I32]),
+                "wqo_layer_layout_g": (None, [C.POINTER(Geom), P, P, I32]),
+                "wqo_reorder_quantize_pack_g": (None, [P, P, P, I32, C.POINTER(Geom), P, I32, P, P, P, I32]),
+                "wqo_dequant_record_g": (None, [P, I32, I32, I32, P, P, I32]),
+                "wqo_decode_attention_g": (None, [P, P, P, P, P, I32, C.POINTER(Geom), P, P, P, P, F32, P, P, I32]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -200,8 +205,8 @@ def assign_bits(scores, thr, g: Geom, budget=0.0, pin=1, vote=0):
 
 
 # --- byte accounting -------------------------------------------------------------
-def record_bytes(bits, d, S):
-    return lib().wqo_record_bytes(bits, d, S)
+def record_bytes(bits, d, S, gran=0):
+    return lib().wqo_record_bytes_g(bits, d, S, gran)
 
 
 def packed_bytes(g: Geom, n_per_class, code_only=False):
@@ -214,10 +219,10 @@ def kv_code_bytes(tokens_per_class, d, H):
     return lib().wqo_kv_code_bytes(_p(t), d, H)
 
 
-def layer_layout(g: Geom, seg_off_l: np.ndarray) -> np.ndarray:
+def layer_layout(g: Geom, seg_off_l: np.ndarray, gran=0) -> np.ndarray:
     seg_off_l = np.ascontiguousarray(seg_off_l, np.int32)
     offs = np.zeros(g.B * g.H + 1, np.int64)
-    lib().wqo_layer_layout(C.byref(g), _p(seg_off_l), _p(offs))
+    lib().wqo_layer_layout_g(C.byref(g), _p(seg_off_l), _p(offs), int(gran))
     return offs
 
 
@@ -244,31 +249,31 @@ def code_pos(is_v, d, b, t, c):
     return int(bo[0]), int(bit[0])
 
 
-def reorder_quantize_pack(k, v, vis_off, g: Geom, perm_l, seg_off_l, offs=None):
-    """k, v: fp16 [B][H][T][d] -> packed u8 image of one layer (D-1)."""
+def reorder_quantize_pack(k, v, vis_off, g: Geom, perm_l, seg_off_l, offs=None, gran=0):
+    """k, v: fp16 [B][H][T][d] -> packed u8 image of one layer (D-1; gran 1: P:508 groups)."""
     k, v = _u16(k), _u16(v)
     perm_l = np.ascontiguousarray(perm_l, np.int32)
     seg_off_l = np.ascontiguousarray(seg_off_l, np.int32)
     if offs is None:
-        offs = layer_layout(g, seg_off_l)
+        offs = layer_layout(g, seg_off_l, gran)
     B, H, T, d = k.shape
     strides = np.array([H * T * d, T * d, d], np.int64)
     packed = np.zeros(max(int(offs[-1]), 16), np.uint8)
-    lib().wqo_reorder_quantize_pack(_p(k), _p(v), _p(strides), vis_off, C.byref(g), _p(perm_l),
-                                    perm_l.shape[-1], _p(seg_off_l), _p(offs), _p(packed))
+    lib().wqo_reorder_quantize_pack_g(_p(k), _p(v), _p(strides), vis_off, C.byref(g), _p(perm_l),
+                                      perm_l.shape[-1], _p(seg_off_l), _p(offs), _p(packed), int(gran))
     return packed, offs
 
 
-def dequant_record(rec: np.ndarray, bits, d, S):
+def dequant_record(rec: np.ndarray, bits, d, S, gran=0):
     rec = np.ascontiguousarray(rec, np.uint8)
     kh = np.zeros((S, d), np.float64)
     vh = np.zeros((S, d), np.float64)
-    lib().wqo_dequant_record(_p(rec), bits, d, S, _p(kh), _p(vh))
+    lib().wqo_dequant_record_g(_p(rec), bits, d, S, _p(kh), _p(vh), int(gran))
     return kh, vh
 
 
 def decode_attention(q, packed, offs, seg_off_l, perm_l, g: Geom, k_rest, v_rest, rest_len,
-                     sm_scale, want_partial=False):
+                     sm_scale, want_partial=False, gran=0):
     """q fp16 [B][Hq][d]; k_rest/v_rest fp16 [B][H][R][d]; -> out fp64 [B][Hq][d] (, partial)."""
     q, k_rest, v_rest = _u16(q), _u16(k_rest), _u16(v_rest)
     B, H, R, d = k_rest.shape
@@ -278,10 +283,10 @@ def decode_attention(q, packed, offs, seg_off_l, perm_l, g: Geom, k_rest, v_rest
     seg_off_l = np.ascontiguousarray(seg_off_l, np.int32)
     out = np.zeros((g.B, g.Hq, g.d), np.float64)
     part = np.zeros((g.B, g.Hq, g.d + 2), np.float64) if want_partial else None
-    lib().wqo_decode_attention(_p(q), _p(np.ascontiguousarray(packed)), _p(np.ascontiguousarray(offs)),
-                               _p(seg_off_l), _p(perm_l), perm_l.shape[-1], C.byref(g),
-                               _p(k_rest), _p(v_rest), _p(rs), _p(rest_len), float(sm_scale),
-                               _p(out), _p(part))
+    lib().wqo_decode_attention_g(_p(q), _p(np.ascontiguousarray(packed)), _p(np.ascontiguousarray(offs)),
+                                 _p(seg_off_l), _p(perm_l), perm_l.shape[-1], C.byref(g),
+                                 _p(k_rest), _p(v_rest), _p(rs), _p(rest_len), float(sm_scale),
+                                 _p(out), _p(part), int(gran))
     return (out, part) if want_partial else out
 
 

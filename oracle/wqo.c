@@ -276,10 +276,15 @@ int wqo_assign_bits(const double *scores, const double *thr, int32_t L, const wq
 /* ------------------------------------------------------------------------ */
 /* Byte accounting of the D-1 image                                           */
 /* ------------------------------------------------------------------------ */
-int64_t wqo_record_bytes(int32_t b, int32_t d, int32_t S) {
+/* gran 0 (default, Q19): per-channel K / per-token V (s, mn) pairs, 4(d + S) bytes;
+ * gran 1 (paper-literal P:508, reading Q37): one (s, mn) per (window, head, K|V) group,
+ * a 16-byte block {mn_K, s_K, mn_V, s_V, 0, 0, 0, 0}. */
+int64_t wqo_record_bytes_g(int32_t b, int32_t d, int32_t S, int32_t gran) {
   if (b == 16) return 2LL * S * d * 2;                   /* K and V fp16 */
+  if (gran == 1) return 2LL * S * d * b / 8 + 16;
   return 2LL * S * d * b / 8 + 4LL * d + 4LL * S;        /* codes + (s, mn) fp16 pairs */
 }
+int64_t wqo_record_bytes(int32_t b, int32_t d, int32_t S) { return wqo_record_bytes_g(b, d, S, 0); }
 
 int64_t wqo_packed_bytes(const wqo_geom *g, const int32_t n_per_class[4], int32_t code_only) {
   int64_t total = 0;
@@ -298,16 +303,17 @@ int64_t wqo_kv_code_bytes(const int64_t tokens_per_class[4], int32_t d, int32_t 
   return total;
 }
 
-void wqo_layer_layout(const wqo_geom *g, const int32_t *seg_off_l, int64_t *offs) {
+void wqo_layer_layout_g(const wqo_geom *g, const int32_t *seg_off_l, int64_t *offs, int32_t gran) {
   int64_t off = 0;
   for (int b = 0; b < g->B; b++) {
     const int32_t *so = seg_off_l + (int64_t)b * 5;
     int64_t img = 0;
-    for (int k = 0; k < 4; k++) img += (int64_t)(so[k + 1] - so[k]) * wqo_record_bytes(CLASS_BITS[k], g->d, g->S);
+    for (int k = 0; k < 4; k++) img += (int64_t)(so[k + 1] - so[k]) * wqo_record_bytes_g(CLASS_BITS[k], g->d, g->S, gran);
     for (int h = 0; h < g->H; h++) { offs[(int64_t)b * g->H + h] = off; off += img; }
   }
   offs[(int64_t)g->B * g->H] = off;
 }
+void wqo_layer_layout(const wqo_geom *g, const int32_t *seg_off_l, int64_t *offs) { wqo_layer_layout_g(g, seg_off_l, offs, 0); }
 
 /* ------------------------------------------------------------------------ */
 /* Eq.14-16 under Q17: fp32, one rounding per operation, RNE codes            */
@@ -425,15 +431,15 @@ int64_t wqo_param_pos(int32_t is_v, int32_t d, int32_t i, int32_t is_min) {
   return is_v ? vparam_off(i, is_min) : kparam_off(d, i, is_min);
 }
 
-static int64_t slot_offset(const wqo_geom *g, const int32_t *so, int slot, int *bits_out) {
+static int64_t slot_offset(const wqo_geom *g, const int32_t *so, int slot, int *bits_out, int gran) {
   int64_t off = 0;
   for (int k = 0; k < 4; k++) {
     int n = so[k + 1] - so[k];
     if (slot < so[k + 1]) {
       *bits_out = CLASS_BITS[k];
-      return off + (int64_t)(slot - so[k]) * wqo_record_bytes(CLASS_BITS[k], g->d, g->S);
+      return off + (int64_t)(slot - so[k]) * wqo_record_bytes_g(CLASS_BITS[k], g->d, g->S, gran);
     }
-    off += (int64_t)n * wqo_record_bytes(CLASS_BITS[k], g->d, g->S);
+    off += (int64_t)n * wqo_record_bytes_g(CLASS_BITS[k], g->d, g->S, gran);
   }
   *bits_out = 0;
   return -1;
@@ -441,26 +447,26 @@ static int64_t slot_offset(const wqo_geom *g, const int32_t *so, int slot, int *
 
 /* Alg.2 prefill branch: window perm[slot] is quantized with its
  * segment's width and written at its slot (reorder + quant in one pass). */
-void wqo_reorder_quantize_pack(const uint16_t *k, const uint16_t *v, const int64_t strides[3],
-                               int32_t vis_off, const wqo_geom *g,
-                               const int32_t *perm_l, int32_t perm_stride,
-                               const int32_t *seg_off_l, const int64_t *offs, uint8_t *packed) {
+void wqo_reorder_quantize_pack_g(const uint16_t *k, const uint16_t *v, const int64_t strides[3],
+                                 int32_t vis_off, const wqo_geom *g,
+                                 const int32_t *perm_l, int32_t perm_stride,
+                                 const int32_t *seg_off_l, const int64_t *offs, uint8_t *packed, int32_t gran) {
   int d = g->d, S = g->S;
 #pragma omp parallel for collapse(2) schedule(dynamic)
   for (int b = 0; b < g->B; b++) {
     for (int h = 0; h < g->H; h++) {
       const int32_t *so = seg_off_l + (int64_t)b * 5;
-      uint16_t *grp = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(S > d ? S : d));
-      uint8_t *codes = (uint8_t *)malloc((size_t)(S > d ? S : d));
+      uint16_t *grp = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)S * d);
+      uint8_t *codes = (uint8_t *)malloc((size_t)S * d);
       for (int slot = 0; slot < so[4]; slot++) {
         int bits;
-        int64_t roff = slot_offset(g, so, slot, &bits);
+        int64_t roff = slot_offset(g, so, slot, &bits, gran);
         uint8_t *rec = packed + offs[(int64_t)b * g->H + h] + roff;
         int w = perm_l[(int64_t)b * perm_stride + slot];
         const uint16_t *K0 = k + b * strides[0] + h * strides[1] + (int64_t)(vis_off + w * S) * strides[2];
         const uint16_t *V0 = v + b * strides[0] + h * strides[1] + (int64_t)(vis_off + w * S) * strides[2];
         int64_t kbytes = (int64_t)S * d * bits / 8;          /* bytes of the K code/value tiles */
-        memset(rec, 0, (size_t)wqo_record_bytes(bits, d, S));
+        memset(rec, 0, (size_t)wqo_record_bytes_g(bits, d, S, gran));
         if (bits == 16) {                                /* FP16 window: values in fragment order */
           for (int t = 0; t < S; t++)
             for (int c = 0; c < d; c++) {
@@ -469,6 +475,35 @@ void wqo_reorder_quantize_pack(const uint16_t *k, const uint16_t *v, const int64
               put_code(rec, bo, bit, 16, K0[(int64_t)t * strides[2] + c]);
               wqo_code_pos(1, d, 16, t, c, &bo, &bit);
               put_code(rec + kbytes, bo, bit, 16, V0[(int64_t)t * strides[2] + c]);
+            }
+          continue;
+        }
+        if (gran == 1) {
+          /* P:508 literal (Q37): ONE group per (window, head, K|V) -- all S*d values share
+           * (s, mn); element (t, c) is group entry t*d + c */
+          uint8_t *pb = rec + 2 * kbytes;
+          uint16_t s16, mn16;
+          for (int t = 0; t < S; t++)
+            for (int c = 0; c < d; c++) grp[t * d + c] = K0[(int64_t)t * strides[2] + c];
+          wqo_quantize_group(grp, S * d, 1, bits, &s16, &mn16, codes);
+          put_u16(pb + 0, mn16);
+          put_u16(pb + 2, s16);
+          for (int t = 0; t < S; t++)
+            for (int c = 0; c < d; c++) {
+              int64_t bo; int bit;
+              wqo_code_pos(0, d, bits, t, c, &bo, &bit);
+              put_code(rec, bo, bit, bits, codes[t * d + c]);
+            }
+          for (int t = 0; t < S; t++)
+            for (int c = 0; c < d; c++) grp[t * d + c] = V0[(int64_t)t * strides[2] + c];
+          wqo_quantize_group(grp, S * d, 1, bits, &s16, &mn16, codes);
+          put_u16(pb + 4, mn16);
+          put_u16(pb + 6, s16);
+          for (int t = 0; t < S; t++)
+            for (int c = 0; c < d; c++) {
+              int64_t bo; int bit;
+              wqo_code_pos(1, d, bits, t, c, &bo, &bit);
+              put_code(rec + kbytes, bo, bit, bits, codes[t * d + c]);
             }
           continue;
         }
@@ -501,9 +536,16 @@ void wqo_reorder_quantize_pack(const uint16_t *k, const uint16_t *v, const int64
     }
   }
 }
+void wqo_reorder_quantize_pack(const uint16_t *k, const uint16_t *v, const int64_t strides[3],
+                               int32_t vis_off, const wqo_geom *g,
+                               const int32_t *perm_l, int32_t perm_stride,
+                               const int32_t *seg_off_l, const int64_t *offs, uint8_t *packed) {
+  wqo_reorder_quantize_pack_g(k, v, strides, vis_off, g, perm_l, perm_stride, seg_off_l, offs, packed, 0);
+}
 
-/* x^ = mn + s * code (Eq.15 with z = -mn/s), exact in fp64 */
-void wqo_dequant_record(const uint8_t *rec, int32_t bits, int32_t d, int32_t S, double *kh, double *vh) {
+/* x^ = mn + s * code (Eq.15 with z = -mn/s), exact in fp64; gran 1: the group's (s, mn) */
+void wqo_dequant_record_g(const uint8_t *rec, int32_t bits, int32_t d, int32_t S, double *kh, double *vh,
+                          int32_t gran) {
   int64_t kbytes = (int64_t)S * d * bits / 8;
   const uint8_t *kp = rec + 2 * kbytes, *vp = kp + 4LL * d;
   for (int t = 0; t < S; t++)
@@ -516,6 +558,11 @@ void wqo_dequant_record(const uint8_t *rec, int32_t bits, int32_t d, int32_t S, 
       if (bits == 16) {
         kh[(int64_t)t * d + c] = wqo_f16_to_f64((uint16_t)kc);
         vh[(int64_t)t * d + c] = wqo_f16_to_f64((uint16_t)vc);
+      } else if (gran == 1) {
+        double km = wqo_f16_to_f64(get_u16(kp + 0)), ks = wqo_f16_to_f64(get_u16(kp + 2));
+        double vm = wqo_f16_to_f64(get_u16(kp + 4)), vs = wqo_f16_to_f64(get_u16(kp + 6));
+        kh[(int64_t)t * d + c] = km + ks * (double)kc;
+        vh[(int64_t)t * d + c] = vm + vs * (double)vc;
       } else {
         double ks = wqo_f16_to_f64(get_u16(kp + kparam_off(d, c, 0)));
         double km = wqo_f16_to_f64(get_u16(kp + kparam_off(d, c, 1)));
@@ -525,6 +572,9 @@ void wqo_dequant_record(const uint8_t *rec, int32_t bits, int32_t d, int32_t S, 
         vh[(int64_t)t * d + c] = vm + vs * (double)vc;
       }
     }
+}
+void wqo_dequant_record(const uint8_t *rec, int32_t bits, int32_t d, int32_t S, double *kh, double *vh) {
+  wqo_dequant_record_g(rec, bits, d, S, kh, vh, 0);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -559,12 +609,12 @@ static void attend(const double *q, const double *K, const double *V, int64_t n,
 /* Alg.2 decode branch evaluated as its definition: invert the
  * reorder (Eq.12-13), dequantize to fp64 and attend in original token order,
  * rest tokens (text/tail/generated, FP16) last. */
-void wqo_decode_attention(const uint16_t *q, const uint8_t *packed, const int64_t *offs,
-                          const int32_t *seg_off_l, const int32_t *perm_l, int32_t perm_stride,
-                          const wqo_geom *g,
-                          const uint16_t *k_rest, const uint16_t *v_rest,
-                          const int64_t rest_strides[2], const int32_t *rest_len,
-                          float sm_scale, double *out, double *partial) {
+void wqo_decode_attention_g(const uint16_t *q, const uint8_t *packed, const int64_t *offs,
+                            const int32_t *seg_off_l, const int32_t *perm_l, int32_t perm_stride,
+                            const wqo_geom *g,
+                            const uint16_t *k_rest, const uint16_t *v_rest,
+                            const int64_t rest_strides[2], const int32_t *rest_len,
+                            float sm_scale, double *out, double *partial, int32_t gran) {
   int d = g->d, S = g->S, grp = g->Hq / g->H;
 #pragma omp parallel for collapse(2) schedule(dynamic)
   for (int b = 0; b < g->B; b++) {
@@ -583,9 +633,9 @@ void wqo_decode_attention(const uint16_t *q, const uint8_t *packed, const int64_
         for (int s = 0; s < nslot; s++) {
           if (perm_l[(int64_t)b * perm_stride + s] != w) continue;
           int bits;
-          int64_t roff = slot_offset(g, so, s, &bits);
-          wqo_dequant_record(packed + offs[(int64_t)b * g->H + h] + roff, bits, d, S,
-                             K + row * d, V + row * d);
+          int64_t roff = slot_offset(g, so, s, &bits, gran);
+          wqo_dequant_record_g(packed + offs[(int64_t)b * g->H + h] + roff, bits, d, S,
+                               K + row * d, V + row * d, gran);
           row += S;
         }
       }
@@ -608,6 +658,15 @@ void wqo_decode_attention(const uint16_t *q, const uint8_t *packed, const int64_
       free(qq); free(K); free(V);
     }
   }
+}
+void wqo_decode_attention(const uint16_t *q, const uint8_t *packed, const int64_t *offs,
+                          const int32_t *seg_off_l, const int32_t *perm_l, int32_t perm_stride,
+                          const wqo_geom *g,
+                          const uint16_t *k_rest, const uint16_t *v_rest,
+                          const int64_t rest_strides[2], const int32_t *rest_len,
+                          float sm_scale, double *out, double *partial) {
+  wqo_decode_attention_g(q, packed, offs, seg_off_l, perm_l, perm_stride, g, k_rest, v_rest, rest_strides, rest_len,
+                         sm_scale, out, partial, 0);
 }
 
 void wqo_bruteforce_attention(const uint16_t *q, const uint16_t *k, const uint16_t *v,
@@ -688,7 +747,7 @@ void wqo_dequantize_image(const uint8_t *packed, const int64_t *offs, const int3
       double *vh = (double *)malloc(sizeof(double) * (size_t)S * d);
       for (int slot = 0; slot < so[4]; slot++) {
         int bits;
-        int64_t roff = slot_offset(g, so, slot, &bits);
+        int64_t roff = slot_offset(g, so, slot, &bits, 0);
         const uint8_t *rec = packed + offs[(int64_t)b * g->H + h] + roff;
         uint8_t *dst = img16 + offs16[(int64_t)b * g->H + h] + (int64_t)slot * rec16;
         wqo_dequant_record(rec, bits, d, S, kh, vh);       /* exact x^ = mn + s*code (fp16 values if 16) */

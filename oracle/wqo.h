@@ -126,4 +126,23 @@ void wqo_merge(const double *parts, int32_t G, int32_t BHq, int32_t d, double *o
 void wqo_dequantize_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l,
                           const wqo_geom *g, const int64_t *offs16, uint8_t *img16);
 
+/* Paper-literal group quantization (reading Q37): gran = 1
+ * stores ONE (s, mn) per (window, head, K|V) group -- all S*d values of the window's K
+ * (resp. V) for that head -- in a 16-byte block {mn_K, s_K, mn_V, s_V, 0,0,0,0} after the
+ * codes (code layout D-1 unchanged); gran = 0 is the default per-channel K / per-token V. */
+int64_t wqo_record_bytes_g(int32_t b, int32_t d, int32_t S, int32_t gran);
+void wqo_layer_layout_g(const wqo_geom *g, const int32_t *seg_off_l, int64_t *offs, int32_t gran);
+void wqo_reorder_quantize_pack_g(const uint16_t *k, const uint16_t *v, const int64_t strides[3],
+                                 int32_t vis_off, const wqo_geom *g,
+                                 const int32_t *perm_l, int32_t perm_stride,
+                                 const int32_t *seg_off_l, const int64_t *offs, uint8_t *packed, int32_t gran);
+void wqo_dequant_record_g(const uint8_t *rec, int32_t bits, int32_t d, int32_t S, double *kh, double *vh,
+                          int32_t gran);
+void wqo_decode_attention_g(const uint16_t *q, const uint8_t *packed, const int64_t *offs,
+                            const int32_t *seg_off_l, const int32_t *perm_l, int32_t perm_stride,
+                            const wqo_geom *g,
+                            const uint16_t *k_rest, const uint16_t *v_rest,
+                            const int64_t rest_strides[2], const int32_t *rest_len,
+                            float sm_scale, double *out, double *partial, int32_t gran);
+
 #endif

@@ -795,3 +795,100 @@ def test_layer_scorer_invariants(orc):
     k2 = k.copy()
     k2[:, :, 5] = (k2[:, :, 5].astype(np.float32) * 2).astype(np.float16)     # whole token row x2 (exact)
     assert np.max(np.abs(orc.window_scores_layer(k2, 0, q, T, S) - base)) <= 1e-12
+
+
+# --------------------------------------------------------------------------------------
+# Paper-literal group quantization (reading Q37)
+# --------------------------------------------------------------------------------------
+def _group_case(orc, K, V, S, d, bits):
+    """One request, one head, one window of class `bits` -> (record bytes, image)."""
+    g = orc.geom(1, 1, 1, d, S, S, [bits])
+    perm = np.zeros((1, 1), np.int32)
+    cls = {2: 0, 4: 1, 8: 2, 16: 3}[bits]
+    seg = np.array([[0] * (cls + 1) + [1] * (4 - cls)], np.int32)
+    pk, offs = orc.reorder_quantize_pack(K.reshape(1, 1, S, d), V.reshape(1, 1, S, d), 0, g, perm, seg, gran=1)
+    return pk[:int(offs[-1])], offs
+
+
+def test_group_record_bytes_closed_form(orc):
+    for d in (64, 128):
+        for S in (16, 32, 64, 128):
+            for b in (2, 4, 8):
+                assert orc.record_bytes(b, d, S, 1) == S * d * b // 4 + 16
+            assert orc.record_bytes(16, d, S, 1) == 4 * S * d
+
+
+def test_group_quantizer_hand_golden(orc):
+    """K values cycling through -3..3 (fp16-exact), V = 2 * K; 2-bit groups: mn_K = -3, range 6,
+    s_K = RU(6/3) = 2 (0x4000), codes rint((x + 3) / 2) half-even: -3,-2 -> 0, -1 -> 1,
+    0 -> 2 (1.5 -> 2), 1 -> 2, 2 -> 2 (2.5 -> 2), 3 -> 3; V: mn_V = -6 (0xC600), s_V = 4 (0x4400),
+    the same codes.  The 16-byte block reads {mn_K, s_K, mn_V, s_V, 0, 0, 0, 0}."""
+    S, d = 16, 64
+    t, c = np.meshgrid(np.arange(S), np.arange(d), indexing="ij")
+    K = (((t * d + c) % 7) - 3).astype(np.float16)
+    V = (2 * K.astype(np.float32)).astype(np.float16)
+    rec, _ = _group_case(orc, K, V, S, d, 2)
+    assert len(rec) == S * d * 2 // 4 + 16
+    blk = rec[2 * S * d * 2 // 8:].view(np.uint16)
+    assert list(blk) == [0xC200, 0x4000, 0xC600, 0x4400, 0, 0, 0, 0]
+    code_of = {-3: 0, -2: 0, -1: 1, 0: 2, 1: 2, 2: 2, 3: 3}
+    kh, vh = orc.dequant_record(rec, 2, d, S, gran=1)
+    want = np.vectorize(lambda x: -3 + 2 * code_of[int(x)])(K.astype(np.float64))
+    assert np.array_equal(kh, want)
+    assert np.array_equal(vh, 2 * want)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_group_quantizer_error_bound(orc, bits):
+    """Every element of the window is within s (1/2 + 2^-14) of its dequantized value, with the
+    group's single scale s = the smallest fp16 >= fl32(range / q_max) over ALL S*d values
+    (range from numpy, the rounding-up from numpy's float16: independent of the oracle)."""
+    rng = np.random.default_rng(40 + bits)
+    S, d = 32, 128
+    qmax = 2 ** bits - 1
+    for _ in range(6):
+        K = (rng.standard_normal((S, d)) * rng.uniform(0.3, 2, d) + rng.standard_normal(d) * 3).astype(np.float16)
+        V = (rng.standard_normal((S, d)) * np.exp(0.5 * rng.standard_normal((S, 1)))).astype(np.float16)
+        rec, _ = _group_case(orc, K, V, S, d, bits)
+        kh, vh = orc.dequant_record(rec, bits, d, S, gran=1)
+        for X, Xh, off in ((K, kh, 2), (V, vh, 6)):
+            x = X.astype(np.float64)
+            rng32 = np.float32(np.float32(x.max()) - np.float32(x.min())) / np.float32(qmax)
+            s = _ru_reference(np.array([rng32], np.float32))[0].view(np.float16).astype(np.float64)
+            blk = rec[2 * S * d * bits // 8:].view(np.uint16)
+            assert blk[off // 2] == np.float16(s).view(np.uint16)
+            assert np.all(np.abs(x - Xh) <= s * (0.5 + 2 ** -14))
+
+
+def test_group_decode_exact_on_lattice(orc):
+    """Windows whose K and V values lie on a power-of-two lattice of their group (x = mn + s k,
+    k in [0, q_max], both extremes present) round-trip exactly, so the group-quantized decode
+    (gran 1) equals fp64 brute-force attention on the original fp16 tokens."""
+    rng = np.random.default_rng(44)
+    B, H, Hq, d, S, W = 2, 2, 6, 64, 16, 5
+    M = W * S
+    bits_w = [16, 2, 4, 8, 2]
+    K = np.zeros((B, H, M, d), np.float16)
+    V = np.zeros((B, H, M, d), np.float16)
+    for b in range(B):
+        for h in range(H):
+            for w, bw in enumerate(bits_w):
+                qm = 2 ** min(bw, 8) - 1
+                for X in (K, V):
+                    s, mn = 2.0 ** int(rng.integers(-4, 0)), float(rng.integers(-8, 8))
+                    k = rng.integers(0, qm + 1, (S, d))
+                    k.flat[0], k.flat[1] = 0, qm
+                    X[b, h, w * S:(w + 1) * S] = (mn + s * k).astype(np.float16)
+    order = [i for cls in (2, 4, 8, 16) for i, x in enumerate(bits_w) if x == cls]
+    perm = np.array([order] * B, np.int32)
+    seg = np.array([[0, 2, 3, 4, 5]] * B, np.int32)
+    g = orc.geom(B, H, Hq, d, M, S, [2, 4, 8, 16])
+    pk, offs = orc.reorder_quantize_pack(K, V, 0, g, perm, seg, gran=1)
+    q = rng.standard_normal((B, Hq, d)).astype(np.float16)
+    kr = rng.standard_normal((B, H, 3, d)).astype(np.float16)
+    vr = rng.standard_normal((B, H, 3, d)).astype(np.float16)
+    rl = np.array([3, 2], np.int32)
+    got = orc.decode_attention(q, pk, offs, seg, perm, g, kr, vr, rl, 0.125, gran=1)
+    win = np.tile(np.arange(W, dtype=np.int32), (B, 1))
+    ref = orc.bruteforce_attention(q, K, V, 0, g, win, np.array([W] * B, np.int32), kr, vr, rl, 0.125)
+    assert np.max(np.abs(got - ref)) <= 1e-12
