@@ -214,16 +214,34 @@ wq_status wq_search(const void *vis, int64_t vis_row_stride, int64_t vis_batch_s
                     double *scores, uint8_t *bits, int32_t *rank, int32_t *perm, int32_t *seg_off,
                     void *workspace, size_t workspace_bytes, void *stream);
 
+/* Quantization granularity of the packed image (the *_ex entries; the plain entries
+ * use WQ_GRAN_CHANNEL_TOKEN).
+ *   WQ_GRAN_CHANNEL_TOKEN: per-channel K / per-token V parameters inside each window
+ *     (reading Q19, KIVI-style; record = K codes, V codes, 2 fp16 per K channel,
+ *     2 fp16 per V token: S*d*b/4 + 4d + 4S bytes).
+ *   WQ_GRAN_GROUP: the paper-literal groups of P:508 ("grouped by sliding windows"):
+ *     one (s, mn) per (window, KV head, K|V) over all S*d values (Eq.14-16 applied to
+ *     the group; reading Q37); record = K codes, V codes, then a 16-byte block
+ *     {mn_K, s_K, mn_V, s_V, 0, 0, 0, 0} (fp16): S*d*b/4 + 16 bytes.
+ * FP16 windows (b = 16) are stored raw under both. */
+enum { WQ_GRAN_CHANNEL_TOKEN = 0, WQ_GRAN_GROUP = 1 };
+
 /* Bytes of one (b, h) image holding n_per_class_host[k] windows of class k
  * ({2,4,8,16}[k]) under contract D-1.  HOST.  With code_bytes_only = 1 the
- * params are not counted and the result is the paper's accounting. */
+ * params are not counted and the result is the paper's accounting.
+ * Errors: WQ_EINVAL (NULL pointer, unknown granularity). */
 wq_status wq_packed_bytes(const wq_geom *g, const int32_t n_per_class_host[4],
                           int32_t code_bytes_only, int64_t *bytes_host);
+wq_status wq_packed_bytes_ex(const wq_geom *g, const int32_t n_per_class_host[4],
+                             int32_t code_bytes_only, int32_t granularity, int64_t *bytes_host);
 
 /* Byte offsets of the (b, h) images of one layer: offs[B*H + 1] (i64, device),
- * offs[0] = 0, offs[B*H] = total bytes.  seg_off_l: i32 [B][5] (device). */
+ * offs[0] = 0, offs[B*H] = total bytes.  seg_off_l: i32 [B][5] (device).
+ * The _ex form takes the granularity (WQ_GRAN_*) of the image it lays out. */
 wq_status wq_layer_layout(const wq_geom *g, const int32_t *seg_off_l, int64_t *offs,
                           void *stream);
+wq_status wq_layer_layout_ex(const wq_geom *g, const int32_t *seg_off_l, int32_t granularity,
+                             int64_t *offs, void *stream);
 
 /* Reorder + group-quantize + pack one layer (Alg.2 lines 2-15, Eq.14-16,
  * group = window P:508; per-channel K / per-token V parameters, Q19).
@@ -241,6 +259,15 @@ wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t s
                                    const int32_t *perm_l, int32_t perm_stride,
                                    const int32_t *seg_off_l, const int64_t *offs,
                                    uint8_t *packed, void *stream);
+/* The same with the granularity (WQ_GRAN_*); offs must come from wq_layer_layout_ex with
+ * the same granularity.  WQ_GRAN_GROUP: Q17's quantizer over the S*d values of each
+ * (window, head, K|V) group; bit-exact with the oracle's gran = 1.
+ * Errors: as above, WQ_EINVAL for an unknown granularity. */
+wq_status wq_reorder_quantize_pack_ex(const void *k, const void *v, const int64_t strides[3],
+                                      int32_t vis_off, const wq_geom *g,
+                                      const int32_t *perm_l, int32_t perm_stride,
+                                      const int32_t *seg_off_l, const int64_t *offs,
+                                      int32_t granularity, uint8_t *packed, void *stream);
 
 /* Decode attention over the reordered mixed-precision cache (Alg.2 decode
  * branch P:450-458, Eq.2-3 without mask P:214, reorder invariance Eq.12-13
@@ -261,7 +288,10 @@ wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t s
  *   channel group |q_c| * s_c < 2^15 (q*s is carried as an fp16 hi + lo pair) and for
  *   every V token group s_t < 255 (p * s_t is an fp16 MMA operand with p <= 2^8, the
  *   lazy-rescale headroom).  Outside it results are undefined.  For b = 2 this allows V
- *   ranges up to 765 and, with |q| <= 8, K channel ranges up to 12288.
+ *   ranges up to 765 and, with |q| <= 8, K channel ranges up to 12288.  Inside it the
+ *   output error is within 2e-3 of the row's largest |output| plus an absolute 2^-16: a
+ *   V group with a subnormal scale (s = 2^-24..2^-14: zero, constant or subnormal-range
+ *   values) makes p * s an fp16 subnormal, worth up to 2^(b-1) * 2^-24 absolute.
  * Errors: WQ_ESHAPE (unsupported d/S, Hq/H > 8), WQ_EINVAL (both outputs NULL). */
 wq_status wq_decode_workspace(const wq_geom *g, size_t *bytes_host);
 
@@ -274,7 +304,12 @@ enum {
    * partition and starts streaming the packed cache into shared memory while
    * that work drains, and touches q, k_rest/v_rest, out, partial and the
    * workspace only after it has completed.  Without the guarantee, pass 0. */
-  WQ_DECODE_EARLY = 1
+  WQ_DECODE_EARLY = 1,
+  /* WQ_DECODE_GROUP: the image is WQ_GRAN_GROUP (one (s, mn) per window and tensor):
+   * logit = s_K * sum_c code_c q_c + mn_K * sum_c q_c, V weight p * s_V.  Numerical
+   * domain: s_V < 255 (as the per-token V scale above); no K-side bound beyond fp32.
+   * Not accepted by the unreordered entry (WQ_EINVAL). */
+  WQ_DECODE_GROUP = 2
 };
 /* wq_decode_attention with flags (WQ_DECODE_*); flags = 0 is wq_decode_attention. */
 wq_status wq_decode_attention_ex(const void *q, const uint8_t *packed, const int64_t *offs,

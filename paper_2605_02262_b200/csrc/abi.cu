@@ -225,31 +225,56 @@ wq_status wq_search(const void *vis, int64_t vrs, int64_t vbs, const void *txt, 
                      "search");
 }
 
-wq_status wq_packed_bytes(const wq_geom *g, const int32_t n_per_class_host[4], int32_t code_bytes_only,
-                          int64_t *bytes_host) {
+static bool gran_ok(int32_t gran) { return gran == WQ_GRAN_CHANNEL_TOKEN || gran == WQ_GRAN_GROUP; }
+
+wq_status wq_packed_bytes_ex(const wq_geom *g, const int32_t n_per_class_host[4], int32_t code_bytes_only,
+                             int32_t granularity, int64_t *bytes_host) {
   if (!g || !n_per_class_host || !bytes_host) return fail(WQ_EINVAL, "NULL pointer");
+  if (!gran_ok(granularity)) return fail(WQ_EINVAL, "granularity=%d", granularity);
   static const int cb[4] = {2, 4, 8, 16};
   int64_t t = 0;
   for (int k = 0; k < 4; k++) {
-    int64_t rec = code_bytes_only ? (int64_t)g->S * g->d * cb[k] / 4 : wq::record_bytes(cb[k], g->d, g->S);
+    int64_t rec = code_bytes_only ? (int64_t)g->S * g->d * cb[k] / 4
+                                  : wq::record_bytes(cb[k], g->d, g->S, granularity);
     t += (int64_t)n_per_class_host[k] * rec;
   }
   *bytes_host = t;
   return WQ_OK;
 }
 
-wq_status wq_layer_layout(const wq_geom *g, const int32_t *seg_off_l, int64_t *offs, void *stream) {
+wq_status wq_packed_bytes(const wq_geom *g, const int32_t n_per_class_host[4], int32_t code_bytes_only,
+                          int64_t *bytes_host) {
+  return wq_packed_bytes_ex(g, n_per_class_host, code_bytes_only, WQ_GRAN_CHANNEL_TOKEN, bytes_host);
+}
+
+wq_status wq_layer_layout_ex(const wq_geom *g, const int32_t *seg_off_l, int32_t granularity, int64_t *offs,
+                             void *stream) {
   wq_status s = check_geom(g, true);
   if (s != WQ_OK) return s;
   if (!seg_off_l || !offs) return fail(WQ_EINVAL, "NULL pointer");
+  if (!gran_ok(granularity)) return fail(WQ_EINVAL, "granularity=%d", granularity);
   if (g->B > 4096) return fail(WQ_ESHAPE, "B=%d > 4096", g->B);
-  return cuda_status(wq::launch_layer_layout(seg_off_l, g->B, g->H, g->d, g->S, offs, S_(stream)), "layout");
+  return cuda_status(wq::launch_layer_layout(seg_off_l, g->B, g->H, g->d, g->S, granularity, offs, S_(stream)),
+                     "layout");
+}
+
+wq_status wq_layer_layout(const wq_geom *g, const int32_t *seg_off_l, int64_t *offs, void *stream) {
+  return wq_layer_layout_ex(g, seg_off_l, WQ_GRAN_CHANNEL_TOKEN, offs, stream);
 }
 
 wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t strides[3], int32_t vis_off,
                                    const wq_geom *g, const int32_t *perm_l, int32_t perm_stride,
                                    const int32_t *seg_off_l, const int64_t *offs, uint8_t *packed,
                                    void *stream) {
+  return wq_reorder_quantize_pack_ex(k, v, strides, vis_off, g, perm_l, perm_stride, seg_off_l, offs,
+                                     WQ_GRAN_CHANNEL_TOKEN, packed, stream);
+}
+
+wq_status wq_reorder_quantize_pack_ex(const void *k, const void *v, const int64_t strides[3], int32_t vis_off,
+                                      const wq_geom *g, const int32_t *perm_l, int32_t perm_stride,
+                                      const int32_t *seg_off_l, const int64_t *offs, int32_t granularity,
+                                      uint8_t *packed, void *stream) {
+  if (!gran_ok(granularity)) return fail(WQ_EINVAL, "granularity=%d", granularity);
   wq_status s = check_geom(g, true);
   if (s != WQ_OK) return s;
   if (!k || !v || !strides || !perm_l || !seg_off_l || !offs || !packed) return fail(WQ_EINVAL, "NULL pointer");
@@ -259,7 +284,8 @@ wq_status wq_reorder_quantize_pack(const void *k, const void *v, const int64_t s
   if (strides[2] < g->d) return fail(WQ_ESHAPE, "token stride %lld < d=%d", (long long)strides[2], g->d);
   if (vis_off < 0) return fail(WQ_EINVAL, "vis_off=%d", vis_off);
   return cuda_status(wq::launch_quant((const __half *)k, (const __half *)v, strides, vis_off, g->B, g->H, g->d,
-                                      g->S, g->M, perm_l, perm_stride, seg_off_l, offs, packed, S_(stream)),
+                                      g->S, g->M, perm_l, perm_stride, seg_off_l, offs, packed, granularity,
+                                      S_(stream)),
                      "quantize");
 }
 
@@ -294,7 +320,8 @@ static wq_status decode_args(const void *q, const uint8_t *packed, const int64_t
                              int32_t R_max, float sm_scale, void *out, float *partial, void *workspace,
                              size_t workspace_bytes, uint32_t flags, const int64_t *woff, const PeerCfg *pc,
                              wq::DecodeArgs &a) {
-  if (flags & ~(uint32_t)WQ_DECODE_EARLY) return fail(WQ_EINVAL, "unknown decode flags 0x%x", flags);
+  if (flags & ~(uint32_t)(WQ_DECODE_EARLY | WQ_DECODE_GROUP)) return fail(WQ_EINVAL, "unknown decode flags 0x%x", flags);
+  if ((flags & WQ_DECODE_GROUP) && woff) return fail(WQ_EINVAL, "WQ_DECODE_GROUP needs a reordered image");
   wq_status s = check_geom(g, true);
   if (s != WQ_OK) return s;
   if (!q || !packed || !offs || !seg_off_l || !workspace) return fail(WQ_EINVAL, "NULL pointer");

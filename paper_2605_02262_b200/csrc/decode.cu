@@ -141,9 +141,71 @@ WQ_DEV void softmax_tiles(const float (&s)[NT][4], float scale2, WarpState &st, 
 // scales/zero points are read once, q' = q*s is formed as an fp16 hi+lo pair
 // (HMUL2 + exact-residual HFMA2) and the bias q.mn accumulates on the tensor core;
 // each tile keeps independent hi/lo accumulators (short dependency chains).
-template <int D, int S, int BITS>
+// GRP (reading Q37, the paper-literal groups of P:508): one (s, mn) per window and tensor, so
+// logit = s_K * sum_c code*q_c + mn_K * sum_c q_c: the K side runs on the raw q (no hi/lo
+// split, no zero-point MMA; qsum = the lane's heads' sum_c q_c, per unit), and the V side
+// takes P' = p * s_V.
+template <int D, int S, int BITS, bool GRP = false>
 WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
-                      WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane) {
+                      WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane,
+                      float2 qsum = make_float2(0.f, 0.f)) {
+  if constexpr (GRP && BITS < 16) {
+    constexpr int NTT = S / 16;
+    constexpr int CH = NTT < 2 ? 1 : 2;
+    constexpr int KT = D / 16;
+    constexpr int WPL = D * BITS / 64;
+    constexpr int TILE = 2 * D * BITS;
+    constexpr int KB = S * D * BITS / 8;
+    const uint2 pg = lds64(rec + 2 * KB);                // {mn_K, s_K, mn_V, s_V}
+    const float mnK = __half2float(__ushort_as_half((unsigned short)pg.x));
+    const float sK = __half2float(__ushort_as_half((unsigned short)(pg.x >> 16)));
+    const float mnV = __half2float(__ushort_as_half((unsigned short)pg.y));
+    const float sV = __half2float(__ushort_as_half((unsigned short)(pg.y >> 16)));
+    constexpr float HALF = (float)(1 << (BITS - 1));
+    const float bias0 = mnK * qsum.x, bias1 = mnK * qsum.y;
+#pragma unroll
+    for (int c0 = 0; c0 < NTT; c0 += CH) {
+      uint32_t wk[CH][WPL];
+#pragma unroll
+      for (int t = 0; t < CH; t++) load_chunk<D, BITS>(wk[t], rec + (c0 + t) * TILE, lane);
+      float ah[CH][4], al[CH][4];
+#pragma unroll
+      for (int t = 0; t < CH; t++)
+#pragma unroll
+        for (int i = 0; i < 4; i++) { ah[t][i] = 0.f; al[t][i] = 0.f; }
+#pragma unroll
+      for (int kt = 0; kt < KT; kt++) {
+        const uint2 qk = lds64(qs + (kt * 32 + lane) * 8);
+#pragma unroll
+        for (int t = 0; t < CH; t++) {
+          uint32_t a[4];
+#pragma unroll
+          for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS>(wk[t], 4 * kt + r);
+          if (kt & 1) mma16816(al[t], a, qk.x, qk.y, al[t]);
+          else mma16816(ah[t], a, qk.x, qk.y, ah[t]);
+        }
+      }
+      float sc[CH][4], vs[CH][2], vm[CH][2];
+#pragma unroll
+      for (int t = 0; t < CH; t++) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) sc[t][i] = fmaf(sK, ah[t][i] + al[t][i], (i & 1) ? bias1 : bias0);
+        vs[t][0] = vs[t][1] = sV;
+        vm[t][0] = vm[t][1] = fmaf(sV, HALF, mnV);
+      }
+      softmax_tiles<CH, KT>(sc, scale2, st, o, vs, vm, true, scratch, lane);
+#pragma unroll
+      for (int t = 0; t < CH; t++) {
+        uint32_t pb[2];
+        ldsm_x2_t(pb, scratch + (16 * t + (lane & 15)) * 16);
+        uint32_t wv[WPL];
+        load_chunk<D, BITS>(wv, rec + KB + (c0 + t) * TILE, lane);
+        tile_pv<D, BITS>(wv, pb[0], pb[1], o);
+      }
+      __syncwarp();
+    }
+    return;
+  }
   constexpr int NTT = S / 16;
   constexpr int CH = (BITS == 16 || NTT < 2) ? 1 : 2;
   constexpr int KT = D / 16;
@@ -575,7 +637,7 @@ size_t peer_buffer_bytes(int B, int H, int Hq, int d, int G) {
 
 // The kernel body; vc / vn = this CTA's index and the CTA count it plans with
 // (blockIdx.x / gridDim.x, or a virtual rank's share of the grid under emulation).
-template <int D, int S, bool UR>
+template <int D, int S, bool UR, bool GRP = false>
 WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
   using SM = DecodeSmem<D, S>;
   constexpr int KT = D / 16;
@@ -598,7 +660,7 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
 
   // ---- prologue (warp 0): unit cost prefix, then this CTA's share ----
   CtaPlan *cp = reinterpret_cast<CtaPlan *>(sm + SM::plan_off);
-  if (warp == 0) plan_cta<D, S, false, (!UR && WQ_DEC_STREAM)>(a, ustart, cp, s_flag, lane, vc, vn);
+  if (warp == 0) plan_cta<D, S, false, (!UR && WQ_DEC_STREAM), GRP>(a, ustart, cp, s_flag, lane, vc, vn);
   if (tid == 32) {
     for (int s = 0; s < NST; s++) {
       mbar_init(&full[s], 1);
@@ -623,7 +685,8 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
       if (lane == 0) produce_ur<D, S, STAGE, NST, SM::NUS, SM::TABN>(a, *cp, ring, full, empty, ent, units_done,
                                                                       reinterpret_cast<int *>(sm + SM::tab_off), vc);
     } else {
-      if (lane == 0) produce<D, S, false, STAGE, NST, SM::NUS>(a, *cp, ustart, ring, full, empty, ent, units_done, ts, vc);
+      if (lane == 0)
+        produce<D, S, false, STAGE, NST, SM::NUS, GRP>(a, *cp, ustart, ring, full, empty, ent, units_done, ts, vc);
     }
     return;
   }
@@ -671,6 +734,18 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
     const int b = u / a.H, h = u % a.H;
     if (warp == 0 && uidx > 0) stage_q(u);        // (entries after the first: unit ua + uidx)
     named_bar_sync(2, NCW * 32);
+    // GRP: sum_c q_c of the lane's heads 2q, 2q+1 (one MMA per k-tile with A = ones)
+    float2 qsum = make_float2(0.f, 0.f);
+    if constexpr (GRP) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint32_t ones[4] = {0x3C003C00u, 0x3C003C00u, 0x3C003C00u, 0x3C003C00u};
+#pragma unroll
+      for (int kt = 0; kt < KT; kt++) {
+        const uint2 qk = lds64(qs + (kt * 32 + lane) * 8);
+        mma16816(acc, ones, qk.x, qk.y, acc);
+      }
+      qsum = make_float2(acc[0], acc[1]);
+    }
 #pragma unroll
     for (int mt = 0; mt < KT; mt++) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
     st.m[0] = st.m[1] = -INFINITY;
@@ -712,12 +787,12 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
     for (int p = UR ? 4 : 0; p < 5; p++) {
       using IG = ItemGeo<D, S, false>;
       // item bytes of class p, computed (a table indexed by p would live in local memory)
-      const int sz = p == 4 ? IG::REST_SZ : (p == 3 ? 4 * S * D : S * D * (2 << p) / 4 + 4 * D + 4 * S);
+      const int sz = p == 4 ? IG::REST_SZ : (p == 3 ? 4 * S * D : S * D * (2 << p) / 4 + (GRP ? 16 : 4 * D + 4 * S));
       const int cap = STAGE / sz;
       const int len = E.len[p], nst = E.nst[p], lo = E.lo[p];
       // 2-bit stages (S <= 32) are consumed in PAIRS of windows (do_window2): a stage of n
       // records is ceil(n/2) work items, handed out round robin like single items
-      constexpr bool PAIRS = WQ_DEC_PAIR && S <= 32;
+      constexpr bool PAIRS = WQ_DEC_PAIR && S <= 32 && !GRP;
       for (int t = 0; t < nst; t++, sg++) {
         const int slot = sg % NST;
         const int nrec = min(cap, len - t * cap);
@@ -737,12 +812,12 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
               if (2 * k + 1 < nrec) do_window2<D, S, 2>(r0, r0 + sz, qs, a.scale_log2, st, o, scratch, lane);
               else do_window<D, S, 2>(r0, qs, a.scale_log2, st, o, scratch, lane);
             } else {
-              do_window<D, S, 2>(rec, qs, a.scale_log2, st, o, scratch, lane);
+              do_window<D, S, 2, GRP>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum);
             }
           } else if (p == 1) {
-            do_window<D, S, 4>(rec, qs, a.scale_log2, st, o, scratch, lane);
+            do_window<D, S, 4, GRP>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum);
           } else if (p == 2) {
-            do_window<D, S, 8>(rec, qs, a.scale_log2, st, o, scratch, lane);
+            do_window<D, S, 8, GRP>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum);
           } else if (p == 3) {
             do_window<D, S, 16>(rec, qs, a.scale_log2, st, o, scratch, lane);
           } else {
@@ -871,9 +946,9 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
 #ifndef WQ_DEC_LBT
 #define WQ_DEC_LBT DT                    // launch-bounds thread count (> DT: a lower register cap; experiments)
 #endif
-template <int D, int S, bool UR>
+template <int D, int S, bool UR, bool GRP>
 __global__ void __launch_bounds__(WQ_DEC_LBT, 1) k_decode(DecodeArgs a) {
-  decode_body<D, S, UR>(a, (int)blockIdx.x, (int)gridDim.x);
+  decode_body<D, S, UR, GRP>(a, (int)blockIdx.x, (int)gridDim.x);
 }
 
 // Fused cross-GPU merge emulated on ONE device in ONE launch (tests): the grid is split
@@ -930,12 +1005,12 @@ size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms) {
   return L.part + L.cnt + L.ts;
 }
 
-template <int D, int S, bool UR>
+template <int D, int S, bool UR, bool GRP = false>
 static cudaError_t launch_decode_t(const DecodeArgs &a, int num_sms, cudaStream_t st) {
   using SM = DecodeSmem<D, S>;
   static bool attr_set = false;                  // per instantiation (per process: one device)
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_decode<D, S, UR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_decode<D, S, UR, GRP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)SM::total);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -945,7 +1020,7 @@ static cudaError_t launch_decode_t(const DecodeArgs &a, int num_sms, cudaStream_
     // must be resident at once (one per SM) or a waiting CTA could starve one not yet
     // scheduled on a peer
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode<D, S, UR>, DT, SM::total);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode<D, S, UR, GRP>, DT, SM::total);
     if (e != cudaSuccess) return e;
     if (per_sm < 1 || num_sms > device_sm_count()) return cudaErrorCooperativeLaunchTooLarge;
   }
@@ -961,7 +1036,7 @@ static cudaError_t launch_decode_t(const DecodeArgs &a, int num_sms, cudaStream_
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, k_decode<D, S, UR>, a);
+  return cudaLaunchKernelEx(&cfg, k_decode<D, S, UR, GRP>, a);
 }
 
 cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st) {
@@ -970,9 +1045,12 @@ cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st) {
   // warps are issue/latency bound), so it is opt-in.
   // (The tcgen05 kernel has no peer exchange: the fused-merge path always runs here.)
   static const bool use_tc = getenv("WQ_DECODE_TC") && atoi(getenv("WQ_DECODE_TC")) != 0;
-  if (a.d == 128 && use_tc && !a.woff && !a.peer_bufs) return launch_decode_tc(a, num_sms, st);
-#define WQ_D(DD, SS) \
-  if (a.d == DD && a.S == SS) return a.woff ? launch_decode_t<DD, SS, true>(a, num_sms, st) : launch_decode_t<DD, SS, false>(a, num_sms, st);
+  if (a.d == 128 && use_tc && !a.woff && !a.peer_bufs && !(a.flags & WQ_DECODE_GROUP_)) return launch_decode_tc(a, num_sms, st);
+#define WQ_D(DD, SS)                                                                                      \
+  if (a.d == DD && a.S == SS)                                                                             \
+    return a.woff ? launch_decode_t<DD, SS, true>(a, num_sms, st)                                         \
+                  : ((a.flags & WQ_DECODE_GROUP_) ? launch_decode_t<DD, SS, false, true>(a, num_sms, st)   \
+                                                  : launch_decode_t<DD, SS, false>(a, num_sms, st));
   WQ_D(64, 16) WQ_D(64, 32) WQ_D(64, 64) WQ_D(64, 128)
   WQ_D(128, 16) WQ_D(128, 32) WQ_D(128, 64) WQ_D(128, 128)
 #undef WQ_D

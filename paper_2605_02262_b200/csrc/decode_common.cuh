@@ -13,6 +13,7 @@ namespace wq {
 constexpr int MAX_UNITS = 1024;         // B * H
 constexpr int64_t MIN_CTA_BYTES = 49152;
 constexpr uint32_t WQ_DECODE_EARLY_ = 1u;     // = WQ_DECODE_EARLY (include/wq.h)
+constexpr uint32_t WQ_DECODE_GROUP_ = 2u;     // = WQ_DECODE_GROUP (include/wq.h)
 constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trace
 #ifndef WQ_DEC_EOV
 #define WQ_DEC_EOV 2000                // per-unit entry overhead in cost units of S*D/100
@@ -34,11 +35,12 @@ constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trac
 // across CTAs in COST space, not bytes: every item costs its bytes plus a per-item
 // compute term, so CTAs that get many narrow windows get fewer of them.
 // TC selects the cost table of the tcgen05 kernel.
-template <int D, int S, bool TC = false>
+template <int D, int S, bool TC = false, bool GRP = false>
 struct ItemGeo {
-  // record bytes of class k (0..2 = 2/4/8-bit, 3 = FP16), D-1 contract
+  // record bytes of class k (0..2 = 2/4/8-bit, 3 = FP16), D-1 contract (GRP: the 16-byte
+  // parameter block of the paper-literal groups, reading Q37)
   static constexpr int64_t rb(int k) {
-    return k == 3 ? 4LL * S * D : (int64_t)S * D * (2 << k) / 4 + 4LL * D + 4LL * S;
+    return k == 3 ? 4LL * S * D : (int64_t)S * D * (2 << k) / 4 + (GRP ? 16LL : 4LL * D + 4LL * S);
   }
   static constexpr int REST_SZ = 64 * D;               // FP16 rest tile: 16 K rows + 16 V rows
   static constexpr int sz(int k) { return k == 4 ? REST_SZ : (int)rb(k); }
@@ -70,9 +72,9 @@ struct UnitGeo {
   int64_t cc[5];                        // cost start of each class segment; cc[4] = windows' cost
 };
 
-template <int D, int S, bool TC>
+template <int D, int S, bool TC, bool GRP = false>
 WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
-  using IG = ItemGeo<D, S, TC>;
+  using IG = ItemGeo<D, S, TC, GRP>;
   g.b = u / a.H;
   g.h = u - g.b * a.H;
   const int32_t *so = a.seg_off + 5 * g.b;
@@ -91,17 +93,17 @@ WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
   g.rl = g.rl < 0 ? 0 : (g.rl > a.R_max ? a.R_max : g.rl);     // contract: rest_len clamped to R_max
   g.ntiles = (g.rl + 15) / 16;
 }
-template <int D, int S, bool TC>
+template <int D, int S, bool TC, bool GRP = false>
 WQ_DEV int64_t unit_cost(const UnitGeo &g) {
-  return g.cc[4] + (int64_t)g.ntiles * ItemGeo<D, S, TC>::cost(4);
+  return g.cc[4] + (int64_t)g.ntiles * ItemGeo<D, S, TC, GRP>::cost(4);
 }
 
 // first item whose start (in cost units, relative to the unit) is >= x.  Planning
 // arithmetic runs in double (no 64-bit integer division on the producer's path);
 // every CTA evaluates the same expressions, so neighbouring CTAs agree on the cut.
-template <int D, int S, bool TC>
+template <int D, int S, bool TC, bool GRP = false>
 WQ_DEV int first_item(const UnitGeo &g, double x) {
-  using IG = ItemGeo<D, S, TC>;
+  using IG = ItemGeo<D, S, TC, GRP>;
   if (x <= 0.0) return 0;
 #pragma unroll
   for (int k = 0; k < 4; k++) {
@@ -119,9 +121,9 @@ WQ_DEV int first_item(const UnitGeo &g, double x) {
 struct UnitPlan {
   int lo[5], hi[5], nst[5];
 };
-template <int D, int S, bool TC, int STAGE>
+template <int D, int S, bool TC, int STAGE, bool GRP = false>
 WQ_DEV void plan_unit(const UnitGeo &g, int i0, int i1, UnitPlan &pl) {
-  using IG = ItemGeo<D, S, TC>;
+  using IG = ItemGeo<D, S, TC, GRP>;
 #pragma unroll
   for (int p = 0; p < 5; p++) {
     const int a0 = p < 4 ? g.so[p] : g.nslots;
@@ -162,7 +164,7 @@ struct CtaPlan {
 // the same cost; a unit-aligned split rounds each unit to a whole number of CTAs.
 // vc / vn: this CTA's index and the CTA count of the grid it plans over (blockIdx.x /
 // gridDim.x, or a virtual rank's share of one grid in the fused-merge emulation).
-template <int D, int S, bool TC, bool STREAM = false>
+template <int D, int S, bool TC, bool STREAM = false, bool GRP = false>
 WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_flag, int lane, int vc, int vn) {
   const int U = a.B * a.H;
   int64_t carry = 0;
@@ -173,8 +175,8 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
     int64_t v = 0;
     if (u < U) {
       ioff = a.offs[u];
-      unit_geo<D, S, TC>(a, u, gg);
-      v = unit_cost<D, S, TC>(gg) + (STREAM ? ItemGeo<D, S, TC>::EOV : 0);
+      unit_geo<D, S, TC, GRP>(a, u, gg);
+      v = unit_cost<D, S, TC, GRP>(gg) + (STREAM ? ItemGeo<D, S, TC, GRP>::EOV : 0);
     }
     int64_t x = v;
 #pragma unroll
@@ -255,10 +257,10 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
 // ---- producer (one lane): stream the CTA's entries into the ring ----
 // Stages of NST x STAGE bytes, full[s] (1 arrival + tx bytes) / empty[s] barriers;
 // entries published in a ring of NUS Entry slots, released via *units_done.
-template <int D, int S, bool TC, int STAGE, int NST, int NUS>
+template <int D, int S, bool TC, int STAGE, int NST, int NUS, bool GRP = false>
 WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart, uint8_t *ring,
                     uint64_t *full, uint64_t *empty, Entry *ent, int *units_done, uint64_t *ts, int vc) {
-  using IG = ItemGeo<D, S, TC>;
+  using IG = ItemGeo<D, S, TC, GRP>;
   const int c = vc;
   const uint64_t pol = policy_evict_first();
   if (ts) ts[62] = gtime();
@@ -293,7 +295,7 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
       img_off = P.img_off;
     } else {
       img_off = a.offs[u];
-      unit_geo<D, S, TC>(a, u, gg);
+      unit_geo<D, S, TC, GRP>(a, u, gg);
     }
     int i0 = 0, i1 = gg.nslots + gg.ntiles;
     int ec0 = P.split == 1 ? P.c0 : c, ec1 = P.split == 1 ? P.c1 : c + 1;
@@ -304,18 +306,18 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
       const double lov = (double)WQ_DEC_LOV * S * D / 100;
       const double ucost = (double)(ustart[u + 1] - ustart[u]) + lov;
       const int k = c - P.c0, n = P.c1 - P.c0;
-      i0 = first_item<D, S, TC>(gg, ucost * k / n);
-      if (k < n - 1) i1 = first_item<D, S, TC>(gg, ucost * (k + 1) / n);
+      i0 = first_item<D, S, TC, GRP>(gg, ucost * k / n);
+      if (k < n - 1) i1 = first_item<D, S, TC, GRP>(gg, ucost * (k + 1) / n);
     } else if (P.split == 2) {
       // this CTA's slice of unit u (items start EOV into the unit's cost range) and the
       // CTAs [ec0, ec1) sharing the unit; every CTA evaluates the same expressions
       const double us = (double)ustart[u], ue = (double)ustart[u + 1];
-      const double eov = (double)ItemGeo<D, S, TC>::EOV;
+      const double eov = (double)ItemGeo<D, S, TC, GRP>::EOV;
       const double Td = (double)ustart[a.B * a.H];
       const int Gp = P.G;
       auto Bk = [&](int k) { return Td * k / Gp; };
-      if (P.lo > us) i0 = first_item<D, S, TC>(gg, P.lo - us - eov);
-      if (P.hi < ue) i1 = first_item<D, S, TC>(gg, P.hi - us - eov);
+      if (P.lo > us) i0 = first_item<D, S, TC, GRP>(gg, P.lo - us - eov);
+      if (P.hi < ue) i1 = first_item<D, S, TC, GRP>(gg, P.hi - us - eov);
       int k0 = (int)(us * Gp / Td);
       k0 = k0 < 0 ? 0 : (k0 > Gp - 1 ? Gp - 1 : k0);
       while (k0 + 1 < Gp && Bk(k0 + 1) <= us) k0++;
@@ -328,7 +330,7 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
       ec1 = k1 + 1;
     }
     UnitPlan pl;
-    plan_unit<D, S, TC, STAGE>(gg, i0, i1, pl);
+    plan_unit<D, S, TC, STAGE, GRP>(gg, i0, i1, pl);
     bool published = false;
     const uint8_t *img = a.packed + img_off;
     const __half *kr = a.k_rest + gg.b * a.rs_b + gg.h * a.rs_h;

@@ -106,7 +106,7 @@ cudaError_t launch_dequant_layout(const int32_t *seg_off, int B, int H, int d, i
   k_seg16<<<(B + 127) / 128, 128, 0, st>>>(seg_off, B, seg16);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_layer_layout(seg16, B, H, d, S, offs16, st);
+  return launch_layer_layout(seg16, B, H, d, S, 0, offs16, st);
 }
 
 cudaError_t launch_dequant_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off, int B, int H,

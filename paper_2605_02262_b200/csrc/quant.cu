@@ -18,13 +18,13 @@ namespace wq {
 
 // offs[b*H + h] of one layer from seg_off_l[B][5]; one thread per request, then a
 // serial prefix (B <= 4096) by thread 0 -- tiny.
-__global__ void k_layer_layout(const int32_t *__restrict__ seg_off, int B, int H, int d, int S,
+__global__ void k_layer_layout(const int32_t *__restrict__ seg_off, int B, int H, int d, int S, int gran,
                                int64_t *__restrict__ offs) {
   extern __shared__ int64_t img[];
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     const int32_t *so = seg_off + 5 * b;
     int64_t t = 0;
-    for (int k = 0; k < 4; k++) t += (int64_t)(so[k + 1] - so[k]) * record_bytes(class_bits(k), d, S);
+    for (int k = 0; k < 4; k++) t += (int64_t)(so[k + 1] - so[k]) * record_bytes(class_bits(k), d, S, gran);
     img[b] = t;
   }
   __syncthreads();
@@ -318,6 +318,140 @@ WQ_DEV void quant_v_tile(const uint8_t *vbox, float2 *vp, uint8_t *rec, int vt, 
   }
 }
 
+// Paper-literal groups (reading Q37): the IEEE minimum / maximum of ALL S x d values
+// of one tensor of the window (its d/64 boxes, any order: the set of values is the window),
+// by one warp: 16-byte chunks lane-strided (conflict-free), then a shuffle reduction.
+template <int D, int S>
+WQ_DEV void group_minmax(const uint8_t *boxes, int lane, __half &mn, __half &mx) {
+  using QG = QuantGeo<D, S>;
+  constexpr int NCH = QG::KH * QG::BOX / 16;
+  __half2 mn2 = __float2half2_rn(65504.f), mx2 = __float2half2_rn(-65504.f);
+#pragma unroll 4
+  for (int i = lane; i < NCH; i += 32) {
+    const uint4 v = lds128(boxes + 16 * i);
+    const __half2 x0 = u2h(v.x), x1 = u2h(v.y), x2 = u2h(v.z), x3 = u2h(v.w);
+    mn2 = __hmin2(mn2, __hmin2(__hmin2(x0, x1), __hmin2(x2, x3)));
+    mx2 = __hmax2(mx2, __hmax2(__hmax2(x0, x1), __hmax2(x2, x3)));
+  }
+  mn = __hmin(__low2half(mn2), __high2half(mn2));
+  mx = __hmax(__low2half(mx2), __high2half(mx2));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    mn = __hmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = __hmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+}
+
+// K channel half hf of a window under group granularity: the window's single (s, mn)
+// (computed by every K task from the whole window), codes of this half
+template <int D, int S, int BITS>
+WQ_DEV void quant_k_half_grp(const uint8_t *kbox, uint8_t *rec, int hf, int lane) {
+  using QG = QuantGeo<D, S>;
+  constexpr float QMAX = (float)((1 << BITS) - 1);
+  constexpr int PPW = 16 / BITS;
+  constexpr int CW = D * BITS / 64;
+  constexpr int TILE = 2 * D * BITS;
+  constexpr int KBYTES = S * D * BITS / 8;
+  __half mnh, mxh;
+  group_minmax<D, S>(kbox, lane, mnh, mxh);
+  const float mn = __half2float(mnh);
+  const __half s16 = q17_scale(mn, __half2float(mxh), QMAX);
+  const float r = __frcp_rn(__half2float(s16));
+  if (hf == 0 && lane == 0) {
+    // the 16-byte block {mn_K, s_K, mn_V, s_V, 0, 0, 0, 0}: K half 0 writes K's pair and the zeros
+    const uint32_t kp = (uint32_t)__half_as_ushort(mnh) | ((uint32_t)__half_as_ushort(s16) << 16);
+    *reinterpret_cast<uint32_t *>(rec + 2 * KBYTES) = kp;
+    *reinterpret_cast<uint2 *>(rec + 2 * KBYTES + 8) = make_uint2(0u, 0u);
+  }
+  constexpr int WH = CW / 2 > 0 ? CW / 2 : 1;
+  const int g = lane >> 2, q = lane & 3;
+  int gx[8];
+#pragma unroll
+  for (int cc = 0; cc < 8; cc++) gx[cc] = (cc ^ g) << 4;
+  const uint8_t *lb = kbox + g * 128 + 4 * q;
+#pragma unroll 1
+  for (int tile = 0; tile < S / 16; tile++) {
+    const uint8_t *tb0 = lb + tile * 16 * 128;
+    uint32_t wv[WH];
+#pragma unroll
+    for (int e = 0; e < WH; e++) {
+      const int wl = hf * WH + e;
+      uint32_t acc = PackBias<BITS>::value();
+#pragma unroll
+      for (int j = 0; j < PPW; j++) {
+        const int P = wl * PPW + j, m = P >> 2, rr = P & 3;
+        const int cc = (2 * m + (rr >> 1)) & 7;
+        const float2 x = __half22float2(u2h(lds32(tb0 + (m >> 2) * QG::BOX + 8 * (rr & 1) * 128 + gx[cc])));
+        acc += q17_big(x.x, mn, r) * (1u << (BITS * j));
+        acc += q17_big(x.y, mn, r) * (1u << (16 + BITS * j));
+      }
+      wv[e] = acc;
+    }
+    uint8_t *tb = rec + tile * TILE;
+    if constexpr (CW >= 4) {
+#pragma unroll
+      for (int e0 = 0; e0 < WH; e0 += (WH >= 4 ? 4 : 2)) {
+        const int wl = hf * WH + e0;
+        uint8_t *dst = tb + (wl >> 2) * 512 + lane * 16 + 4 * (wl & 3);
+        if constexpr (WH >= 4) *reinterpret_cast<uint4 *>(dst) = make_uint4(wv[e0], wv[e0 + 1], wv[e0 + 2], wv[e0 + 3]);
+        else *reinterpret_cast<uint2 *>(dst) = make_uint2(wv[e0], wv[e0 + 1]);
+      }
+    } else {
+      *reinterpret_cast<uint32_t *>(tb + lane * 8 + 4 * hf) = wv[0];
+    }
+  }
+}
+
+// V tile vt under group granularity: the window's single (s, mn) for V, codes of this tile
+template <int D, int S, int BITS>
+WQ_DEV void quant_v_tile_grp(const uint8_t *vbox, uint8_t *rec, int vt, int lane) {
+  using QG = QuantGeo<D, S>;
+  constexpr float QMAX = (float)((1 << BITS) - 1);
+  constexpr int PPW = 16 / BITS;
+  constexpr int CW = D * BITS / 64;
+  constexpr int TILE = 2 * D * BITS;
+  constexpr int KBYTES = S * D * BITS / 8;
+  __half mnh, mxh;
+  group_minmax<D, S>(vbox, lane, mnh, mxh);
+  const float mn = __half2float(mnh);
+  const __half s16 = q17_scale(mn, __half2float(mxh), QMAX);
+  const float r = __frcp_rn(__half2float(s16));
+  if (vt == 0 && lane == 0)
+    *reinterpret_cast<uint32_t *>(rec + 2 * KBYTES + 4) =
+        (uint32_t)__half_as_ushort(mnh) | ((uint32_t)__half_as_ushort(s16) << 16);
+  const int g = lane >> 2, q = lane & 3;
+  uint8_t *tb = rec + KBYTES + vt * TILE;
+  constexpr int NG = CW >= 4 ? CW / 4 : 1;
+  int qx0[8], qx1[8];
+#pragma unroll
+  for (int cc = 0; cc < 8; cc++) { qx0[cc] = (cc ^ (2 * q)) << 4; qx1[cc] = 128 + ((cc ^ (2 * q + 1)) << 4); }
+  const uint8_t *lb = vbox + (vt * 16 + 2 * q) * 128 + 2 * g;
+#pragma unroll
+  for (int gi = 0; gi < NG; gi++) {
+    uint32_t wv[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int e = 0; e < (CW >= 4 ? 4 : CW); e++) {
+      const int wl = 4 * gi + e;
+      uint32_t acc = PackBias<BITS>::value();
+#pragma unroll
+      for (int j = 0; j < PPW; j++) {
+        const int P = wl * PPW + j, m = P >> 2, rr = P & 3;
+        const int cc = (2 * m + (rr & 1)) & 7;
+        const uint8_t *rb = lb + (m >> 2) * QG::BOX + 8 * (rr >> 1) * 128;
+        const float x0 = __half2float(*reinterpret_cast<const __half *>(rb + qx0[cc]));
+        const float x1 = __half2float(*reinterpret_cast<const __half *>(rb + qx1[cc]));
+        acc += q17_big(x0, mn, r) * (1u << (BITS * j));
+        acc += q17_big(x1, mn, r) * (1u << (16 + BITS * j));
+      }
+      wv[e] = acc;
+    }
+    if constexpr (CW >= 4)
+      *reinterpret_cast<uint4 *>(tb + gi * 512 + lane * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    else
+      *reinterpret_cast<uint2 *>(tb + lane * 8) = make_uint2(wv[0], wv[1]);
+  }
+}
+
 // FP16 window, task tk: K halves / V tiles copied into fragment order.
 template <int D, int S>
 WQ_DEV void copy_task_fp16(const uint8_t *kbox, const uint8_t *vbox, uint8_t *rec, int tk, int lane) {
@@ -366,9 +500,10 @@ WQ_DEV void tma_load_4d(void *dst, const CUtensorMap *tm, int c0, int c1, int c2
       : "memory");
 }
 
-template <int D, int S>
+template <int D, int S, bool GRP>
 __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1)
     k_quant(QuantArgs a, const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
+  constexpr int GR = GRP ? 1 : 0;
   using QG = QuantGeo<D, S>;
   extern __shared__ __align__(1024) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -432,10 +567,11 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1)
     int64_t roff = m.base;
 #pragma unroll
     for (int kk = 0; kk < 3; kk++)
-      if (kk < cls) roff += (int64_t)(m.so[kk + 1] - m.so[kk]) * record_bytes(class_bits(kk), D, S);
+      if (kk < cls) roff += (int64_t)(m.so[kk + 1] - m.so[kk]) * record_bytes(class_bits(kk), D, S, GR);
     const int sbase = cls == 0 ? m.so[0] : cls == 1 ? m.so[1] : cls == 2 ? m.so[2] : m.so[3];
-    roff += (int64_t)(slot - sbase) * record_bytes(bits, D, S);
-    WQ_CHECK(roff >= a.offs[(int64_t)b * a.H + h] && roff + record_bytes(bits, D, S) <= a.offs[(int64_t)b * a.H + h + 1]);
+    roff += (int64_t)(slot - sbase) * record_bytes(bits, D, S, GR);
+    WQ_CHECK(roff >= a.offs[(int64_t)b * a.H + h] &&
+             roff + record_bytes(bits, D, S, GR) <= a.offs[(int64_t)b * a.H + h + 1]);
     wdesc[sl].roff = roff;
     wdesc[sl].bits = bits;
     uint8_t *dst = tbase + (size_t)sl * QG::WIN;
@@ -472,10 +608,26 @@ __global__ void __launch_bounds__(QuantGeo<D, S>::TEAMS * 128, 1)
     if (bits) {
       uint8_t *rec = a.packed + wdesc[sl].roff;
       const uint8_t *kbox = tbase + (size_t)sl * QG::WIN, *vbox = kbox + QG::KH * QG::BOX;
-      for (int tk = tw; tk < QG::NT; tk += 4) {
-        if (bits == 16) {
-          copy_task_fp16<D, S>(kbox, vbox, rec, tk, lane);
-        } else if (tk < 2) {
+      // one task loop per record kind: with the kind tested inside a single loop, ptxas
+      // 12.9 mis-allocated k_quant<128, S >= 64, true> (a K task clobbered the thread-index
+      // register the next FP16 V task of the same warp reused: odd-token halves of V tiles
+      // 2-3 read from wrong rows; tests/test_gpu_group.py caught it)
+      if (bits == 16) {
+        for (int tk = tw; tk < QG::NT; tk += 4) copy_task_fp16<D, S>(kbox, vbox, rec, tk, lane);
+      } else if constexpr (GRP) {
+        for (int tk = tw; tk < QG::NT; tk += 4) {
+          if (tk < 2) {
+            if (bits == 2) quant_k_half_grp<D, S, 2>(kbox, rec, tk, lane);
+            else if (bits == 4) quant_k_half_grp<D, S, 4>(kbox, rec, tk, lane);
+            else quant_k_half_grp<D, S, 8>(kbox, rec, tk, lane);
+          } else {
+            if (bits == 2) quant_v_tile_grp<D, S, 2>(vbox, rec, tk - 2, lane);
+            else if (bits == 4) quant_v_tile_grp<D, S, 4>(vbox, rec, tk - 2, lane);
+            else quant_v_tile_grp<D, S, 8>(vbox, rec, tk - 2, lane);
+          }
+        }
+      } else for (int tk = tw; tk < QG::NT; tk += 4) {
+        if (tk < 2) {
           if (bits == 2) quant_k_half<D, S, 2>(kbox, scr, rec, tk, lane);
           else if (bits == 4) quant_k_half<D, S, 4>(kbox, scr, rec, tk, lane);
           else quant_k_half<D, S, 8>(kbox, scr, rec, tk, lane);
@@ -518,12 +670,12 @@ static bool encode_kv_map(CUtensorMap *tm, const __half *base, int B, int H, int
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D, int S>
+template <int D, int S, bool GRP>
 static cudaError_t launch_quant_t(const QuantArgs &a, cudaStream_t st) {
   using QG = QuantGeo<D, S>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_quant<D, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_quant<D, S, GRP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)QG::total);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -539,7 +691,7 @@ static cudaError_t launch_quant_t(const QuantArgs &a, cudaStream_t st) {
   if (!encode_kv_map(&tmk, a.k, a.B, a.H, T, D, S, a.sb, a.sh, a.st) ||
       !encode_kv_map(&tmv, a.v, a.B, a.H, T, D, S, a.sb, a.sh, a.st))
     return cudaErrorInvalidValue;
-  k_quant<D, S><<<(unsigned)grid, QG::TEAMS * 128, QG::total, st>>>(a, tmk, tmv);
+  k_quant<D, S, GRP><<<(unsigned)grid, QG::TEAMS * 128, QG::total, st>>>(a, tmk, tmv);
   return cudaGetLastError();
 }
 
@@ -571,20 +723,20 @@ cudaError_t launch_shard_slots(const int32_t *perm, const int32_t *seg, int B, i
   return cudaGetLastError();
 }
 
-cudaError_t launch_layer_layout(const int32_t *seg_off, int B, int H, int d, int S, int64_t *offs,
+cudaError_t launch_layer_layout(const int32_t *seg_off, int B, int H, int d, int S, int gran, int64_t *offs,
                                 cudaStream_t st) {
-  k_layer_layout<<<1, 256, (size_t)B * sizeof(int64_t), st>>>(seg_off, B, H, d, S, offs);
+  k_layer_layout<<<1, 256, (size_t)B * sizeof(int64_t), st>>>(seg_off, B, H, d, S, gran, offs);
   return cudaGetLastError();
 }
 
 cudaError_t launch_quant(const __half *k, const __half *v, const int64_t strides[3], int vis_off,
                          int B, int H, int d, int S, int M, const int32_t *perm, int perm_stride,
-                         const int32_t *seg_off, const int64_t *offs, uint8_t *packed,
+                         const int32_t *seg_off, const int64_t *offs, uint8_t *packed, int gran,
                          cudaStream_t st) {
   QuantArgs a{k, v, strides[0], strides[1], strides[2], vis_off, B, H, d, S, M, perm, perm_stride,
               seg_off, offs, packed};
 #define WQ_Q(DD, SS) \
-  if (d == DD && S == SS) return launch_quant_t<DD, SS>(a, st);
+  if (d == DD && S == SS) return gran ? launch_quant_t<DD, SS, true>(a, st) : launch_quant_t<DD, SS, false>(a, st);
   WQ_Q(64, 16) WQ_Q(64, 32) WQ_Q(64, 64) WQ_Q(64, 128)
   WQ_Q(128, 16) WQ_Q(128, 32) WQ_Q(128, 64) WQ_Q(128, 128)
 #undef WQ_Q

@@ -35,9 +35,11 @@ namespace wq {
 // bits of width class k (segment order of a packed image, Alg.2)
 WQ_DEV int class_bits(int k) { return k == 0 ? 2 : k == 1 ? 4 : k == 2 ? 8 : 16; }
 
-// Bytes of one window record (D-1): codes K|V, then (s, mn) params K|V.
-__host__ __device__ __forceinline__ int64_t record_bytes(int bits, int d, int S) {
-  return bits == 16 ? 4LL * S * d : (int64_t)S * d * bits / 4 + 4LL * d + 4LL * S;
+// Bytes of one window record (D-1): codes K|V, then (s, mn) params K|V -- per channel /
+// per token (gran 0), or one 16-byte block {mn_K, s_K, mn_V, s_V, 0...} per window-head
+// (gran 1: the paper-literal groups of P:508, reading Q37).
+__host__ __device__ __forceinline__ int64_t record_bytes(int bits, int d, int S, int gran = 0) {
+  return bits == 16 ? 4LL * S * d : (int64_t)S * d * bits / 4 + (gran ? 16LL : 4LL * d + 4LL * S);
 }
 
 // ---------------------------------------------------------------------------

@@ -34,13 +34,13 @@ cudaError_t launch_search(const __half *vis, int64_t vrs, int64_t vbs, const __h
                           double *scores, int32_t *order, uint8_t *bits, int32_t *rank, int32_t *perm, int32_t *seg,
                           cudaStream_t st);
 
-cudaError_t launch_layer_layout(const int32_t *seg_off, int B, int H, int d, int S, int64_t *offs,
+cudaError_t launch_layer_layout(const int32_t *seg_off, int B, int H, int d, int S, int gran, int64_t *offs,
                                 cudaStream_t st);
 cudaError_t launch_shard_slots(const int32_t *perm, const int32_t *seg, int B, int W, int G, int r,
                                int32_t *perm_r, int32_t *seg_r, cudaStream_t st);
 cudaError_t launch_quant(const __half *k, const __half *v, const int64_t strides[3], int vis_off,
                          int B, int H, int d, int S, int M, const int32_t *perm, int perm_stride,
-                         const int32_t *seg_off, const int64_t *offs, uint8_t *packed,
+                         const int32_t *seg_off, const int64_t *offs, uint8_t *packed, int gran,
                          cudaStream_t st);
 
 struct DecodeArgs {

@@ -69,8 +69,11 @@ def load(build_if_missing: bool = True):
         "wq_search": [P, I64, I64, P, I64, I64, I32, I32, I32, P, I32, C.POINTER(Geom), C.POINTER(AssignOpts), P, P,
                       P, P, P, P, SZ, P],
         "wq_packed_bytes": [C.POINTER(Geom), P, I32, P],
+        "wq_packed_bytes_ex": [C.POINTER(Geom), P, I32, I32, P],
         "wq_layer_layout": [C.POINTER(Geom), P, P, P],
+        "wq_layer_layout_ex": [C.POINTER(Geom), P, I32, P, P],
         "wq_reorder_quantize_pack": [P, P, P, I32, C.POINTER(Geom), P, I32, P, P, P, P],
+        "wq_reorder_quantize_pack_ex": [P, P, P, I32, C.POINTER(Geom), P, I32, P, P, I32, P, P],
         "wq_decode_workspace": [C.POINTER(Geom), P],
         "wq_decode_attention": [P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, P, SZ, P],
         "wq_decode_attention_ex": [P, P, P, P, C.POINTER(Geom), P, P, P, P, I32, F32, P, P, P, SZ, C.c_uint32, P],
@@ -103,7 +106,8 @@ def load(build_if_missing: bool = True):
 def exported_symbols():
     return ["wq_thresholds", "wq_window_scores_workspace", "wq_window_scores", "wq_window_scores_ex",
             "wq_window_scores_layer", "wq_assign_bits", "wq_search_workspace", "wq_search",
-            "wq_packed_bytes", "wq_layer_layout", "wq_reorder_quantize_pack", "wq_decode_workspace",
+            "wq_packed_bytes", "wq_packed_bytes_ex", "wq_layer_layout", "wq_layer_layout_ex",
+            "wq_reorder_quantize_pack", "wq_reorder_quantize_pack_ex", "wq_decode_workspace",
             "wq_decode_attention", "wq_decode_attention_ex", "wq_merge_partials", "wq_shard_slots", "wq_dequant_layout", "wq_dequantize_image",
             "wq_unreordered_layout", "wq_unreorder_image", "wq_decode_attention_unreordered",
             "wq_peer_buffer_bytes", "wq_peer_error_offset", "wq_decode_attention_peer",
@@ -199,29 +203,45 @@ def wq_assign_bits(scores: torch.Tensor, thr, L: int, g: Geom, opts: AssignOpts 
     return bits, rank, perm, seg_off
 
 
-def wq_packed_bytes(g: Geom, n_per_class, code_bytes_only: bool = False) -> int:
+WQ_GRAN_CHANNEL_TOKEN, WQ_GRAN_GROUP = 0, 1
+
+
+def wq_packed_bytes(g: Geom, n_per_class, code_bytes_only: bool = False, gran: int = 0) -> int:
+    """gran: WQ_GRAN_* (non-zero calls wq_packed_bytes_ex)."""
     import numpy as np
     n = np.ascontiguousarray(n_per_class, dtype=np.int32)
     out = C.c_int64(0)
-    _check(load().wq_packed_bytes(C.byref(g), _host_ptr(n), int(code_bytes_only), C.byref(out)))
+    if gran:
+        _check(load().wq_packed_bytes_ex(C.byref(g), _host_ptr(n), int(code_bytes_only), int(gran), C.byref(out)))
+    else:
+        _check(load().wq_packed_bytes(C.byref(g), _host_ptr(n), int(code_bytes_only), C.byref(out)))
     return out.value
 
 
-def wq_layer_layout(g: Geom, seg_off_l: torch.Tensor, offs=None, stream=None) -> torch.Tensor:
+def wq_layer_layout(g: Geom, seg_off_l: torch.Tensor, offs=None, stream=None, gran: int = 0) -> torch.Tensor:
     if offs is None:
         offs = torch.empty(g.B * g.H + 1, dtype=torch.int64, device=seg_off_l.device)
-    _check(load().wq_layer_layout(C.byref(g), _ptr(seg_off_l), _ptr(offs), _stream(stream)))
+    if gran:
+        _check(load().wq_layer_layout_ex(C.byref(g), _ptr(seg_off_l), int(gran), _ptr(offs), _stream(stream)))
+    else:
+        _check(load().wq_layer_layout(C.byref(g), _ptr(seg_off_l), _ptr(offs), _stream(stream)))
     return offs
 
 
 def wq_reorder_quantize_pack(k: torch.Tensor, v: torch.Tensor, vis_off: int, g: Geom, perm_l: torch.Tensor,
-                             seg_off_l: torch.Tensor, offs: torch.Tensor, packed: torch.Tensor, stream=None):
-    """k, v fp16 [B][H][T][d] (channel stride 1); perm_l i32 [B][Ws]; seg_off_l i32 [B][5]."""
+                             seg_off_l: torch.Tensor, offs: torch.Tensor, packed: torch.Tensor, stream=None,
+                             gran: int = 0):
+    """k, v fp16 [B][H][T][d] (channel stride 1); perm_l i32 [B][Ws]; seg_off_l i32 [B][5].
+    gran: WQ_GRAN_* (non-zero calls wq_reorder_quantize_pack_ex)."""
     assert k.stride() == v.stride() and k.stride(3) == 1
     strides = (C.c_int64 * 3)(k.stride(0), k.stride(1), k.stride(2))
-    _check(load().wq_reorder_quantize_pack(_ptr(k), _ptr(v), strides, vis_off, C.byref(g), _ptr(perm_l),
-                                           perm_l.shape[-1], _ptr(seg_off_l), _ptr(offs), _ptr(packed),
-                                           _stream(stream)))
+    L = load()
+    head = (_ptr(k), _ptr(v), strides, vis_off, C.byref(g), _ptr(perm_l), perm_l.shape[-1], _ptr(seg_off_l),
+            _ptr(offs))
+    if gran:
+        _check(L.wq_reorder_quantize_pack_ex(*head, int(gran), _ptr(packed), _stream(stream)))
+    else:
+        _check(L.wq_reorder_quantize_pack(*head, _ptr(packed), _stream(stream)))
     return packed
 
 
@@ -232,13 +252,14 @@ def wq_decode_workspace(g: Geom) -> int:
 
 
 WQ_DECODE_EARLY = 1
+WQ_DECODE_GROUP = 2     # the image is WQ_GRAN_GROUP
 
 
 def wq_decode_attention(q: torch.Tensor, packed: torch.Tensor, offs: torch.Tensor, seg_off_l: torch.Tensor,
                         g: Geom, k_rest, v_rest, rest_len, sm_scale: float, out=None, partial=None,
                         workspace=None, stream=None, flags: int = 0):
     """q fp16 [B][Hq][d]; k_rest/v_rest fp16 [B][H][R_max][d] (or None); rest_len i32 [B].
-    flags: WQ_DECODE_EARLY (see include/wq.h) calls wq_decode_attention_ex."""
+    flags: WQ_DECODE_EARLY | WQ_DECODE_GROUP (see include/wq.h) calls wq_decode_attention_ex."""
     if workspace is None:
         workspace = torch.zeros(wq_decode_workspace(g), dtype=torch.uint8, device=q.device)
     R_max = 0 if k_rest is None else k_rest.shape[2]

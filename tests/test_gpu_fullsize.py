@@ -62,23 +62,25 @@ def search(orc, cfg):
     return g, perm, seg
 
 
-def layer_check(orc, cfg, g, perm_l, seg_l, layer, byte_reqs, attn_reqs):
+def layer_check(orc, cfg, g, perm_l, seg_l, layer, byte_reqs, attn_reqs, gran=0):
+    """gran: WQ_GRAN_* of the packed image (1: the paper-literal groups, WQ_DECODE_GROUP)."""
     m = cfg.model
     K, V, kr, vr, rest_len = synth.layer_tensors(cfg, layer, "cuda")
     q = synth.queries(cfg.B, m.Hq, m.H, m.d, cfg.seed, layer, device="cuda")
     sm = 1 / math.sqrt(m.d)
-    offs = wq.wq_layer_layout(g, seg_l)
+    offs = wq.wq_layer_layout(g, seg_l, gran=gran)
     packed = torch.zeros(int(offs[-1].item()) + 16, dtype=torch.uint8, device="cuda")
-    wq.wq_reorder_quantize_pack(K, V, 0, g, perm_l, seg_l, offs, packed)
+    wq.wq_reorder_quantize_pack(K, V, 0, g, perm_l, seg_l, offs, packed, gran=gran)
     out = torch.empty((cfg.B, m.Hq, m.d), dtype=torch.float16, device="cuda")
-    wq.wq_decode_attention(q, packed, offs, seg_l, g, kr, vr, rest_len, sm, out=out)
+    wq.wq_decode_attention(q, packed, offs, seg_l, g, kr, vr, rest_len, sm, out=out,
+                           flags=wq.WQ_DECODE_GROUP if gran else 0)
     torch.cuda.synchronize()
     g1 = orc.geom(1, m.H, m.Hq, m.d, cfg.M, cfg.S, list(cfg.widths))
     pm, sg = perm_l.cpu().numpy(), seg_l.cpu().numpy()
     of = offs.cpu().numpy()
     for b in byte_reqs:
         opk, ooffs = orc.reorder_quantize_pack(K[b:b + 1].cpu().numpy(), V[b:b + 1].cpu().numpy(), 0, g1,
-                                               pm[b:b + 1], sg[b:b + 1])
+                                               pm[b:b + 1], sg[b:b + 1], gran=gran)
         n = int(ooffs[-1])
         got = packed[int(of[b * m.H]):int(of[b * m.H]) + n].cpu().numpy()
         assert np.array_equal(got, opk[:n]), (cfg.name, layer, b)
@@ -87,7 +89,7 @@ def layer_check(orc, cfg, g, perm_l, seg_l, layer, byte_reqs, attn_reqs):
         ob = of[b * m.H:(b + 1) * m.H + 1] - of[b * m.H]
         ref = orc.decode_attention(q[b:b + 1].cpu().numpy(), packed[lo:hi].cpu().numpy(), ob, sg[b:b + 1],
                                    pm[b:b + 1], g1, kr[b:b + 1].cpu().numpy(), vr[b:b + 1].cpu().numpy(),
-                                   rest_len[b:b + 1].cpu().numpy(), sm)
+                                   rest_len[b:b + 1].cpu().numpy(), sm, gran=gran)
         e = rel_err(out[b:b + 1].float().cpu().numpy(), ref)
         assert e <= ATTN_TOL, (cfg.name, layer, b, e)
 
@@ -115,6 +117,16 @@ def test_c5_all_requests_bytes(orc):
     for l in range(cfg.layers):
         byte_reqs = list(range(cfg.B)) if l in (0, 9, 18, cfg.layers - 1) else []
         layer_check(orc, cfg, g, perm[l], seg[l], l, byte_reqs, [l % cfg.B])
+
+
+@pytest.mark.parametrize("name,S", [("C5", None), ("C4", 16), ("C4", 128), ("C2", None)])
+def test_group_granularity_full_size(orc, name, S):
+    """The paper-literal group quantizer (WQ_GRAN_GROUP, reading Q37) at full config size:
+    bytes of every request and attention of one request on 3 layers."""
+    cfg = configs.c4(S) if name == "C4" else configs.CONFIGS[name]
+    g, perm, seg = search(orc, cfg)
+    for l in (0, cfg.layers // 2, cfg.layers - 1):
+        layer_check(orc, cfg, g, perm[l], seg[l], l, list(range(min(cfg.B, 4))), [l % cfg.B], gran=1)
 
 
 def test_bench_launch_path_c5(orc):
