@@ -418,11 +418,15 @@ def run_wq(args, rank, world, local_rank):
     achieved = dec_bytes / (dec_launch_us * 1e-6) / 1e9
     q_bytes = float(sum(w.quant_bytes_per_call(l) for l in range(cfg.layers)))
     q_gbs = q_bytes / (quant_ms * 1e-3) / 1e9
-    traffic = None
+    # traffic: DRAM bytes of one decode launch from an `ncu --set full` capture of this
+    # config (not measured in this run; the capture is named in traffic_source)
+    traffic, traffic_src = None, None
     tf = os.path.join(ROOT, "profiles", "decode_dram_bytes.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(cfg.name)
+            tj = json.load(open(tf))
+            traffic = tj.get(cfg.name)
+            traffic_src = tj.get("_source") if traffic is not None else None
         except Exception:
             traffic = None
     result = {
@@ -441,6 +445,7 @@ def run_wq(args, rank, world, local_rank):
                    "window_mix": dict(zip(["2", "4", "8", "16"], [int(x) for x in w.class_windows]))},
         "roofline": {"bound": "hbm", "kernel": "wq_decode_attention", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "bytes_per_launch": round(dec_bytes), "avg_launch_us": round(dec_launch_us, 3),
                      "peak_source": peak_src},
         "quantize": {"kernel": "wq_reorder_quantize_pack", "GB/s": round(q_gbs, 1),
@@ -454,6 +459,8 @@ def run_wq(args, rank, world, local_rank):
         result["ablation_unfused_t9"] = run_ablation_unfused(w, stream)
         result["ablation_unreordered_t8"] = run_ablation_unreordered(w, stream)
         result["ablation_similarity_t11"] = run_ablation_similarity(w, stream)
+        result["ablation_group_quantizer"] = run_ablation_group(w, stream)
+        result["ablation_search"] = run_ablation_search(w, stream)
     if not args.no_e2e:
         # every rank runs the end-to-end steps (the sequence split's decodes are
         # collective); the time is the max over ranks, the value the whole job's tokens
@@ -584,6 +591,106 @@ def run_ablation_similarity(w, stream, reps=5):
     return out
 
 
+def _timed_layers(fn, L, stream, reps):
+    """us per call of fn(l) over L rotated layers (one warm-up pass, reps timed passes)."""
+    import torch
+    for l in range(L):
+        fn(l)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        for l in range(L):
+            fn(l)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / (reps * L)
+
+
+def run_ablation_group(w, stream, n_layers=4, reps=5):
+    """the paper-literal group quantizer (WQ_GRAN_GROUP: one (s, mn) per
+    (window, head, K|V), reading Q37) against the default per-channel K / per-token V
+    parameters (Q19) on the bench workload: packed bytes, quantize and decode device time
+    per layer call (n_layers rotated layers, reps passes)."""
+    import torch
+    wq = w.wq
+    L = min(n_layers, w.L)
+    GR = wq.WQ_GRAN_GROUP
+    offs_g = [wq.wq_layer_layout(w.g, w.seg_r[l], gran=GR) for l in range(L)]
+    torch.cuda.synchronize()
+    bytes_g = [int(o[-1].item()) for o in offs_g]
+    imgs_g = [torch.zeros(n + 16, dtype=torch.uint8, device=w.dev) for n in bytes_g]
+    rl = w.rest_len[0]
+
+    def quant(gran):
+        def f(l):
+            offs, img = (offs_g[l], imgs_g[l]) if gran else (w.offs[l], w.packed[l])
+            wq.wq_reorder_quantize_pack(w.K[l], w.V[l], 0, w.g, w.perm_r[l], w.seg_r[l], offs, img, gran=gran)
+        return f
+
+    def dec(gran):
+        def f(l):
+            offs, img = (offs_g[l], imgs_g[l]) if gran else (w.offs[l], w.packed[l])
+            wq.wq_decode_attention(w.q[0, l], img, offs, w.seg_r[l], w.g, w.kr[l], w.vr[l], rl, w.sm_scale,
+                                   out=w.out[0, l], workspace=w.dws, flags=wq.WQ_DECODE_GROUP if gran else 0)
+        return f
+
+    tq0, tq1 = _timed_layers(quant(0), L, stream, reps), _timed_layers(quant(GR), L, stream, reps)
+    td0, td1 = _timed_layers(dec(0), L, stream, reps), _timed_layers(dec(GR), L, stream, reps)
+    b0 = sum(w.packed_bytes[:L]) / L
+    b1 = sum(bytes_g) / L
+    rest = w.decode_bytes_per_call(0) - w.packed_bytes[0]
+    del imgs_g
+    return {"packed_MB_per_layer": {"channel_token": round(b0 / 1e6, 2), "group": round(b1 / 1e6, 2)},
+            "group_over_channel_token_bytes": round(b1 / b0, 4),
+            "quantize_us": {"channel_token": round(tq0, 2), "group": round(tq1, 2)},
+            "decode_us": {"channel_token": round(td0, 2), "group": round(td1, 2)},
+            "decode_GBps": {"channel_token": round((b0 + rest) / (td0 * 1e-6) / 1e9, 1),
+                            "group": round((b1 + rest) / (td1 * 1e-6) / 1e9, 1)},
+            "note": "same windows, widths and kernels' structure; group = 16 B of parameters per record "
+                    "instead of 4(d + S)"}
+
+
+def run_ablation_search(w, stream, reps=5):
+    """SURVEY §8(f) row 4 and the fused search: (a) the unfused chain wq_window_scores +
+    wq_assign_bits (the bench step's search), (b) wq_search (one cooperative launch, the
+    same results), (c) the per-layer K/Q scorer (wq_window_scores_layer: visual keys of
+    layer l vs that layer's text queries, reading Q36) + a per-layer assignment -- L calls
+    each.  Device time per search of all L layers."""
+    import torch
+    from paper_2605_02262_b200 import synth
+    wq, cfg, m = w.wq, w.cfg, w.m
+    L, B, W = w.L, cfg.B, cfg.W
+    fo = (w.scores, w.bits, w.rank_t, w.perm, w.seg)
+    qt = synth.text_queries(B, m.Hq, cfg.n_text, m.d, cfg.seed, 0, w.dev)
+    sl = torch.empty((B, W), dtype=torch.float64, device=w.dev)
+    lws = torch.empty(wq.wq_window_scores_workspace(B, m.H * m.d), dtype=torch.uint8, device=w.dev)
+    bl = torch.empty((1, B, W), dtype=torch.uint8, device=w.dev)
+    rk = torch.empty((B, W), dtype=torch.int32, device=w.dev)
+    pl = torch.empty((1, B, W), dtype=torch.int32, device=w.dev)
+    sg = torch.empty((1, B, 5), dtype=torch.int32, device=w.dev)
+
+    def chain(_):
+        w.search()
+
+    def fused(_):
+        wq.wq_search(w.vis, w.txt, w.thr, L, w.g, w.opts, outs=fo)
+
+    def per_layer(_):
+        for l in range(L):
+            wq.wq_window_scores_layer(w.K[l], 0, qt, cfg.M, cfg.S, scores=sl, workspace=lws)
+            wq.wq_assign_bits(sl, w.thr, 1, w.g, w.opts, bl, rk, pl, sg)
+
+    t_c = _timed_layers(chain, 1, stream, reps)
+    t_f = _timed_layers(fused, 1, stream, reps)
+    t_l = _timed_layers(per_layer, 1, stream, reps)
+    w.search()                                              # restore the step's plan
+    torch.cuda.synchronize()
+    return {"chain_us": round(t_c, 1), "fused_us": round(t_f, 1), "per_layer_scorer_us": round(t_l, 1),
+            "fused_over_chain": round(t_f / t_c, 3),
+            "layers": L, "note": "chain = the step's search; fused = wq_search (bit-identical outputs); "
+                                 "per_layer = L x (wq_window_scores_layer + wq_assign_bits with L = 1)"}
+
+
 def imgs_bytes(w, l):
     """bytes of layer l's FP16 image: every slot at 4*S*d bytes per (b, h)."""
     n_slots = int(w.seg_r[l][:, 4].sum().item())
@@ -682,6 +789,63 @@ def _cores():
         return os.cpu_count() or 1
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+_ONE_THREAD = r"""
+import json, math, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[2])
+import oracle
+z = np.load(sys.argv[1])
+S, d, H, Hq = (int(z[k]) for k in ("S", "d", "H", "Hq"))
+vis, txt, K, V = z["vis"], z["txt"], z["K"], z["V"]
+nw = vis.shape[1] // S
+t0 = time.perf_counter()
+oracle.window_scores(vis, txt, S)
+t1 = time.perf_counter()
+M = K.shape[2]
+og = oracle.geom(1, H, Hq, d, M, S, [2, 4, 8, 16])
+pk, offs = oracle.reorder_quantize_pack(K, V, 0, og, z["perm"], z["seg"])
+t2 = time.perf_counter()
+oracle.decode_attention(z["q"], pk, offs, z["seg"], z["perm"], og, z["kr"], z["vr"], z["rest_len"], 1 / math.sqrt(d))
+t3 = time.perf_counter()
+print(json.dumps({"scores_per_window_s": (t1 - t0) / nw, "quantize_1req_1layer_s": t2 - t1,
+                  "decode_1req_1layer_1token_s": t3 - t2}))
+"""
+
+
+def oracle_one_thread(cfg, w, l, n_windows=48):
+    """The oracle's quantize + decode of one request-layer and its scorer on the first
+    n_windows windows, in a child process with OMP_NUM_THREADS=1 (single-core times)."""
+    import subprocess
+    import tempfile
+    m = cfg.model
+    S = cfg.S
+    with tempfile.TemporaryDirectory() as td:
+        f = os.path.join(td, "s.npz")
+        np.savez(f, vis=w.vis[:1, :n_windows * S].cpu().numpy(), txt=w.txt[:1].cpu().numpy(),
+                 K=w.K[l][:1].cpu().numpy(), V=w.V[l][:1].cpu().numpy(), kr=w.kr[l][:1].cpu().numpy(),
+                 vr=w.vr[l][:1].cpu().numpy(), rest_len=w.rest_len[0][:1].cpu().numpy(),
+                 q=w.q[0, l][:1].cpu().numpy(), perm=w.perm[l][:1].cpu().numpy(), seg=w.seg[l][:1].cpu().numpy(),
+                 S=S, d=m.d, H=m.H, Hq=m.Hq)
+        env = dict(os.environ, OMP_NUM_THREADS="1")
+        try:
+            out = subprocess.run([sys.executable, "-c", _ONE_THREAD, f, ROOT], env=env, capture_output=True,
+                                 text=True, timeout=300)
+            r = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception as e:
+            return {"error": f"{type(e).__name__}: {e}"}
+    return {k: round(v, 4) for k, v in r.items()} | {"threads": 1, "scorer_sample_windows": n_windows}
+
+
 def cpu_baseline(cfg, w, args):
     vis, txt = w.vis[:1].cpu().numpy(), w.txt[:1].cpu().numpy()
     l = cfg.layers - 1
@@ -689,10 +853,12 @@ def cpu_baseline(cfg, w, args):
                w.vr[l][:1].cpu().numpy(), w.rest_len[0][:1].cpu().numpy(), w.q[0, l][:1].cpu().numpy())
     est, per, wall = oracle_sample_time(cfg, tensors)
     return {"value": round(cfg.B * cfg.n_gen / est, 4), "unit": UNIT, "cores": _cores(), "kind": "oracle",
+            "cpu_model": _cpu_model(),
             "sample": (f"request 0, layer {l}, 1 generated token of {cfg.name} (scores + assign + quantize + decode), "
-                       f"{wall:.1f}s of CPU work, extrapolated linearly to B={cfg.B} x {cfg.layers} layers x "
-                       f"{cfg.n_gen} tokens"),
-            "per_phase_s": {k: round(v, 4) for k, v in per.items()}}
+                       f"{wall:.1f}s of CPU work on {_cores()} threads, extrapolated linearly to B={cfg.B} x "
+                       f"{cfg.layers} layers x {cfg.n_gen} tokens"),
+            "per_phase_s": {k: round(v, 4) for k, v in per.items()},
+            "oracle_1thread": oracle_one_thread(cfg, w, l)}
 
 
 def run_reference(args, rank, world):
@@ -718,13 +884,17 @@ def run_reference(args, rank, world):
     ms = float(np.mean(times)) * 1e3
     value = cfg.B * cfg.n_gen / (ms / 1e3)
     return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
+            "ms_per_step_kind": (f"extrapolated: each step times a bounded sample ({wall:.1f}s of CPU work) and "
+                                 f"scales it linearly to the full step"),
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "layers": cfg.layers, "batch": cfg.B, "visual_tokens": cfg.M,
                        "window": cfg.S, "widths": list(cfg.widths), "gen_tokens": cfg.n_gen},
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "kind": "oracle", "cores": _cores(),
                              "sample": (f"each step: request 0, layer {l}, 1 token of {cfg.name}; "
-                                        f"time extrapolated to the full step")},
+                                        f"time extrapolated to the full step"),
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

@@ -20,7 +20,8 @@
  *    NULL = legacy default stream).  Argument validation is synchronous: a call
  *    that returns anything but WQ_OK launched nothing, and wq_last_error()
  *    names the offending argument and shape.
- *  - fp16 tensors are IEEE binary16 (the paper's KV precision).
+ *  - fp16 tensors are IEEE binary16 (the paper's KV precision).  KV,
+ *    queries and outputs are fp16 ONLY: there is no bf16 entry point (Q40).
  *  - No floating-point atomics anywhere: every output is bit-reproducible run
  *    to run and GPU to GPU.
  *  - There is no CPU fallback: every device call launches CUDA kernels.
@@ -98,7 +99,7 @@ typedef struct {
  * (For b = 16 a pair is one word holding two raw fp16 values.)
  *
  * K params (per channel c over the window's S tokens, Q19): 4 x d/16 groups
- * of 16 bytes, group (q, m) at byte (q*(d/16) + m)*16 holds fp16
+ * of 16 bytes, group (q, m) at byte (4*m + q)*16 holds fp16
  *   { mn(c0), mn(c0+1), s(c0), s(c0+1), mn(c0+8), mn(c0+9), s(c0+8), s(c0+9) },
  *   c0 = 16*m + 2*q  (one 16-byte load is directly the mma A fragment of the
  *   zero-point term: rows g hold mn, rows g+8 are ignored).

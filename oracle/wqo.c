@@ -421,7 +421,8 @@ static uint16_t get_u16(const uint8_t *p) { return (uint16_t)(p[0] | (p[1] << 8)
 /* byte offset of the (s, mn) of K channel c / V token t inside the params */
 static int64_t kparam_off(int d, int c, int is_min) {
   int m = c / 16, q = (c % 8) / 2, h = (c % 16) / 8, e = c % 2;
-  return ((int64_t)q * (d / 16) + m) * 16 + 2 * (4 * h + (is_min ? 0 : 2) + e);
+  (void)d;
+  return ((int64_t)4 * m + q) * 16 + 2 * (4 * h + (is_min ? 0 : 2) + e);
 }
 static int64_t vparam_off(int t, int is_min) {
   int i = t / 16, col = t % 16, q = (col % 8) / 2, h = col / 8, e = col % 2;

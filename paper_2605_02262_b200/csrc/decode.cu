@@ -233,7 +233,9 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
       if constexpr (BITS < 16) {
         // {mn01, s01, mn89, s89}: the quad is the zero-point term's A fragment as
         // loaded (rows g: mn, rows g+8: don't-care -- only d0/d1 of b0/b1 are used)
-        const uint4 pr = lds128(kp + (q * KT + kt) * 16);
+        // group (q, kt) at (4 kt + q) * 16: the quads' 4 groups are adjacent 16-byte chunks
+        // (conflict-free; the former q-major order was a 4-way conflict, 2 % of a C5 launch)
+        const uint4 pr = lds128(kp + (4 * kt + q) * 16);
         if (c0 == 0 && !WQ_EXP_NOZP) {
           const uint32_t am[4] = {pr.x, pr.y, pr.z, pr.w};
           if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
@@ -332,8 +334,8 @@ WQ_DEV void do_window2(const uint8_t *recA, const uint8_t *recB, const uint8_t *
 #pragma unroll
   for (int kt = 0; kt < KT; kt++) {
     const uint2 qk = lds64(qs + (kt * 32 + lane) * 8);
-    const uint4 pa = lds128(kpA + (q * KT + kt) * 16);     // {mn01, s01, mn89, s89} of A
-    const uint4 pb = lds128(kpB + (q * KT + kt) * 16);     // ... of B
+    const uint4 pa = lds128(kpA + (4 * kt + q) * 16);     // {mn01, s01, mn89, s89} of A
+    const uint4 pb = lds128(kpB + (4 * kt + q) * 16);     // ... of B
     {
       const uint32_t am[4] = {pa.x, pb.x, pa.z, pb.z};     // rows g: A's minima, rows g + 8: B's
       if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
@@ -432,10 +434,17 @@ WQ_DEV void do_rest(const uint8_t *Kb, const uint8_t *Vb, int ntok, const uint8_
 // -------------------------------------------------------------------------------------
 // the kernel
 // -------------------------------------------------------------------------------------
+// FP16 items per window in reordered mode: 2 when a 64 KB record would leave a 2-stage ring
 template <int D, int S>
+constexpr int fsplit() { return 4 * S * D >= 2 * WQ_DEC_STAGE ? 2 : 1; }
+
+template <int D, int S, int FS = 1>
 struct DecodeSmem {
-  // a stage must hold the largest item (an FP16 window: 4*S*D bytes)
-  static constexpr int STAGE = (4 * S * D > WQ_DEC_STAGE) ? 4 * S * D : WQ_DEC_STAGE;
+  // a stage must hold the largest item: an FP16 window (4*S*D bytes), or an FS-th of it and
+  // the largest quantized record when FP16 windows are split (FS > 1, reordered mode only)
+  static constexpr int REC8 = S * D * 2 + 4 * D + 4 * S;
+  static constexpr int BIG = FS > 1 ? (4 * S * D / FS > REC8 ? 4 * S * D / FS : REC8) : 4 * S * D;
+  static constexpr int STAGE = (BIG > WQ_DEC_STAGE) ? BIG : WQ_DEC_STAGE;
   static constexpr int RING = WQ_DEC_RING;
   static constexpr int NST = (RING / STAGE) < 2 ? 2 : RING / STAGE;
   static constexpr int KT = D / 16;
@@ -639,7 +648,8 @@ size_t peer_buffer_bytes(int B, int H, int Hq, int d, int G) {
 // (blockIdx.x / gridDim.x, or a virtual rank's share of the grid under emulation).
 template <int D, int S, bool UR, bool GRP = false>
 WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
-  using SM = DecodeSmem<D, S>;
+  constexpr int FS = UR ? 1 : fsplit<D, S>();
+  using SM = DecodeSmem<D, S, FS>;
   constexpr int KT = D / 16;
   constexpr int NST = SM::NST;
   constexpr int STAGE = SM::STAGE;
@@ -660,7 +670,7 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
 
   // ---- prologue (warp 0): unit cost prefix, then this CTA's share ----
   CtaPlan *cp = reinterpret_cast<CtaPlan *>(sm + SM::plan_off);
-  if (warp == 0) plan_cta<D, S, false, (!UR && WQ_DEC_STREAM), GRP>(a, ustart, cp, s_flag, lane, vc, vn);
+  if (warp == 0) plan_cta<D, S, false, (!UR && WQ_DEC_STREAM), GRP, FS>(a, ustart, cp, s_flag, lane, vc, vn);
   if (tid == 32) {
     for (int s = 0; s < NST; s++) {
       mbar_init(&full[s], 1);
@@ -686,7 +696,8 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
                                                                       reinterpret_cast<int *>(sm + SM::tab_off), vc);
     } else {
       if (lane == 0)
-        produce<D, S, false, STAGE, NST, SM::NUS, GRP>(a, *cp, ustart, ring, full, empty, ent, units_done, ts, vc);
+        produce<D, S, false, STAGE, NST, SM::NUS, GRP, FS>(a, *cp, ustart, ring, full, empty, ent, units_done, ts,
+                                                           vc);
     }
     return;
   }
@@ -787,7 +798,7 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
     for (int p = UR ? 4 : 0; p < 5; p++) {
       using IG = ItemGeo<D, S, false>;
       // item bytes of class p, computed (a table indexed by p would live in local memory)
-      const int sz = p == 4 ? IG::REST_SZ : (p == 3 ? 4 * S * D : S * D * (2 << p) / 4 + (GRP ? 16 : 4 * D + 4 * S));
+      const int sz = p == 4 ? IG::REST_SZ : (p == 3 ? 4 * S * D / FS : S * D * (2 << p) / 4 + (GRP ? 16 : 4 * D + 4 * S));
       const int cap = STAGE / sz;
       const int len = E.len[p], nst = E.nst[p], lo = E.lo[p];
       // 2-bit stages (S <= 32) are consumed in PAIRS of windows (do_window2): a stage of n
@@ -819,7 +830,7 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
           } else if (p == 2) {
             do_window<D, S, 8, GRP>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum);
           } else if (p == 3) {
-            do_window<D, S, 16>(rec, qs, a.scale_log2, st, o, scratch, lane);
+            do_window<D, S / FS, 16>(rec, qs, a.scale_log2, st, o, scratch, lane);   // (a part of) an FP16 window
           } else {
             const int ii = lo + t * cap + k;
             do_rest<D>(sbase + (size_t)k * 32 * D, sbase + (size_t)(cap + k) * 32 * D, min(16, rl - 16 * (ii - nslots)),
@@ -1007,7 +1018,7 @@ size_t decode_workspace_bytes(int B, int H, int Hq, int d, int num_sms) {
 
 template <int D, int S, bool UR, bool GRP = false>
 static cudaError_t launch_decode_t(const DecodeArgs &a, int num_sms, cudaStream_t st) {
-  using SM = DecodeSmem<D, S>;
+  using SM = DecodeSmem<D, S, UR ? 1 : fsplit<D, S>()>;
   static bool attr_set = false;                  // per instantiation (per process: one device)
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_decode<D, S, UR, GRP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1059,7 +1070,7 @@ cudaError_t launch_decode(const DecodeArgs &a, int num_sms, cudaStream_t st) {
 
 template <int D, int S>
 static cudaError_t launch_emu_t(const DecodeArgs *ra, int nr, int num_sms, cudaStream_t st) {
-  using SM = DecodeSmem<D, S>;
+  using SM = DecodeSmem<D, S, fsplit<D, S>()>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_decode_emu<D, S, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,

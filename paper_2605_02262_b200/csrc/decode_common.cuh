@@ -35,7 +35,10 @@ constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trac
 // across CTAs in COST space, not bytes: every item costs its bytes plus a per-item
 // compute term, so CTAs that get many narrow windows get fewer of them.
 // TC selects the cost table of the tcgen05 kernel.
-template <int D, int S, bool TC = false, bool GRP = false>
+// FS > 1 (S = 128, d = 128: 64 KB FP16 records): an FP16 window is FS items of S/FS
+// tokens each (its K tiles and V tiles of those tokens, copied as one (S/FS)-token FP16
+// record), so a stage need not hold a whole 64 KB record and the ring keeps 4 stages.
+template <int D, int S, bool TC = false, bool GRP = false, int FS = 1>
 struct ItemGeo {
   // record bytes of class k (0..2 = 2/4/8-bit, 3 = FP16), D-1 contract (GRP: the 16-byte
   // parameter block of the paper-literal groups, reading Q37)
@@ -43,7 +46,9 @@ struct ItemGeo {
     return k == 3 ? 4LL * S * D : (int64_t)S * D * (2 << k) / 4 + (GRP ? 16LL : 4LL * D + 4LL * S);
   }
   static constexpr int REST_SZ = 64 * D;               // FP16 rest tile: 16 K rows + 16 V rows
-  static constexpr int sz(int k) { return k == 4 ? REST_SZ : (int)rb(k); }
+  // item bytes: a record, an FS-th of an FP16 record, or a rest tile
+  static constexpr int sz(int k) { return k == 4 ? REST_SZ : (k == 3 ? (int)(rb(3) / FS) : (int)rb(k)); }
+  static constexpr int per_slot(int k) { return k == 3 ? FS : 1; }   // items per window slot
   // Cost of an item ~ its time on one SM inside a full decode launch.
   //  mma.sync kernel: measured per-class CTA-level item times on C5
   //   (tools/dbg_decode_time.py least-squares fit): 2-bit 0.167 us, 4-bit 0.182,
@@ -59,7 +64,8 @@ struct ItemGeo {
                     : (int64_t)(k == 0 ? 100 : k == 1 ? 140 : k == 2 ? 220 : 300) * S * D / 100;
     } else {
       return k == 4 ? (int64_t)WQ_DEC_CR * D
-                    : (int64_t)(k == 0 ? 156 : k == 1 ? 170 : k == 2 ? 233 : WQ_DEC_C16) * S * D / 100;
+                    : (int64_t)(k == 0 ? 156 : k == 1 ? 170 : k == 2 ? 233 : WQ_DEC_C16) * S * D / 100 /
+                          (k == 3 ? FS : 1);
     }
   }
 };
@@ -68,13 +74,14 @@ struct ItemGeo {
 struct UnitGeo {
   int b, h, nslots, rl, ntiles;
   int so[5];
+  int io[6];                            // item starts: classes 0-3 (FS items per FP16 slot), rest, end
   int64_t cs[5];                        // byte start of each class segment; cs[4] = image bytes
   int64_t cc[5];                        // cost start of each class segment; cc[4] = windows' cost
 };
 
-template <int D, int S, bool TC, bool GRP = false>
+template <int D, int S, bool TC, bool GRP = false, int FS = 1>
 WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
-  using IG = ItemGeo<D, S, TC, GRP>;
+  using IG = ItemGeo<D, S, TC, GRP, FS>;
   g.b = u / a.H;
   g.h = u - g.b * a.H;
   const int32_t *so = a.seg_off + 5 * g.b;
@@ -86,33 +93,37 @@ WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
   for (int k = 0; k < 4; k++) {
     const int64_t n = g.so[k + 1] - g.so[k];
     g.cs[k + 1] = g.cs[k] + n * IG::rb(k);
-    g.cc[k + 1] = g.cc[k] + n * IG::cost(k);
+    g.cc[k + 1] = g.cc[k] + n * IG::per_slot(k) * IG::cost(k);
   }
   g.nslots = g.so[4];
   g.rl = a.rest_len ? a.rest_len[g.b] : 0;
   g.rl = g.rl < 0 ? 0 : (g.rl > a.R_max ? a.R_max : g.rl);     // contract: rest_len clamped to R_max
   g.ntiles = (g.rl + 15) / 16;
+#pragma unroll
+  for (int k = 0; k < 4; k++) g.io[k] = g.so[k];
+  g.io[4] = g.so[3] + FS * (g.so[4] - g.so[3]);
+  g.io[5] = g.io[4] + g.ntiles;
 }
-template <int D, int S, bool TC, bool GRP = false>
+template <int D, int S, bool TC, bool GRP = false, int FS = 1>
 WQ_DEV int64_t unit_cost(const UnitGeo &g) {
-  return g.cc[4] + (int64_t)g.ntiles * ItemGeo<D, S, TC, GRP>::cost(4);
+  return g.cc[4] + (int64_t)g.ntiles * ItemGeo<D, S, TC, GRP, FS>::cost(4);
 }
 
 // first item whose start (in cost units, relative to the unit) is >= x.  Planning
 // arithmetic runs in double (no 64-bit integer division on the producer's path);
 // every CTA evaluates the same expressions, so neighbouring CTAs agree on the cut.
-template <int D, int S, bool TC, bool GRP = false>
+template <int D, int S, bool TC, bool GRP = false, int FS = 1>
 WQ_DEV int first_item(const UnitGeo &g, double x) {
-  using IG = ItemGeo<D, S, TC, GRP>;
+  using IG = ItemGeo<D, S, TC, GRP, FS>;
   if (x <= 0.0) return 0;
 #pragma unroll
   for (int k = 0; k < 4; k++) {
-    if (x <= (double)g.cc[k]) return g.so[k];
-    if (x < (double)g.cc[k + 1]) return g.so[k] + (int)ceil((x - (double)g.cc[k]) / (double)IG::cost(k));
+    if (x <= (double)g.cc[k]) return g.io[k];
+    if (x < (double)g.cc[k + 1]) return g.io[k] + (int)ceil((x - (double)g.cc[k]) / (double)IG::cost(k));
   }
-  if (x <= (double)g.cc[4]) return g.nslots;
+  if (x <= (double)g.cc[4]) return g.io[4];
   const int t = (int)ceil((x - (double)g.cc[4]) / (double)IG::cost(4));
-  return g.nslots + (t < g.ntiles ? t : g.ntiles);
+  return g.io[4] + (t < g.ntiles ? t : g.ntiles);
 }
 
 // Stage plan of one unit's item range [i0, i1): five "pieces" (the width-class
@@ -121,13 +132,13 @@ WQ_DEV int first_item(const UnitGeo &g, double x) {
 struct UnitPlan {
   int lo[5], hi[5], nst[5];
 };
-template <int D, int S, bool TC, int STAGE, bool GRP = false>
+template <int D, int S, bool TC, int STAGE, bool GRP = false, int FS = 1>
 WQ_DEV void plan_unit(const UnitGeo &g, int i0, int i1, UnitPlan &pl) {
-  using IG = ItemGeo<D, S, TC, GRP>;
+  using IG = ItemGeo<D, S, TC, GRP, FS>;
 #pragma unroll
   for (int p = 0; p < 5; p++) {
-    const int a0 = p < 4 ? g.so[p] : g.nslots;
-    const int a1 = p < 4 ? g.so[p + 1] : g.nslots + g.ntiles;
+    const int a0 = g.io[p];
+    const int a1 = g.io[p + 1];
     const int lo = i0 > a0 ? i0 : a0;
     const int hi = i1 < a1 ? i1 : a1;
     const int cap = STAGE / IG::sz(p);
@@ -164,7 +175,7 @@ struct CtaPlan {
 // the same cost; a unit-aligned split rounds each unit to a whole number of CTAs.
 // vc / vn: this CTA's index and the CTA count of the grid it plans over (blockIdx.x /
 // gridDim.x, or a virtual rank's share of one grid in the fused-merge emulation).
-template <int D, int S, bool TC, bool STREAM = false, bool GRP = false>
+template <int D, int S, bool TC, bool STREAM = false, bool GRP = false, int FS = 1>
 WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_flag, int lane, int vc, int vn) {
   const int U = a.B * a.H;
   int64_t carry = 0;
@@ -175,8 +186,8 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
     int64_t v = 0;
     if (u < U) {
       ioff = a.offs[u];
-      unit_geo<D, S, TC, GRP>(a, u, gg);
-      v = unit_cost<D, S, TC, GRP>(gg) + (STREAM ? ItemGeo<D, S, TC, GRP>::EOV : 0);
+      unit_geo<D, S, TC, GRP, FS>(a, u, gg);
+      v = unit_cost<D, S, TC, GRP, FS>(gg) + (STREAM ? ItemGeo<D, S, TC, GRP, FS>::EOV : 0);
     }
     int64_t x = v;
 #pragma unroll
@@ -257,10 +268,10 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
 // ---- producer (one lane): stream the CTA's entries into the ring ----
 // Stages of NST x STAGE bytes, full[s] (1 arrival + tx bytes) / empty[s] barriers;
 // entries published in a ring of NUS Entry slots, released via *units_done.
-template <int D, int S, bool TC, int STAGE, int NST, int NUS, bool GRP = false>
+template <int D, int S, bool TC, int STAGE, int NST, int NUS, bool GRP = false, int FS = 1>
 WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart, uint8_t *ring,
                     uint64_t *full, uint64_t *empty, Entry *ent, int *units_done, uint64_t *ts, int vc) {
-  using IG = ItemGeo<D, S, TC, GRP>;
+  using IG = ItemGeo<D, S, TC, GRP, FS>;
   const int c = vc;
   const uint64_t pol = policy_evict_first();
   if (ts) ts[62] = gtime();
@@ -275,7 +286,7 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
     d.c0 = ec0;
     d.c1 = ec1;
     d.rl = gg ? gg->rl : 0;
-    d.nslots = gg ? gg->nslots : 0;
+    d.nslots = gg ? gg->io[4] : 0;               // items before the rest tiles
 #pragma unroll
     for (int pp = 0; pp < 5; pp++) {
       d.lo[pp] = pl ? pl->lo[pp] : 0;
@@ -295,9 +306,9 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
       img_off = P.img_off;
     } else {
       img_off = a.offs[u];
-      unit_geo<D, S, TC, GRP>(a, u, gg);
+      unit_geo<D, S, TC, GRP, FS>(a, u, gg);
     }
-    int i0 = 0, i1 = gg.nslots + gg.ntiles;
+    int i0 = 0, i1 = gg.io[5];
     int ec0 = P.split == 1 ? P.c0 : c, ec1 = P.split == 1 ? P.c1 : c + 1;
     if (P.split == 1) {
       // the unit's cost plus the last CTA's merge allowance, cut into n equal shares: the
@@ -306,18 +317,18 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
       const double lov = (double)WQ_DEC_LOV * S * D / 100;
       const double ucost = (double)(ustart[u + 1] - ustart[u]) + lov;
       const int k = c - P.c0, n = P.c1 - P.c0;
-      i0 = first_item<D, S, TC, GRP>(gg, ucost * k / n);
-      if (k < n - 1) i1 = first_item<D, S, TC, GRP>(gg, ucost * (k + 1) / n);
+      i0 = first_item<D, S, TC, GRP, FS>(gg, ucost * k / n);
+      if (k < n - 1) i1 = first_item<D, S, TC, GRP, FS>(gg, ucost * (k + 1) / n);
     } else if (P.split == 2) {
       // this CTA's slice of unit u (items start EOV into the unit's cost range) and the
       // CTAs [ec0, ec1) sharing the unit; every CTA evaluates the same expressions
       const double us = (double)ustart[u], ue = (double)ustart[u + 1];
-      const double eov = (double)ItemGeo<D, S, TC, GRP>::EOV;
+      const double eov = (double)ItemGeo<D, S, TC, GRP, FS>::EOV;
       const double Td = (double)ustart[a.B * a.H];
       const int Gp = P.G;
       auto Bk = [&](int k) { return Td * k / Gp; };
-      if (P.lo > us) i0 = first_item<D, S, TC, GRP>(gg, P.lo - us - eov);
-      if (P.hi < ue) i1 = first_item<D, S, TC, GRP>(gg, P.hi - us - eov);
+      if (P.lo > us) i0 = first_item<D, S, TC, GRP, FS>(gg, P.lo - us - eov);
+      if (P.hi < ue) i1 = first_item<D, S, TC, GRP, FS>(gg, P.hi - us - eov);
       int k0 = (int)(us * Gp / Td);
       k0 = k0 < 0 ? 0 : (k0 > Gp - 1 ? Gp - 1 : k0);
       while (k0 + 1 < Gp && Bk(k0 + 1) <= us) k0++;
@@ -330,7 +341,7 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
       ec1 = k1 + 1;
     }
     UnitPlan pl;
-    plan_unit<D, S, TC, STAGE, GRP>(gg, i0, i1, pl);
+    plan_unit<D, S, TC, STAGE, GRP, FS>(gg, i0, i1, pl);
     bool published = false;
     const uint8_t *img = a.packed + img_off;
     const __half *kr = a.k_rest + gg.b * a.rs_b + gg.h * a.rs_h;
@@ -346,19 +357,32 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
         mbar_wait_sleep(&empty[slot], (fill & 1) ^ 1, 64);
         if (ts && sg < 64) ts[72 + sg] = clock64();
         uint8_t *dst = ring + (size_t)slot * STAGE;
-        if (p < 4) {
+        if (p < 4 && (p < 3 || FS == 1)) {
           const uint32_t nb = (uint32_t)(f1 - f0) * IG::sz(p);
           WQ_CHECK(f0 >= gg.so[p] && f1 <= gg.so[p + 1] && nb <= (uint32_t)STAGE);
           WQ_CHECK(img_off + gg.cs[p] + (int64_t)(f1 - gg.so[p]) * IG::sz(p) <= a.offs[a.B * a.H]);
           WQ_CHECK(img_off + gg.cs[4] <= a.offs[u + 1]);
           mbar_arrive_expect_tx(&full[slot], nb);
           bulk_g2s_evict_first(dst, img + gg.cs[p] + (int64_t)(f0 - gg.so[p]) * IG::sz(p), nb, &full[slot], pol);
+        } else if (p == 3) {
+          // FP16 sub-items: item f = part (f - io[3]) % FS of window slot so[3] + (f - io[3]) / FS;
+          // its K tiles and V tiles are copied back to back (an (S/FS)-token FP16 record)
+          constexpr uint32_t HB = (uint32_t)(2 * S * D / FS);          // K (or V) bytes of a part
+          mbar_arrive_expect_tx(&full[slot], (uint32_t)(f1 - f0) * 2u * HB);
+          for (int f = f0; f < f1; f++) {
+            const int wi = (f - gg.io[3]) / FS, part = (f - gg.io[3]) - wi * FS;
+            const uint8_t *rec = img + gg.cs[3] + (int64_t)wi * IG::rb(3);
+            WQ_CHECK(gg.so[3] + wi < gg.so[4] && (uint32_t)(f - f0 + 1) * 2u * HB <= (uint32_t)STAGE);
+            uint8_t *di = dst + (size_t)(f - f0) * 2 * HB;
+            bulk_g2s_evict_first(di, rec + (size_t)part * HB, HB, &full[slot], pol);
+            bulk_g2s_evict_first(di + HB, rec + 2 * (size_t)S * D + (size_t)part * HB, HB, &full[slot], pol);
+          }
         } else {
           // rest tiles [f0, f1) = rows [r0, r1): one bulk copy for K, one for V
           // (the rest buffers may be written by the preceding work: wait for it)
           if (a.flags & WQ_DECODE_EARLY_) griddep_wait();
-          const int r0 = 16 * (f0 - gg.nslots);
-          const int r1 = min(gg.rl, 16 * (f1 - gg.nslots));
+          const int r0 = 16 * (f0 - gg.io[4]);
+          const int r1 = min(gg.rl, 16 * (f1 - gg.io[4]));
           const uint32_t nb = (uint32_t)(r1 - r0) * 2u * D;
           WQ_CHECK(r0 >= 0 && r1 <= a.R_max && 2u * (uint32_t)cap * 32u * D <= (uint32_t)STAGE);
           mbar_arrive_expect_tx(&full[slot], 2 * nb);

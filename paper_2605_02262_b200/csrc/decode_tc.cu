@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(NT, 1) k_decode_tc(DecodeArgs a) {
 #pragma unroll
                   for (int i = 0; i < C::KB; i++) {        // all loads first
                     qk[i] = ldsp<uint2>(qs + ((kb0 + i) * 32 + lane) * 8);
-                    if constexpr (BITS < 16) pr[i] = ldsp<uint4>(kp + (q * KT + kb0 + i) * 16);
+                    if constexpr (BITS < 16) pr[i] = ldsp<uint4>(kp + (4 * (kb0 + i) + q) * 16);
                   }
 #pragma unroll
                   for (int i = 0; i < C::KB; i++) {

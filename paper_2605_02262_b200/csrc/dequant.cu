@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256, 8) k_dequant_image(const uint8_t *__restr
     const uint8_t *tb = rec + (isv ? kbytes : 0) + (int64_t)tile * 2 * D * bits;
     // one 16-byte parameter group serves the lane's 4 pairs: K group (q, m) =
     // {mn01, s01, mn89, s89}; V group (tile, q) = {s01, s89, mn01, mn89} (D-1)
-    pq[i] = __ldg(reinterpret_cast<const uint4 *>(isv ? vp + (4 * tile + q) * 8 : kp + (q * (D / 16) + m) * 8));
+    pq[i] = __ldg(reinterpret_cast<const uint4 *>(isv ? vp + (4 * tile + q) * 8 : kp + (4 * m + q) * 8));
     const int w0 = (4 * m) / PPW;
     wa[i] = __ldg(reinterpret_cast<const uint32_t *>(tb + wofs(w0, L)));
     wb[i] = bits == 8 ? __ldg(reinterpret_cast<const uint32_t *>(tb + wofs(w0 + 1, L))) : wa[i];

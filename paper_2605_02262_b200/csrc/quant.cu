@@ -187,7 +187,7 @@ WQ_DEV void quant_k_half(const uint8_t *kbox, float2 *kp, uint8_t *rec, int hf, 
     uint2 pv;
     pv.x = (uint32_t)__half_as_ushort(__low2half(mn2)) | ((uint32_t)__half_as_ushort(__high2half(mn2)) << 16);
     pv.y = (uint32_t)__half_as_ushort(s0) | ((uint32_t)__half_as_ushort(s1) << 16);
-    *reinterpret_cast<uint2 *>(rec + 2 * KBYTES + (q * (D / 16) + m) * 16 + hh * 8) = pv;
+    *reinterpret_cast<uint2 *>(rec + 2 * KBYTES + (4 * m + q) * 16 + hh * 8) = pv;
   }
   __syncwarp();
   // (2) codes: words of fragment lane L = lane whose pairs lie in this channel half

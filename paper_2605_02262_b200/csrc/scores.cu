@@ -41,6 +41,90 @@ __global__ void __launch_bounds__(ST) k_text_pool_q(const __half *__restrict__ q
   for (int c = threadIdx.x; c < D; c += ST) tbar[(int64_t)b * D + c] = pooled[c];
 }
 
+// Per-layer scorer visual side for short head-split rows (D = H d <= 1024): one CTA of
+// 4 warps per (window, request), a WARP per token row -- lane l owns the 16-byte chunks
+// l + 32 i (i < NCW) of every row, the row's sum of squares is a warp-shuffle tree (no
+// block barrier per row), RB rows per warp in flight; the 4 warps' pooled vectors are
+// summed in fixed order through shared memory and dotted with tbar.  Same arithmetic as
+// window_score_body (fp64, zero-norm rows contribute 0), another fixed summation order.
+template <int NCW>
+__global__ void __launch_bounds__(ST) k_window_scores_rows(const __half *__restrict__ vis, int64_t vrs,
+                                                           int64_t vbs, int N, int D, int S,
+                                                           const double *__restrict__ tbar,
+                                                           double *__restrict__ scores, int dh, int64_t hs) {
+  constexpr int RB = 4;
+  extern __shared__ double wpool[];              // [4][D]
+  __shared__ double red[4];
+  const int w = blockIdx.x, b = blockIdx.y, W = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nchunk = D / 8;
+  int coff[NCW];
+#pragma unroll
+  for (int i = 0; i < NCW; i++) {
+    const int c = 8 * (lane + 32 * i);
+    coff[i] = (int)((int64_t)(c / dh) * hs + c % dh);
+  }
+  double pool[NCW][8];
+#pragma unroll
+  for (int i = 0; i < NCW; i++)
+#pragma unroll
+    for (int e = 0; e < 8; e++) pool[i][e] = 0.0;
+  const __half *base = vis + b * vbs + (int64_t)w * S * vrs;
+  for (int r0 = warp * RB; r0 < S; r0 += 4 * RB) {
+    uint4 raw[RB][NCW];
+#pragma unroll
+    for (int r = 0; r < RB; r++)
+#pragma unroll
+      for (int i = 0; i < NCW; i++)
+        raw[r][i] = (r0 + r < S && lane + 32 * i < nchunk)
+                        ? __ldcs(reinterpret_cast<const uint4 *>(base + (int64_t)(r0 + r) * vrs + coff[i]))
+                        : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int r = 0; r < RB; r++) {
+      double ss = 0.0;
+#pragma unroll
+      for (int i = 0; i < NCW; i++) {
+        const __half2 *h = reinterpret_cast<const __half2 *>(&raw[r][i]);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const float2 f = __half22float2(h[e]);
+          ss = fma((double)f.x, (double)f.x, ss);
+          ss = fma((double)f.y, (double)f.y, ss);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const double inv = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+#pragma unroll
+      for (int i = 0; i < NCW; i++) {
+        const __half2 *h = reinterpret_cast<const __half2 *>(&raw[r][i]);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const float2 f = __half22float2(h[e]);
+          pool[i][2 * e] = fma((double)f.x, inv, pool[i][2 * e]);
+          pool[i][2 * e + 1] = fma((double)f.y, inv, pool[i][2 * e + 1]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NCW; i++) {
+    const int k = lane + 32 * i;
+    if (k < nchunk)
+#pragma unroll
+      for (int e = 0; e < 8; e++) wpool[warp * D + 8 * k + e] = pool[i][e];
+  }
+  __syncthreads();
+  double dot[1] = {0.0};
+  const double *tb = tbar + (int64_t)b * D;
+  for (int c = threadIdx.x; c < D; c += ST) {
+    const double v = ((wpool[c] + wpool[D + c]) + wpool[2 * D + c]) + wpool[3 * D + c];
+    dot[0] = fma(v, tb[c], dot[0]);
+  }
+  block_sum<1>(dot, red);
+  if (threadIdx.x == 0) scores[(int64_t)b * W + w] = dot[0] / ((double)S * (double)N);
+}
+
 cudaError_t launch_text_pool_q(const __half *qt, int64_t qsb, int64_t qsh, int64_t qsj, int B, int N, int H,
                                int grp, int d, double *tbar, cudaStream_t st) {
   const size_t smem = (size_t)2 * H * d * sizeof(double);
@@ -67,10 +151,27 @@ cudaError_t launch_window_scores(const __half *vis, int64_t vrs, int64_t vbs, in
   int nc = (D / 8 + ST - 1) / ST;
   dim3 grid(W, B);
   if (dh <= 0) { dh = D; hs = 0; }
-#define WQ_WS(NCV)                                                                                   \
-  case NCV:                                                                                          \
-    if (metric == 1) k_window_scores<NCV, true><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores, dh, hs); \
-    else k_window_scores<NCV, false><<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores, dh, hs);          \
+  if ((int64_t)(D / dh - 1) * hs + dh >= (1LL << 31)) return cudaErrorInvalidValue;
+  const bool split = dh != D;
+  if (split && metric == 0 && D <= 1024 && D % 8 == 0) {
+    // short head-split rows (the per-layer scorer): warp per row
+    const size_t smem = (size_t)4 * D * sizeof(double);
+    const int ncw = (D / 8 + 31) / 32;
+    auto kern = ncw <= 1 ? k_window_scores_rows<1> : ncw <= 2 ? k_window_scores_rows<2>
+                         : k_window_scores_rows<4>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, ST, smem, st>>>(vis, vrs, vbs, N, D, S, tbar, scores, dh, hs);
+    return cudaGetLastError();
+  }
+#define WQ_WS(NCV)                                                                                      \
+  case NCV:                                                                                             \
+    if (split)                                                                                          \
+      (metric == 1 ? k_window_scores<NCV, true, true> : k_window_scores<NCV, false, true>)              \
+          <<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores, dh, hs);                       \
+    else                                                                                                \
+      (metric == 1 ? k_window_scores<NCV, true, false> : k_window_scores<NCV, false, false>)            \
+          <<<grid, ST, 0, st>>>(vis, vrs, vbs, M, N, D, S, tbar, scores, dh, hs);                       \
     break;
   switch (nc) {
     WQ_WS(1) WQ_WS(2) WQ_WS(3) WQ_WS(4)

@@ -77,6 +77,19 @@ int main(void) {
       wqo_code_pos(t & 1, d, 4, t, c, &bo, &bit);
     }
   (void)wqo_param_pos(1, d, 3, 1);
+  /* paper-literal group granularity (gran 1) and the per-layer scorer */
+  int64_t *offs_g = malloc(sizeof(int64_t) * (B * H + 1));
+  wqo_layer_layout_g(&g, seg, offs_g, 1);
+  uint8_t *packed_g = calloc((size_t)offs_g[B * H] + 16, 1);
+  wqo_reorder_quantize_pack_g(k, v, strides, 0, &g, perm, W, seg, offs_g, packed_g, 1);
+  wqo_decode_attention_g(q, packed_g, offs_g, seg, perm, W, &g, kr, vr, rs, rest_len, 0.125f, out, part, 1);
+  wqo_dequant_record_g(packed_g, 4, d, S, kh, vh, 1);
+  if (wqo_record_bytes_g(2, d, S, 1) != (int64_t)S * d * 2 / 4 + 16) return 6;
+  uint16_t qt[B * Hq * N * d];
+  for (int i = 0; i < B * Hq * N * d; i++) qt[i] = h16(urand() - 0.5);
+  int64_t qs[3] = {(int64_t)Hq * N * d, (int64_t)N * d, d};
+  wqo_window_scores_layer(k, strides, 0, qt, qs, B, H, Hq, d, M, N, S, scores);
+  free(offs_g); free(packed_g);
   printf("oracle_asan: ok %.6f\n", out[0]);
   free(vis); free(txt); free(scores); free(bits); free(rank); free(perm); free(seg); free(offs);
   free(k); free(v); free(packed); free(out); free(part); free(offs16); free(img16);

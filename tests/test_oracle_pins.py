@@ -640,10 +640,10 @@ def test_param_layout_hand_derived(orc):
     """D-1 params: K group (q, m) = {mn(c0), mn(c0+1), s(c0), s(c0+1), mn(c0+8), mn(c0+9),
     s(c0+8), s(c0+9)} with c0 = 16m + 2q; V group (i, q) = {s(t0), s(t0+1), s(t0+8), s(t0+9),
     mn(t0), ...}.  K c=9 (d=64): m=0, q=0, second half (c0+8), e=1 -> mn at half 5, s at half 7.
-    K c=34 (d=128): m=2, q=1, first half, e=0 -> group 1*8+2=10 -> s at byte 160+4.
+    K c=34 (d=128): m=2, q=1, first half, e=0 -> group 4*2+1=9 -> s at byte 144+4.
     V t=9: group 0, second half, e=1 -> s at half 3, mn at half 7."""
     assert orc.param_pos(0, 64, 9, 1) == 10 and orc.param_pos(0, 64, 9, 0) == 14
-    assert orc.param_pos(0, 128, 34, 0) == 164 and orc.param_pos(0, 128, 34, 1) == 160
+    assert orc.param_pos(0, 128, 34, 0) == 148 and orc.param_pos(0, 128, 34, 1) == 144
     assert orc.param_pos(1, 64, 9, 0) == 6 and orc.param_pos(1, 64, 9, 1) == 14
     # every param slot used exactly once (K: 2 x d halves in 4d bytes)
     used = sorted(orc.param_pos(0, 128, c, m) for c in range(128) for m in (0, 1))

@@ -1,7 +1,9 @@
 """C1-sized run of every libwq device call, for the checked build (tests/test_gpu_checked.py):
 scores (cosine, Pearson), rank + assign (budget and vote), layout, quantize, decode
 (flags 0, then a PDL-chained WQ_DECODE_EARLY decode, and partials), merge, shard,
-the unfused (T9) and unreordered (T8) baselines and the two-rank fused-merge emulation.
+the unfused (T9) and unreordered (T8) baselines, the group granularity (quantize +
+WQ_DECODE_GROUP decode), the per-layer scorer, the fused search and the two-rank
+fused-merge emulation.
 Exits 0 when every call returned WQ_OK; under WQ_VARIANT=checked (-DWQ_CHECKS=1) every
 device-side bounds check of the path ran."""
 import math
@@ -40,6 +42,18 @@ def main():
     wq.wq_decode_attention(q, packed, offs, seg[0], g, kr, vr, rest_len, sm, out=out, workspace=ws,
                            flags=wq.WQ_DECODE_EARLY)
     wq.wq_merge_partials(torch.stack([part, part]), g)
+    # paper-literal group granularity: layout, quantize, decode (plain and PDL-chained)
+    offs_g = wq.wq_layer_layout(g, seg[0], gran=wq.WQ_GRAN_GROUP)
+    packed_g = torch.zeros(int(offs_g[-1].item()) + 16, dtype=torch.uint8, device=dev)
+    wq.wq_reorder_quantize_pack(K, V, 0, g, perm[0], seg[0], offs_g, packed_g, gran=wq.WQ_GRAN_GROUP)
+    for fl in (wq.WQ_DECODE_GROUP, wq.WQ_DECODE_GROUP | wq.WQ_DECODE_EARLY):
+        wq.wq_decode_attention(q, packed_g, offs_g, seg[0], g, kr, vr, rest_len, sm, out=out, partial=part,
+                               workspace=ws, flags=fl)
+    # per-layer K/Q scorer and the fused search
+    qt = synth.text_queries(cfg.B, m.Hq, cfg.n_text, m.d, cfg.seed, 0, dev)
+    wq.wq_window_scores_layer(K, 0, qt, cfg.M, cfg.S)
+    wq.wq_search(vis, txt, thr, 2, g, wq.AssignOpts(4.5, 1, 1))
+    wq.wq_search(vis, txt, thr, 2, g, wq.AssignOpts(0.0, 1, 0), metric=wq.WQ_SIM_PEARSON)
     pr, sr = wq.wq_shard_slots(perm[0], seg[0], 2, 1)
     seg16, offs16 = wq.wq_dequant_layout(g, seg[0])
     img16 = torch.zeros(int(offs16[-1].item()) + 16, dtype=torch.uint8, device=dev)
