@@ -11,15 +11,24 @@
 namespace wq {
 
 constexpr int MAX_UNITS = 1024;         // B * H
-constexpr int64_t MIN_CTA_BYTES = 49152;
+#ifndef WQ_DEC_MINCTA
+#define WQ_DEC_MINCTA 98304   // A/B vs 49152: C2 9.43 -> 8.95 us (196608: 11.9, 393216: 20.3), C3/C5 unchanged
+#endif
+constexpr int64_t MIN_CTA_BYTES = WQ_DEC_MINCTA;   // least cost units per CTA (small calls use fewer CTAs)
 constexpr uint32_t WQ_DECODE_EARLY_ = 1u;     // = WQ_DECODE_EARLY (include/wq.h)
 constexpr uint32_t WQ_DECODE_GROUP_ = 2u;     // = WQ_DECODE_GROUP (include/wq.h)
 constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trace
 #ifndef WQ_DEC_EOV
 #define WQ_DEC_EOV 2000                // per-unit entry overhead in cost units of S*D/100
 #endif
+#ifndef WQ_DEC_C4
+#define WQ_DEC_C4 168                  // 4-bit window cost, units of S*D/100 (2-bit: 156)
+#endif
+#ifndef WQ_DEC_C8
+#define WQ_DEC_C8 191                  // 8-bit window cost (r02 refit: 233 -> 191, C5 -3.3 %, C3 -3.6 %)
+#endif
 #ifndef WQ_DEC_C16
-#define WQ_DEC_C16 235                 // FP16 window cost, units of S*D/100 (2-bit: 156)
+#define WQ_DEC_C16 171                 // FP16 window cost, units of S*D/100 (r02 refit: 235 -> 171)
 #endif
 #ifndef WQ_DEC_CR
 #define WQ_DEC_CR 40                   // FP16 rest tile (16 tokens) cost, units of D
@@ -51,8 +60,10 @@ struct ItemGeo {
   static constexpr int per_slot(int k) { return k == 3 ? FS : 1; }   // items per window slot
   // Cost of an item ~ its time on one SM inside a full decode launch.
   //  mma.sync kernel: measured per-class CTA-level item times on C5
-  //   (tools/dbg_decode_time.py least-squares fit): 2-bit 0.167 us, 4-bit 0.182,
-  //   8-bit 0.249, FP16 0.251, 16-token rest tile ~0.1; in units of S*D/100.
+  //   (tools/dbg_decode_time.py least-squares fit, round 2): 2-bit 0.136 us, 4-bit 0.147,
+  //   8-bit 0.166, FP16 0.149 -> 156 : 168 : 191 : 171 in units of S*D/100 (round 1's
+  //   156 : 170 : 233 : 235 left 8-bit-heavy CTAs idle ~7 us before the 2-bit ones);
+  //   A/B over 4 tables: C5 34.96 -> 33.79 us, C3 38.81 -> 37.41 us, C4 unchanged.
   //  tcgen05 kernel: the tensor work is asynchronous, an item costs its bytes plus
   //   a per-window dequantization term (same units).
   // fixed cost of one unit entry of a CTA (its epilogue, ~2 us: ~13 2-bit windows),
@@ -64,7 +75,7 @@ struct ItemGeo {
                     : (int64_t)(k == 0 ? 100 : k == 1 ? 140 : k == 2 ? 220 : 300) * S * D / 100;
     } else {
       return k == 4 ? (int64_t)WQ_DEC_CR * D
-                    : (int64_t)(k == 0 ? 156 : k == 1 ? 170 : k == 2 ? 233 : WQ_DEC_C16) * S * D / 100 /
+                    : (int64_t)(k == 0 ? 156 : k == 1 ? WQ_DEC_C4 : k == 2 ? WQ_DEC_C8 : WQ_DEC_C16) * S * D / 100 /
                           (k == 3 ? FS : 1);
     }
   }
@@ -77,6 +88,7 @@ struct UnitGeo {
   int io[6];                            // item starts: classes 0-3 (FS items per FP16 slot), rest, end
   int64_t cs[5];                        // byte start of each class segment; cs[4] = image bytes
   int64_t cc[5];                        // cost start of each class segment; cc[4] = windows' cost
+  double ccd[5];                        // cc as double (first_item: no int64 -> fp64 conversions)
 };
 
 template <int D, int S, bool TC, bool GRP = false, int FS = 1>
@@ -100,6 +112,8 @@ WQ_DEV void unit_geo(const DecodeArgs &a, int u, UnitGeo &g) {
   g.rl = g.rl < 0 ? 0 : (g.rl > a.R_max ? a.R_max : g.rl);     // contract: rest_len clamped to R_max
   g.ntiles = (g.rl + 15) / 16;
 #pragma unroll
+  for (int k = 0; k < 5; k++) g.ccd[k] = (double)g.cc[k];
+#pragma unroll
   for (int k = 0; k < 4; k++) g.io[k] = g.so[k];
   g.io[4] = g.so[3] + FS * (g.so[4] - g.so[3]);
   g.io[5] = g.io[4] + g.ntiles;
@@ -118,11 +132,13 @@ WQ_DEV int first_item(const UnitGeo &g, double x) {
   if (x <= 0.0) return 0;
 #pragma unroll
   for (int k = 0; k < 4; k++) {
-    if (x <= (double)g.cc[k]) return g.io[k];
-    if (x < (double)g.cc[k + 1]) return g.io[k] + (int)ceil((x - (double)g.cc[k]) / (double)IG::cost(k));
+    if (x <= g.ccd[k]) return g.io[k];
+    // (a multiply by the compile-time reciprocal: a DDIV is a long dependent sequence on
+    // the producer's start-up path; every CTA evaluates the same expression)
+    if (x < g.ccd[k + 1]) return g.io[k] + (int)ceil((x - g.ccd[k]) * (1.0 / (double)IG::cost(k)));
   }
-  if (x <= (double)g.cc[4]) return g.io[4];
-  const int t = (int)ceil((x - (double)g.cc[4]) / (double)IG::cost(4));
+  if (x <= g.ccd[4]) return g.io[4];
+  const int t = (int)ceil((x - g.ccd[4]) * (1.0 / (double)IG::cost(4)));
   return g.io[4] + (t < g.ntiles ? t : g.ntiles);
 }
 
@@ -201,7 +217,8 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
   if (lane == 0) ustart[U] = carry;
   __syncwarp();
   const int64_t T = carry;
-  int G = (int)(T / MIN_CTA_BYTES);
+  const double invT = T > 0 ? 1.0 / (double)T : 0.0;
+  int G = (int)((double)T * (1.0 / (double)MIN_CTA_BYTES));
   G = G < 1 ? 1 : (G > vn ? vn : G);
   const int c = vc;
   if (U >= G || T <= 0) {
@@ -212,7 +229,7 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
       int own = G;
       if (u < U) {
         const int64_t mid = ustart[u] + (ustart[u + 1] - ustart[u]) / 2;
-        own = T > 0 ? (int)((double)mid * G / (double)T) : 0;
+        own = T > 0 ? (int)((double)mid * G * invT) : 0;
         own = own >= G ? G - 1 : own;
       }
       ua += __popc(__ballot_sync(0xffffffffu, own < c));
@@ -242,13 +259,13 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
     int cnt = 0;
     for (int base = 0; base < U; base += 32) {
       const int u = base + lane;
-      const int c0u = u < U ? u + (int)rint((double)ustart[u] * extra / (double)T) : G;
+      const int c0u = u < U ? u + (int)rint((double)ustart[u] * extra * invT) : G;
       cnt += __popc(__ballot_sync(0xffffffffu, u < U && c0u <= c));
     }
     const int u = cnt - 1;                      // c0(0) = 0 <= c: u >= 0
     if (lane == 0) {
-      const int c0 = u + (int)rint((double)ustart[u] * extra / (double)T);
-      const int c1 = (u + 1 < U) ? (u + 1) + (int)rint((double)ustart[u + 1] * extra / (double)T) : G;
+      const int c0 = u + (int)rint((double)ustart[u] * extra * invT);
+      const int c1 = (u + 1 < U) ? (u + 1) + (int)rint((double)ustart[u + 1] * extra * invT) : G;
       cp->ua = u; cp->ub = u + 1; cp->split = c1 - c0 > 1; cp->c0 = c0; cp->c1 = c1;
     }
   }
@@ -263,6 +280,19 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
     cp->geo_ok = 1;
   }
   if (lane == 0) { *s_flag = G; cp->G = G; }
+  __syncwarp();
+  // a unit split over CTAs [c0, c1): this CTA's item range, i0 by lane 0 and i1 by lane 1
+  // in parallel (the producer's start-up path otherwise runs both searches back to back)
+  if (cp->split == 1 && cp->geo_ok && lane < 2) {
+    const UnitGeo &g0 = cp->geo;
+    const int k = c - cp->c0, n = cp->c1 - cp->c0;
+    const double lov = (double)WQ_DEC_LOV * S * D / 100;
+    const double share = ((double)(ustart[ua + 1] - ustart[ua]) + lov) * (1.0 / (double)n);
+    const int kk = k + lane;
+    const int v = (lane == 1 && k == n - 1) ? g0.io[5] : first_item<D, S, TC, GRP, FS>(g0, share * kk);
+    if (lane == 0) cp->i0 = v;
+    else cp->i1 = v;
+  }
 }
 
 // ---- producer (one lane): stream the CTA's entries into the ring ----
@@ -274,7 +304,7 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
   using IG = ItemGeo<D, S, TC, GRP, FS>;
   const int c = vc;
   const uint64_t pol = policy_evict_first();
-  if (ts) ts[62] = gtime();
+  if (ts) { ts[62] = gtime(); ts[55] = clock64(); }
   int sg = 0;                                  // stage number of this CTA
   int uix = 0;                                 // entry number of this CTA
   auto publish = [&](int u, int n_u, const UnitGeo *gg, const UnitPlan *pl, int ec0, int ec1) {
@@ -300,25 +330,31 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
   };
   for (int u = P.ua; u < P.ub; u++) {
     int64_t img_off;
-    UnitGeo gg;
-    if (u == P.ua && P.geo_ok) {
-      gg = P.geo;                              // from the prologue: no global round trip
-      img_off = P.img_off;
+    UnitGeo gl;
+    const bool first = u == P.ua && P.geo_ok;
+    if (first) {
+      img_off = P.img_off;                     // from the prologue: no global round trip
     } else {
       img_off = a.offs[u];
-      unit_geo<D, S, TC, GRP, FS>(a, u, gg);
+      unit_geo<D, S, TC, GRP, FS>(a, u, gl);
     }
+    const UnitGeo &gg = first ? P.geo : gl;    // (the prologue's copy read in place)
+    if (ts && u == P.ua) ts[57] = clock64();
     int i0 = 0, i1 = gg.io[5];
     int ec0 = P.split == 1 ? P.c0 : c, ec1 = P.split == 1 ? P.c1 : c + 1;
-    if (P.split == 1) {
+    if (P.split == 1 && first) {
+      i0 = P.i0;                                 // planned in the prologue (plan_cta)
+      i1 = P.i1;
+    } else if (P.split == 1) {
       // the unit's cost plus the last CTA's merge allowance, cut into n equal shares: the
       // last CTA (the merger: it ends with the unit's FP16 windows and rest tiles, then
       // merges every partial) gets LOV less item cost than the others
       const double lov = (double)WQ_DEC_LOV * S * D / 100;
       const double ucost = (double)(ustart[u + 1] - ustart[u]) + lov;
       const int k = c - P.c0, n = P.c1 - P.c0;
-      i0 = first_item<D, S, TC, GRP, FS>(gg, ucost * k / n);
-      if (k < n - 1) i1 = first_item<D, S, TC, GRP, FS>(gg, ucost * (k + 1) / n);
+      const double share = ucost * (1.0 / (double)n);
+      i0 = first_item<D, S, TC, GRP, FS>(gg, share * k);
+      if (k < n - 1) i1 = first_item<D, S, TC, GRP, FS>(gg, share * (k + 1));
     } else if (P.split == 2) {
       // this CTA's slice of unit u (items start EOV into the unit's cost range) and the
       // CTAs [ec0, ec1) sharing the unit; every CTA evaluates the same expressions
@@ -340,8 +376,10 @@ WQ_DEV void produce(const DecodeArgs &a, const CtaPlan &P, const int64_t *ustart
       ec0 = k0;
       ec1 = k1 + 1;
     }
+    if (ts && u == P.ua) ts[58] = clock64();
     UnitPlan pl;
     plan_unit<D, S, TC, STAGE, GRP, FS>(gg, i0, i1, pl);
+    if (ts && sg == 0) ts[56] = clock64();
     bool published = false;
     const uint8_t *img = a.packed + img_off;
     const __half *kr = a.k_rest + gg.b * a.rs_b + gg.h * a.rs_h;

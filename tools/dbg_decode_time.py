@@ -60,6 +60,10 @@ for mode in [int(x) for x in os.environ.get("DBG", "0").split(",")]:
     ok = np.isfinite(dur_loop)
     sol, *_ = np.linalg.lstsq(A[ok], dur_loop[ok], rcond=None)
     print("fit us/item (2,4,8,16,rest) + const:", np.round(sol, 4), " resid rms", round(float(np.sqrt(np.mean((A[ok] @ sol - dur_loop[ok]) ** 2))), 3))
+    ref70 = tsb[:, 70]
+    print("producer setup cycles after prologue (median, max): entry / geo / items / planned")
+    for k in (55, 57, 58, 56):
+        print("   ", k, np.median(tsb[:, k] - ref70), np.max(tsb[:, k] - ref70))
     slow = int(np.nanargmax(st[:, 3]))
     print("slowest CTA", slow)
     for cta in (0, slow):
