@@ -145,10 +145,14 @@ WQ_DEV void softmax_tiles(const float (&s)[NT][4], float scale2, WarpState &st, 
 // logit = s_K * sum_c code*q_c + mn_K * sum_c q_c: the K side runs on the raw q (no hi/lo
 // split, no zero-point MMA; qsum = the lane's heads' sum_c q_c, per unit), and the V side
 // takes P' = p * s_V.
-template <int D, int S, int BITS, bool GRP = false>
+// S tokens of a record of SR tokens (SR = S: the whole record): part `part` = tokens
+// [part*S, part*S + S) read in place -- its K and V code tiles, the record's K parameters,
+// the part's V parameters (large windows are consumed as 32-token parts by several warps).
+template <int D, int S, int BITS, bool GRP = false, int SR = S>
 WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
                       WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane,
-                      float2 qsum = make_float2(0.f, 0.f)) {
+                      float2 qsum = make_float2(0.f, 0.f), int part = 0) {
+  constexpr int KBR = SR * D * BITS / 8;                 // K code bytes of the record
   if constexpr (GRP && BITS < 16) {
     constexpr int NTT = S / 16;
     constexpr int CH = NTT < 2 ? 1 : 2;
@@ -156,7 +160,8 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
     constexpr int WPL = D * BITS / 64;
     constexpr int TILE = 2 * D * BITS;
     constexpr int KB = S * D * BITS / 8;
-    const uint2 pg = lds64(rec + 2 * KB);                // {mn_K, s_K, mn_V, s_V}
+    const uint8_t *kc = rec + part * KB, *vc = rec + KBR + part * KB;
+    const uint2 pg = lds64(rec + 2 * KBR);               // {mn_K, s_K, mn_V, s_V}
     const float mnK = __half2float(__ushort_as_half((unsigned short)pg.x));
     const float sK = __half2float(__ushort_as_half((unsigned short)(pg.x >> 16)));
     const float mnV = __half2float(__ushort_as_half((unsigned short)pg.y));
@@ -167,7 +172,7 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
     for (int c0 = 0; c0 < NTT; c0 += CH) {
       uint32_t wk[CH][WPL];
 #pragma unroll
-      for (int t = 0; t < CH; t++) load_chunk<D, BITS>(wk[t], rec + (c0 + t) * TILE, lane);
+      for (int t = 0; t < CH; t++) load_chunk<D, BITS>(wk[t], kc + (c0 + t) * TILE, lane);
       float ah[CH][4], al[CH][4];
 #pragma unroll
       for (int t = 0; t < CH; t++)
@@ -199,7 +204,7 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
         uint32_t pb[2];
         ldsm_x2_t(pb, scratch + (16 * t + (lane & 15)) * 16);
         uint32_t wv[WPL];
-        load_chunk<D, BITS>(wv, rec + KB + (c0 + t) * TILE, lane);
+        load_chunk<D, BITS>(wv, vc + (c0 + t) * TILE, lane);
         tile_pv<D, BITS>(wv, pb[0], pb[1], o);
       }
       __syncwarp();
@@ -211,9 +216,9 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
   constexpr int KT = D / 16;
   constexpr int WPL = D * BITS / 64;
   constexpr int TILE = 2 * D * BITS;          // bytes of one 16-token code tile
-  const uint8_t *kcodes = rec;
-  const uint8_t *vcodes = rec + S * D * BITS / 8;
-  const uint8_t *kp = rec + 2 * (S * D * BITS / 8);
+  const uint8_t *kcodes = rec + part * (S * D * BITS / 8);
+  const uint8_t *vcodes = rec + KBR + part * (S * D * BITS / 8);
+  const uint8_t *kp = rec + 2 * KBR;
   const int g = lane >> 2, q = lane & 3;
   float b0[4] = {0.f, 0.f, 0.f, 0.f}, b1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -274,7 +279,7 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
       for (int i = 0; i < 4; i++) sc[t][i] = (ah[t][i] + al[t][i]) + (b0[i & 1] + b1[i & 1]);
     float vs[CH][2], vm[CH][2];
     if constexpr (BITS < 16) {
-      const uint8_t *vp = kp + 4 * D;
+      const uint8_t *vp = kp + 4 * D + part * 4 * S;
 #pragma unroll
       for (int t = 0; t < CH; t++) {
         // group (tile, g/2): {s(t0),s(t0+1)}, {s(t0+8),s(t0+9)}, {mn..}, {mn..}; token g = t0 + (g&1)
@@ -434,6 +439,10 @@ WQ_DEV void do_rest(const uint8_t *Kb, const uint8_t *Vb, int ntok, const uint8_
 // -------------------------------------------------------------------------------------
 // the kernel
 // -------------------------------------------------------------------------------------
+#ifndef WQ_DEC_SUB
+#define WQ_DEC_SUB 32                    // records of more tokens are consumed as parts of this many (0: off;
+                                         // C4 S=128 185.4 -> 127.8 us, S=64 133.8 -> 127.9)
+#endif
 // FP16 items per window in reordered mode: 2 when a 64 KB record would leave a 2-stage ring
 template <int D, int S>
 constexpr int fsplit() { return 4 * S * D >= 2 * WQ_DEC_STAGE ? 2 : 1; }
@@ -670,7 +679,7 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
 
   // ---- prologue (warp 0): unit cost prefix, then this CTA's share ----
   CtaPlan *cp = reinterpret_cast<CtaPlan *>(sm + SM::plan_off);
-  if (warp == 0) plan_cta<D, S, false, (!UR && WQ_DEC_STREAM), GRP, FS>(a, ustart, cp, s_flag, lane, vc, vn);
+  if (warp == 0) plan_cta<D, S, false, (UR ? 0 : WQ_DEC_STREAM), GRP, FS>(a, ustart, cp, s_flag, lane, vc, vn);
   if (tid == 32) {
     for (int s = 0; s < NST; s++) {
       mbar_init(&full[s], 1);
@@ -804,10 +813,16 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
       // 2-bit stages (S <= 32) are consumed in PAIRS of windows (do_window2): a stage of n
       // records is ceil(n/2) work items, handed out round robin like single items
       constexpr bool PAIRS = WQ_DEC_PAIR && S <= 32 && !GRP;
+      // records of more than WQ_DEC_SUB tokens are consumed as WQ_DEC_SUB-token parts, each
+      // part one work item (a record of n parts keeps n warps busy)
+      constexpr int SR16 = S / FS;                 // tokens of an FP16 item
+      constexpr int SQ = S > WQ_DEC_SUB && WQ_DEC_SUB > 0 ? WQ_DEC_SUB : S;
+      constexpr int SF = SR16 > WQ_DEC_SUB && WQ_DEC_SUB > 0 ? WQ_DEC_SUB : SR16;
+      const int np = p == 4 ? 1 : (p == 3 ? SR16 / SF : S / SQ);
       for (int t = 0; t < nst; t++, sg++) {
         const int slot = sg % NST;
         const int nrec = min(cap, len - t * cap);
-        const int n = (PAIRS && p == 0) ? (nrec + 1) / 2 : nrec;
+        const int n = (PAIRS && p == 0) ? (nrec + 1) / 2 : nrec * np;
         const uint64_t t0 = ts ? clock64() : 0;
         mbar_wait(&full[slot], (uint32_t)(sg / NST) & 1u);
         const uint64_t t1 = ts ? clock64() : 0;
@@ -815,22 +830,24 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
         const uint8_t *sbase = ring + (size_t)slot * STAGE;
         for (; nxt < kbase + n; nxt += NCW) {
           const int k = nxt - kbase;
-          WQ_CHECK(k < n && (k + 1) * sz <= STAGE);
-          const uint8_t *rec = sbase + (size_t)k * sz;
+          const int kr = np > 1 ? k / np : k, part = np > 1 ? k - kr * np : 0;
+          WQ_CHECK(k < n && (kr + 1) * sz <= STAGE);
+          const uint8_t *rec = sbase + (size_t)kr * sz;
           if (p == 0) {
             if constexpr (PAIRS) {
               const uint8_t *r0 = sbase + (size_t)(2 * k) * sz;
               if (2 * k + 1 < nrec) do_window2<D, S, 2>(r0, r0 + sz, qs, a.scale_log2, st, o, scratch, lane);
               else do_window<D, S, 2>(r0, qs, a.scale_log2, st, o, scratch, lane);
             } else {
-              do_window<D, S, 2, GRP>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum);
+              do_window<D, SQ, 2, GRP, S>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum, part);
             }
           } else if (p == 1) {
-            do_window<D, S, 4, GRP>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum);
+            do_window<D, SQ, 4, GRP, S>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum, part);
           } else if (p == 2) {
-            do_window<D, S, 8, GRP>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum);
+            do_window<D, SQ, 8, GRP, S>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum, part);
           } else if (p == 3) {
-            do_window<D, S / FS, 16>(rec, qs, a.scale_log2, st, o, scratch, lane);   // (a part of) an FP16 window
+            do_window<D, SF, 16, false, SR16>(rec, qs, a.scale_log2, st, o, scratch, lane, make_float2(0.f, 0.f),
+                                              part);
           } else {
             const int ii = lo + t * cap + k;
             do_rest<D>(sbase + (size_t)k * 32 * D, sbase + (size_t)(cap + k) * 32 * D, min(16, rl - 16 * (ii - nslots)),

@@ -37,7 +37,10 @@ constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trac
 #define WQ_DEC_LOV 0                   // merge allowance of a split unit's last CTA, units of S*D/100
 #endif
 #ifndef WQ_DEC_STREAM
-#define WQ_DEC_STREAM 0                // 1: cost-stream split when units < CTAs (measured slower)
+#define WQ_DEC_STREAM 2                // cost-stream split: bit 0 when units < CTAs (measured slower,
+                                       // DESIGN §5), bit 1 when units >= CTAs (C4, 256 units on 148
+                                       // CTAs: whole units left 1.73 -> 2 units of makespan; C4 S=32
+                                       // 121.6 -> 112.2 us, S=16 139.1 -> 127.0, S=128 127.8 -> 119.0)
 #endif
 
 // Compile-time item sizes and costs of a (D, S) instantiation.  Work is partitioned
@@ -191,7 +194,7 @@ struct CtaPlan {
 // the same cost; a unit-aligned split rounds each unit to a whole number of CTAs.
 // vc / vn: this CTA's index and the CTA count of the grid it plans over (blockIdx.x /
 // gridDim.x, or a virtual rank's share of one grid in the fused-merge emulation).
-template <int D, int S, bool TC, bool STREAM = false, bool GRP = false, int FS = 1>
+template <int D, int S, bool TC, int STREAM = 0, bool GRP = false, int FS = 1>
 WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_flag, int lane, int vc, int vn) {
   const int U = a.B * a.H;
   int64_t carry = 0;
@@ -221,7 +224,7 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
   int G = (int)((double)T * (1.0 / (double)MIN_CTA_BYTES));
   G = G < 1 ? 1 : (G > vn ? vn : G);
   const int c = vc;
-  if (U >= G || T <= 0) {
+  if ((U >= G && !(STREAM & 2)) || T <= 0) {
     // whole units to the CTA owning their cost midpoint: a contiguous unit range
     int ua = 0, ub = 0;
     for (int base = 0; base < U; base += 32) {
@@ -236,7 +239,7 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
       ub += __popc(__ballot_sync(0xffffffffu, own <= c));
     }
     if (lane == 0) { cp->ua = ua; cp->ub = ub; cp->split = 0; cp->c0 = c; cp->c1 = c + 1; }
-  } else if (STREAM) {
+  } else if (STREAM & (U >= G ? 2 : 1)) {
     const double Td = (double)T;
     const double lo = Td * c / G, hi = Td * (c + 1) / G;
     int ua = 0, ub = 0;

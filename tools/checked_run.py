@@ -49,6 +49,24 @@ def main():
     for fl in (wq.WQ_DECODE_GROUP, wq.WQ_DECODE_GROUP | wq.WQ_DECODE_EARLY):
         wq.wq_decode_attention(q, packed_g, offs_g, seg[0], g, kr, vr, rest_len, sm, out=out, partial=part,
                                workspace=ws, flags=fl)
+    # more (request, head) units than SMs (the cost-stream split of whole units) and S = 128
+    # windows consumed as 32-token parts, FP16 windows as two 64-token items
+    for S_ in (64, 128):
+        Bn, Hn, Mn = 40, 4, 5 * S_ + 7
+        gb = wq.geom(Bn, Hn, 7 * Hn, 128, Mn, S_, (2, 4, 8, 16))
+        Kb = torch.randn((Bn, Hn, Mn, 128), device=dev).half()
+        Vb = torch.randn((Bn, Hn, Mn, 128), device=dev).half()
+        wb = Mn // S_
+        bits_b = torch.tensor([[2, 4, 8, 16, 2][:wb] for _ in range(Bn)], dtype=torch.int32)
+        perm_b = torch.argsort(bits_b * 8 + torch.arange(wb), dim=1).to(torch.int32).to(dev)
+        seg_b = torch.tensor([[0, 2, 3, 4, 5] for _ in range(Bn)], dtype=torch.int32, device=dev)
+        ob = wq.wq_layer_layout(gb, seg_b)
+        pb = torch.zeros(int(ob[-1].item()) + 16, dtype=torch.uint8, device=dev)
+        wq.wq_reorder_quantize_pack(Kb, Vb, 0, gb, perm_b, seg_b, ob, pb)
+        krb = torch.randn((Bn, Hn, 21, 128), device=dev).half()
+        rlb = torch.full((Bn,), 19, dtype=torch.int32, device=dev)
+        qb = torch.randn((Bn, 7 * Hn, 128), device=dev).half()
+        wq.wq_decode_attention(qb, pb, ob, seg_b, gb, krb, krb, rlb, 0.088, out=torch.empty_like(qb))
     # per-layer K/Q scorer and the fused search
     qt = synth.text_queries(cfg.B, m.Hq, cfg.n_text, m.d, cfg.seed, 0, dev)
     wq.wq_window_scores_layer(K, 0, qt, cfg.M, cfg.S)

@@ -6,7 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2605_02262_b200 import configs, synth, wq
 import oracle
-cfg = configs.CONFIGS[os.environ.get("CFG", "C5")]; m = cfg.model
+_c = os.environ.get("CFG", "C5")
+cfg = configs.CONFIGS[_c] if _c in configs.CONFIGS else configs.c4(int(_c[3:])); m = cfg.model
 dev = "cuda"
 vis, txt = synth.embeddings(cfg.B, cfg.M, cfg.n_text, m.D, cfg.S, cfg.seed, dev)
 g = wq.geom(cfg.B, m.H, m.Hq, m.d, cfg.M, cfg.S, cfg.widths)
