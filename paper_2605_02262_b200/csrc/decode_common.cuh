@@ -36,6 +36,11 @@ constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trac
 #ifndef WQ_DEC_LOV
 #define WQ_DEC_LOV 0                   // merge allowance of a split unit's last CTA, units of S*D/100
 #endif
+#ifndef WQ_DEC_SGAIN
+#define WQ_DEC_SGAIN 8                 // least predicted makespan gain (%) for the stream split when units < CTAs
+                                       // (with bit 0 of WQ_DEC_STREAM: A/B C3 37.8 -> 37.2 us, C5 33.75 -> 33.9,
+                                       // C1 10.8 -> 11.1: left off)
+#endif
 #ifndef WQ_DEC_STREAM
 #define WQ_DEC_STREAM 2                // cost-stream split: bit 0 when units < CTAs (measured slower,
                                        // DESIGN §5), bit 1 when units >= CTAs (C4, 256 units on 148
@@ -224,7 +229,28 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
   int G = (int)((double)T * (1.0 / (double)MIN_CTA_BYTES));
   G = G < 1 ? 1 : (G > vn ? vn : G);
   const int c = vc;
-  if ((U >= G && !(STREAM & 2)) || T <= 0) {
+  bool stream = (STREAM & (U >= G ? 2 : 1)) != 0;
+  if (stream && U < G && T > 0) {
+    // units < CTAs: the unit-aligned split gives unit u n_u = c0(u+1) - c0(u) CTAs (below);
+    // stream only if its makespan T/G beats max_u cost_u/n_u by the margin WQ_DEC_SGAIN %
+    // (a CTA spanning two units runs two epilogues: C5, 9-10 CTAs per unit, stays aligned;
+    // C3, 2-3 CTAs per unit, streams)
+    const int64_t extra = G - U;
+    double mk = 0.0;
+    for (int base = 0; base < U; base += 32) {
+      const int u = base + lane;
+      if (u < U) {
+        const int c0u = u + (int)rint((double)ustart[u] * extra * invT);
+        const int c1u = (u + 1 < U) ? (u + 1) + (int)rint((double)ustart[u + 1] * extra * invT) : G;
+        const double cu = (double)(ustart[u + 1] - ustart[u]);
+        mk = fmax(mk, cu / (double)(c1u > c0u ? c1u - c0u : 1));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mk = fmax(mk, __shfl_xor_sync(0xffffffffu, mk, o));
+    stream = (double)T * (1.0 + WQ_DEC_SGAIN / 100.0) < mk * (double)G;
+  }
+  if ((U >= G && !stream) || T <= 0) {
     // whole units to the CTA owning their cost midpoint: a contiguous unit range
     int ua = 0, ub = 0;
     for (int base = 0; base < U; base += 32) {
@@ -239,7 +265,7 @@ WQ_DEV void plan_cta(const DecodeArgs &a, int64_t *ustart, CtaPlan *cp, int *s_f
       ub += __popc(__ballot_sync(0xffffffffu, own <= c));
     }
     if (lane == 0) { cp->ua = ua; cp->ub = ub; cp->split = 0; cp->c0 = c; cp->c1 = c + 1; }
-  } else if (STREAM & (U >= G ? 2 : 1)) {
+  } else if (stream) {
     const double Td = (double)T;
     const double lo = Td * c / G, hi = Td * (c + 1) / G;
     int ua = 0, ub = 0;
