@@ -167,8 +167,9 @@ wq_status wq_window_scores_ex(const void *vis, int64_t vis_row_stride, int64_t v
  * identity, fp64).  k: fp16, element (b, h, t, c) at k[b*k_strides[0] + h*k_strides[1] +
  * t*k_strides[2] + c] (rows 16-byte aligned); q_text: fp16, element (b, hq, j, c) at
  * q_text[b*q_strides[0] + hq*q_strides[1] + j*q_strides[2] + c].  scores fp64 [B][W].
- * workspace: wq_window_scores_workspace(B, H*d) bytes.
- * Errors: WQ_ESHAPE (S, M < S, H*d > 4096, Hq % H), WQ_EUNSUPPORTED (d not 64/128). */
+ * workspace: wq_window_scores_workspace(B, H*d) bytes.  k and q_text rows 16-byte aligned.
+ * Errors: WQ_ESHAPE (S, M < S, H*d > 1024, Hq % H, Hq/H > 8), WQ_EUNSUPPORTED (d not 64/128),
+ * WQ_EINVAL (alignment). */
 wq_status wq_window_scores_layer(const void *k, const int64_t k_strides[3], int32_t vis_off, const void *q_text,
                                  const int64_t q_strides[3], int32_t B, int32_t H, int32_t Hq, int32_t d,
                                  int32_t M, int32_t N, int32_t S, double *scores, void *workspace,

@@ -134,9 +134,12 @@ wq_status wq_window_scores_layer(const void *k, const int64_t k_strides[3], int3
   if (!(d == 64 || d == 128)) return fail(WQ_EUNSUPPORTED, "head dim d=%d not in {64,128}", d);
   if (H < 1 || Hq < H || Hq % H) return fail(WQ_ESHAPE, "Hq=%d not a multiple of H=%d", Hq, H);
   const int D = H * d;
-  if (D > 4096) return fail(WQ_ESHAPE, "H*d=%d > 4096", D);
+  if (D > 1024) return fail(WQ_ESHAPE, "H*d=%d > 1024", D);
+  if (Hq / H > 8) return fail(WQ_ESHAPE, "GQA group Hq/H=%d > 8", Hq / H);
   if (k_strides[0] % 8 || k_strides[1] % 8 || k_strides[2] % 8 || !aligned16(k))
     return fail(WQ_EINVAL, "K rows must be 16-byte aligned (strides multiple of 8 elements)");
+  if (q_strides[0] % 8 || q_strides[1] % 8 || q_strides[2] % 8 || !aligned16(q_text))
+    return fail(WQ_EINVAL, "q_text rows must be 16-byte aligned (strides multiple of 8 elements)");
   if (workspace_bytes < (size_t)B * D * sizeof(double)) return fail(WQ_EINVAL, "workspace too small");
   double *tbar = reinterpret_cast<double *>(workspace);
   wq_status s = cuda_status(wq::launch_text_pool_q((const __half *)q_text, q_strides[0], q_strides[1], q_strides[2],

@@ -14,31 +14,73 @@ namespace wq {
 // Per-layer scorer text side (reading Q36): text row j of request b is the concatenation
 // over kv heads h of the mean of its GQA group's queries, (1/g) sum_{g'} Q[b][h g + g'][j][:]
 // (D = H d, fp64); tbar[b][:] = sum_j row_j / ||row_j|| (a zero row contributes 0).
-__global__ void __launch_bounds__(ST) k_text_pool_q(const __half *__restrict__ qt, int64_t qsb, int64_t qsh,
-                                                    int64_t qsj, int N, int H, int grp, int d,
-                                                    double *__restrict__ tbar) {
-  extern __shared__ double sh[];                 // pooled [D], row [D]
-  __shared__ double red[4];
+// A warp per text row (8 warps, rows j = warp, warp + 8, ...): lane l owns channels
+// l + 32 i of the row; the row's norm is a warp-shuffle tree; the 8 warps' pooled
+// vectors are summed in fixed order at the end (sh: [8][D] doubles).
+constexpr int TPQ = 256;
+template <int NCH>                               // 8-channel chunks per lane: ceil(D / 256)
+__global__ void __launch_bounds__(TPQ) k_text_pool_q(const __half *__restrict__ qt, int64_t qsb, int64_t qsh,
+                                                     int64_t qsj, int N, int H, int grp, int d,
+                                                     double *__restrict__ tbar) {
+  extern __shared__ double sh[];                 // [8][D] per-warp pooled vectors
   const int b = blockIdx.x, D = H * d;
-  double *pooled = sh, *row = sh + D;
-  for (int c = threadIdx.x; c < D; c += ST) pooled[c] = 0.0;
-  for (int j = 0; j < N; j++) {
-    double ss[1] = {0.0};
-    for (int c = threadIdx.x; c < D; c += ST) {
-      const int h = c / d, cc = c - h * d;
-      double acc = 0.0;
-      for (int gq = 0; gq < grp; gq++)
-        acc += (double)__half2float(qt[b * qsb + (int64_t)(h * grp + gq) * qsh + (int64_t)j * qsj + cc]);
-      const double x = acc / (double)grp;
-      row[c] = x;
-      ss[0] = fma(x, x, ss[0]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *mine = sh + (size_t)warp * D;
+  for (int c = lane; c < D; c += 32) mine[c] = 0.0;
+  __syncwarp();
+  const double ginv = 1.0 / (double)grp;
+  for (int j = warp; j < N; j += TPQ / 32) {
+    double x[NCH][8];
+    double ss = 0.0;
+#pragma unroll
+    for (int i = 0; i < NCH; i++) {
+      const int c0 = 8 * (lane + 32 * i);
+#pragma unroll
+      for (int e = 0; e < 8; e++) x[i][e] = 0.0;
+      if (c0 < D) {
+        const int h = c0 / d, cc = c0 - h * d;
+        const __half *row = qt + b * qsb + (int64_t)h * grp * qsh + (int64_t)j * qsj + cc;
+        // the group's query rows: independent 16-byte loads, summed in fp64 in head order
+        uint4 u[8];
+#pragma unroll
+        for (int gq = 0; gq < 8; gq++)
+          if (gq < grp) u[gq] = __ldg(reinterpret_cast<const uint4 *>(row + gq * qsh));
+#pragma unroll
+        for (int gq = 0; gq < 8; gq++) {
+          if (gq >= grp) break;
+          const __half2 *hh = reinterpret_cast<const __half2 *>(&u[gq]);
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const float2 f = __half22float2(hh[e]);
+            x[i][2 * e] += (double)f.x;
+            x[i][2 * e + 1] += (double)f.y;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+          x[i][e] *= ginv;
+          ss = fma(x[i][e], x[i][e], ss);
+        }
+      }
     }
-    block_sum<1>(ss, red);
-    const double inv = ss[0] > 0.0 ? 1.0 / sqrt(ss[0]) : 0.0;
-    for (int c = threadIdx.x; c < D; c += ST) pooled[c] = fma(row[c], inv, pooled[c]);
-    __syncthreads();
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const double inv = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+#pragma unroll
+    for (int i = 0; i < NCH; i++) {
+      const int c0 = 8 * (lane + 32 * i);
+      if (c0 < D)
+#pragma unroll
+        for (int e = 0; e < 8; e++) mine[c0 + e] = fma(x[i][e], inv, mine[c0 + e]);
+    }
   }
-  for (int c = threadIdx.x; c < D; c += ST) tbar[(int64_t)b * D + c] = pooled[c];
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += TPQ) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < TPQ / 32; w++) v += sh[(size_t)w * D + c];
+    tbar[(int64_t)b * D + c] = v;
+  }
 }
 
 // Per-layer scorer visual side for short head-split rows (D = H d <= 1024): one CTA of
@@ -127,10 +169,14 @@ __global__ void __launch_bounds__(ST) k_window_scores_rows(const __half *__restr
 
 cudaError_t launch_text_pool_q(const __half *qt, int64_t qsb, int64_t qsh, int64_t qsj, int B, int N, int H,
                                int grp, int d, double *tbar, cudaStream_t st) {
-  const size_t smem = (size_t)2 * H * d * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(k_text_pool_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = (size_t)(TPQ / 32) * H * d * sizeof(double);
+  if (grp > 8 || (d % 8) || (qsb % 8) || (qsh % 8) || (qsj % 8) || (reinterpret_cast<uintptr_t>(qt) & 15))
+    return cudaErrorInvalidValue;                // (16-byte loads: the ABI checks these first)
+  const int nch = (H * d / 8 + 31) / 32;
+  auto kern = nch <= 1 ? k_text_pool_q<1> : nch <= 2 ? k_text_pool_q<2> : k_text_pool_q<4>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_text_pool_q<<<B, ST, smem, st>>>(qt, qsb, qsh, qsj, N, H, grp, d, tbar);
+  kern<<<B, TPQ, smem, st>>>(qt, qsb, qsh, qsj, N, H, grp, d, tbar);
   return cudaGetLastError();
 }
 
