@@ -56,3 +56,17 @@ def test_host_packed_bytes_match_oracle(orc):
             for counts in ([1, 0, 0, 0], [3, 5, 7, 1], [0, 0, 0, 9]):
                 for code_only in (False, True):
                     assert wq.wq_packed_bytes(g, counts, code_only) == orc.packed_bytes(og, counts, code_only)
+
+
+def test_host_packed_bytes_group_granularity(orc):
+    """WQ_GRAN_GROUP record sizes (reading Q37) against the oracle's record_bytes(gran=1);
+    an unknown granularity is rejected on the host."""
+    for d in (64, 128):
+        for S in (16, 32, 64, 128):
+            g = wq.geom(1, 4, 28, d, S * 40, S, (2, 4, 8, 16))
+            for counts in ([1, 0, 0, 0], [3, 5, 7, 1], [0, 0, 0, 9]):
+                ref = sum(n * orc.record_bytes(b, d, S, 1) for n, b in zip(counts, (2, 4, 8, 16)))
+                assert wq.wq_packed_bytes(g, counts, False, gran=wq.WQ_GRAN_GROUP) == ref
+                assert wq.wq_packed_bytes(g, counts, True, gran=wq.WQ_GRAN_GROUP) == wq.wq_packed_bytes(g, counts, True)
+    with pytest.raises(wq.WQError):
+        wq.wq_packed_bytes(wq.geom(1, 4, 28, 128, 320, 32, (2, 4, 8, 16)), [1, 1, 1, 1], False, gran=7)
