@@ -240,8 +240,17 @@ class Workload:
                     wq.wq_decode_attention(self.q[t, l], self.packed[l], self.offs[l], self.seg_r[l], self.g,
                                            self.kr[l], self.vr[l], rl, self.sm_scale, partial=self.part,
                                            workspace=self.dws, flags=flags)
-                    torch.distributed.all_gather_into_tensor(self.gathered, self.part, group=group)
+                    self._all_gather(group)
                     wq.wq_merge_partials(self.gathered, self.g, out=self.out[t, l])
+
+    def _all_gather(self, group):
+        """partials of every rank into self.gathered: one NCCL all-gather (the gloo
+        backend of the CPU-collective test runs takes the list form)."""
+        import torch.distributed as dist
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(self.gathered, self.part, group=group)
+        else:
+            dist.all_gather(list(self.gathered.unbind(0)), self.part, group=group)
 
     def _peer_checked(self, group):
         """After the first fused call: every rank checks its timeout flag, and if any rank's
@@ -259,7 +268,7 @@ class Workload:
         rl = self.rest_len[0] if self.rank == 0 else self.rest_zero
         wq.wq_decode_attention(self.q[0, 0], self.packed[0], self.offs[0], self.seg_r[0], self.g, self.kr[0],
                                self.vr[0], rl, self.sm_scale, partial=self.part, workspace=self.dws)
-        torch.distributed.all_gather_into_tensor(self.gathered, self.part, group=group)
+        self._all_gather(group)
         wq.wq_merge_partials(self.gathered, self.g, out=self.out[0, 0])
         return False
 
