@@ -360,6 +360,7 @@ wq_status wq_shard_slots(const int32_t *perm_l, const int32_t *seg_off_l, int32_
  *     x^16 = RN_fp16(mn + s * code)    (the exact Eq.15 value, one rounding to fp16)
  *   for b-bit records and the stored values for FP16 records.  Bit-exact with the
  *   oracle.  Decode the result with wq_decode_attention(..., img16, offs16, seg16, ...).
+ *   Input images of WQ_GRAN_CHANNEL_TOKEN granularity only (the default).
  * Errors: WQ_EINVAL (NULL, misaligned), WQ_ESHAPE (geometry). */
 wq_status wq_dequant_layout(const wq_geom *g, const int32_t *seg_off_l, int32_t *seg16, int64_t *offs16,
                             void *stream);
@@ -379,7 +380,8 @@ wq_status wq_dequantize_image(const uint8_t *packed, const int64_t *offs, const 
  *   image a quantizer without the reordering step writes).
  * wq_decode_attention_unreordered: wq_decode_attention over uimg; windows are visited
  *   in original order, each dispatched on its own width.  Same outputs/workspace/errors
- *   as wq_decode_attention (the result equals the reordered decode, Eq.12-13). */
+ *   as wq_decode_attention (the result equals the reordered decode, Eq.12-13).
+ *   WQ_GRAN_CHANNEL_TOKEN images only (record sizes of the default granularity). */
 wq_status wq_unreordered_layout(const wq_geom *g, const uint8_t *bits_l, int64_t *woff, void *stream);
 wq_status wq_unreorder_image(const uint8_t *packed, const int64_t *offs, const int32_t *seg_off_l,
                              const int32_t *perm_l, const wq_geom *g, const int64_t *woff, uint8_t *uimg,
@@ -409,7 +411,8 @@ wq_status wq_decode_attention_unreordered(const void *q, const uint8_t *uimg, co
  *   `epoch` = 1, 2, 3, ... on every call (the same on all ranks); all G ranks must make
  *   the same sequence of calls (the kernel waits on its peers' contributions).
  *   peer_bufs: device array [G] of device pointers (entry `rank` = local_buf).
- *   No PDL flag.  With G = 1 it is the ordinary decode through the exchange path.
+ *   No PDL flag, WQ_GRAN_CHANNEL_TOKEN images only.  With G = 1 it is the ordinary decode
+ *   through the exchange path.
  *   Every CTA of the launch must be resident at once (one per SM, grid = SM count):
  *   the call returns WQ_ECUDA if the occupancy query says otherwise.  The tcgen05
  *   variant (WQ_DECODE_TC) is never used for this call.
