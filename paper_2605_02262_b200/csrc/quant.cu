@@ -122,13 +122,18 @@ struct QuantGeo {
 #ifndef WQ_Q_NSL
 #define WQ_Q_NSL 0                                      // 0: by window size (below)
 #endif
-  // window slots per team: small windows buffer 3-4 deep (bytes in flight: the copy latency
-  // under load is ~3 us); for S >= 64 (32-64 KB windows) one slot per team and more teams
-  static constexpr int NSL0 = S >= 64 ? 1 : ((50 * 1024) / WIN > 4 ? 4 : (50 * 1024) / WIN);
-  static constexpr int NSL = WQ_Q_NSL > 0 ? WQ_Q_NSL : (NSL0 < 2 && S < 64 ? 2 : NSL0);
+  // window slots per team: two for S <= 32, one for S >= 64 (32-64 KB windows), and up to
+  // five teams: more warps to hide the latencies of an issue-bound kernel beat deeper
+  // per-team buffering (A/B round 2, tools/quant_ab.py, vs 3-4 slots x 4 teams: C5 117.4 ->
+  // 110.8 us, C4 S=32 418 -> 379, S=16 639 -> 538, S=64 509 -> 467, S=128 unchanged)
+  static constexpr int NSL0 = S >= 64 ? 1 : 2;
+  static constexpr int NSL = WQ_Q_NSL > 0 ? WQ_Q_NSL : NSL0;
   static constexpr int PER_TEAM = ((NSL * WIN + 4 * SCR) + 1023) / 1024 * 1024;   // slots 1024-B aligned
   static constexpr int T0 = (216 * 1024) / PER_TEAM;
-  static constexpr int TEAMS = T0 > 4 ? 4 : (T0 < 1 ? 1 : T0);
+#ifndef WQ_Q_TMAX
+#define WQ_Q_TMAX 5                                     // most teams (4 warps each) per CTA
+#endif
+  static constexpr int TEAMS = T0 > WQ_Q_TMAX ? WQ_Q_TMAX : (T0 < 1 ? 1 : T0);
   static constexpr int NT = S / 16 + 2;                 // tasks per window: 2 K halves + S/16 V tiles
   static constexpr size_t bar_off = (size_t)TEAMS * PER_TEAM;
   static constexpr size_t desc_off = bar_off + TEAMS * 2 * NSL * 8;   // [TEAMS][NSL] WinDesc
