@@ -183,7 +183,11 @@ cudaError_t launch_text_pool_q(const __half *qt, int64_t qsb, int64_t qsh, int64
 cudaError_t launch_text_pool(const __half *txt, int64_t trs, int64_t tbs, int B, int N, int D,
                              double *tbar, int metric, cudaStream_t st) {
   size_t smem = (size_t)D * sizeof(double);
-  auto kern = metric == 1 ? k_text_pool<true> : k_text_pool<false>;
+  const int nc = (D / 8 + ST - 1) / ST;
+  auto kern = metric == 1 ? (nc <= 1 ? k_text_pool<1, true> : nc <= 2 ? k_text_pool<2, true>
+                             : nc <= 3 ? k_text_pool<3, true> : k_text_pool<4, true>)
+                          : (nc <= 1 ? k_text_pool<1, false> : nc <= 2 ? k_text_pool<2, false>
+                             : nc <= 3 ? k_text_pool<3, false> : k_text_pool<4, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<B, ST, smem, st>>>(txt, trs, tbs, N, D, tbar);

@@ -43,44 +43,80 @@ WQ_DEV void load8(const __half *p, double (&x)[8]) {
   }
 }
 
-// tbar[b] of request b by one CTA of ST threads; pooled: shared [D], red: shared [4]
-template <bool CENTER>
+// tbar[b] of request b by one CTA of ST threads; pooled: shared [D] doubles (>= 8), red:
+// shared [4].  Rows are taken in batches of NB: (A) a warp per row computes its mean
+// (Pearson) and inverse norm with lane-strided 16-byte loads and a shuffle tree into
+// pooled; (B) each thread accumulates its NC channel chunks over the batch's rows in row
+// order (independent loads, no barrier per row).  tbar[b][c] = sum_j (x_j[c] - mu_j) /
+// ||x_j - mu_j|| in ascending j for every c (a zero row contributes 0).
+template <int NC, bool CENTER>
 WQ_DEV void text_pool_body(const __half *__restrict__ txt, int64_t trs, int64_t tbs, int N, int D,
                            double *__restrict__ tbar, int b, double *pooled, double *red) {
+  (void)red;
   const int nchunk = D / 8;
-  for (int c = threadIdx.x; c < D; c += ST) pooled[c] = 0.0;
-  for (int j = 0; j < N; j++) {
-    const __half *row = txt + b * tbs + (int64_t)j * trs;
-    double mu = 0.0;
-    if (CENTER) {                                  // Pearson: centre the row first (T11)
-      double sm[1] = {0.0};
-      for (int k = threadIdx.x; k < nchunk; k += ST) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NB = D / 2 < 32 ? D / 2 : 32;        // rows per batch ((mu, inv) pairs in pooled)
+  double acc[NC][8];
+#pragma unroll
+  for (int i = 0; i < NC; i++)
+#pragma unroll
+    for (int e = 0; e < 8; e++) acc[i][e] = 0.0;
+  const __half *base = txt + b * tbs;
+  for (int j0 = 0; j0 < N; j0 += NB) {
+    const int nb = N - j0 < NB ? N - j0 : NB;
+    for (int jj = warp; jj < nb; jj += ST / 32) {
+      const __half *row = base + (int64_t)(j0 + jj) * trs;
+      double mu = 0.0;
+      if (CENTER) {
+        double sm = 0.0;
+        for (int k = lane; k < nchunk; k += 32) {
+          double x[8];
+          load8(row + 8 * k, x);
+#pragma unroll
+          for (int e = 0; e < 8; e++) sm += x[e];
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+        mu = sm / (double)D;
+      }
+      double ss = 0.0;
+      for (int k = lane; k < nchunk; k += 32) {
         double x[8];
         load8(row + 8 * k, x);
 #pragma unroll
-        for (int i = 0; i < 8; i++) sm[0] += x[i];
+        for (int e = 0; e < 8; e++) ss = fma(x[e] - mu, x[e] - mu, ss);
       }
-      block_sum<1>(sm, red);
-      mu = sm[0] / (double)D;
-    }
-    double ss[1] = {0.0};
-    for (int k = threadIdx.x; k < nchunk; k += ST) {
-      double x[8];
-      load8(row + 8 * k, x);
 #pragma unroll
-      for (int i = 0; i < 8; i++) ss[0] = fma(x[i] - mu, x[i] - mu, ss[0]);
+      for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) {
+        pooled[2 * jj] = mu;
+        pooled[2 * jj + 1] = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+      }
     }
-    block_sum<1>(ss, red);
-    double inv = ss[0] > 0.0 ? 1.0 / sqrt(ss[0]) : 0.0;
-    for (int k = threadIdx.x; k < nchunk; k += ST) {
-      double x[8];
-      load8(row + 8 * k, x);
+    __syncthreads();
 #pragma unroll
-      for (int i = 0; i < 8; i++) pooled[8 * k + i] = fma(x[i] - mu, inv, pooled[8 * k + i]);
+    for (int i = 0; i < NC; i++) {
+      const int k = threadIdx.x + ST * i;
+      if (k < nchunk) {
+#pragma unroll 4
+        for (int jj = 0; jj < nb; jj++) {
+          double x[8];
+          load8(base + (int64_t)(j0 + jj) * trs + 8 * k, x);
+          const double m = pooled[2 * jj], inv = pooled[2 * jj + 1];
+#pragma unroll
+          for (int e = 0; e < 8; e++) acc[i][e] = fma(x[e] - m, inv, acc[i][e]);
+        }
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < D; c += ST) tbar[(int64_t)b * D + c] = pooled[c];
+#pragma unroll
+  for (int i = 0; i < NC; i++) {
+    const int k = threadIdx.x + ST * i;
+    if (k < nchunk)
+#pragma unroll
+      for (int e = 0; e < 8; e++) tbar[(int64_t)b * D + 8 * k + e] = acc[i][e];
+  }
   __syncthreads();
 }
 
@@ -192,12 +228,12 @@ WQ_DEV void window_score_body(const __half *__restrict__ vis, int64_t vrs, int64
 }  // namespace wq
 
 namespace wq {
-template <bool CENTER>
+template <int NC, bool CENTER>
 __global__ void __launch_bounds__(ST) k_text_pool(const __half *__restrict__ txt, int64_t trs,
                                                   int64_t tbs, int N, int D, double *__restrict__ tbar) {
   extern __shared__ double pooled[];  // [D]
   __shared__ double red[4];
-  text_pool_body<CENTER>(txt, trs, tbs, N, D, tbar, blockIdx.x, pooled, red);
+  text_pool_body<NC, CENTER>(txt, trs, tbs, N, D, tbar, blockIdx.x, pooled, red);
 }
 
 template <int NC, bool CENTER, bool HS>

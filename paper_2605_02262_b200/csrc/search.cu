@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(ST, WQ_SC_MINB) k_search(SearchArgs a) {
   const int W = a.M / a.S;
   // 1. pooled text rows
   for (int b = blockIdx.x; b < a.B; b += gridDim.x)
-    text_pool_body<CENTER>(a.txt, a.trs, a.tbs, a.N, a.D, a.tbar, b, reinterpret_cast<double *>(sm), red);
+    text_pool_body<NC, CENTER>(a.txt, a.trs, a.tbs, a.N, a.D, a.tbar, b, reinterpret_cast<double *>(sm), red);
   grid.sync();
   // 2. window scores
   for (int t = blockIdx.x; t < a.B * W; t += gridDim.x)
