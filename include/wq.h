@@ -287,7 +287,8 @@ wq_status wq_reorder_quantize_pack_ex(const void *k, const void *v, const int64_
  *   (unnormalized; m = -inf, l = 0 for an empty cache), may be NULL.
  * workspace: wq_decode_workspace(g) bytes, zero-filled once.
  * Numerical domain (fp16 intermediates of the fused dequantization): for every K
- *   channel group |q_c| * s_c < 2^15 (q*s is carried as an fp16 hi + lo pair) and for
+ *   channel group |q_c| * s_c < 2^15 (q*s is carried as an fp16 hi + lo pair; 2-bit
+ *   windows carry (code - 2) * s_c in fp16 instead, which needs s_c <= 32752) and for
  *   every V token group s_t < 255 (p * s_t is an fp16 MMA operand with p <= 2^8, the
  *   lazy-rescale headroom).  Outside it results are undefined.  For b = 2 this allows V
  *   ranges up to 765 and, with |q| <= 8, K channel ranges up to 12288.  Inside it the

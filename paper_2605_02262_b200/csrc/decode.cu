@@ -15,7 +15,9 @@
 //  * Consumers: one warp per window.  K side: scores[t][j] = sum_c code[t][c] *
 //    q'_j[c] + bias_j with q' = q*s_c folded per window (split hi+lo in fp16 so the
 //    product is carried to ~2^-22) and bias_j = sum_c q_j[c]*mn_c, all on
-//    mma.sync m16n8k16 (tokens x heads, fp32 accumulate).  Codes are loaded in
+//    mma.sync m16n8k16 (tokens x heads, fp32 accumulate).  2-bit windows instead put
+//    the scale on the A side: (code - 2) * s_c in {-2s, -s, 0, s} is exact in fp16, so
+//    one MMA against the raw q has exact products (WQ_DEC_K2S).  Codes are loaded in
 //    D-1 fragment order straight into MMA A registers and turned into exact fp16
 //    integers with one LOP3 + one HSUB2 per pair (magic-exponent trick).  Online
 //    softmax per window in the exp2 domain with a lazy rescale (max may run 2^8
@@ -39,6 +41,12 @@ constexpr int NCW = WQ_DEC_NCW;                 // consumer warps
 constexpr int DT = (NCW + 1) * 32;      // threads per CTA: consumers + the producer warp
 #ifndef WQ_DEC_QLO
 #define WQ_DEC_QLO 1                     // carry q*s as fp16 hi + lo (0: hi only, experiment)
+#endif
+#ifndef WQ_DEC_KCENTER
+#define WQ_DEC_KCENTER 0                 // 1: centered K codes, q' = q*s in fp16 hi only (no lo MMA); 0: hi + lo
+#endif
+#ifndef WQ_DEC_K2S
+#define WQ_DEC_K2S 1                     // 2-bit K side: A = (code - 2) * s_c (exact in fp16), B = q, one MMA
 #endif
 #ifndef WQ_DEC_PAIR
 #define WQ_DEC_PAIR 0                    // 1: 2-bit windows in pairs (do_window2), S <= 32 (A/B: slower)
@@ -220,6 +228,12 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
   const uint8_t *vcodes = rec + KBR + part * (S * D * BITS / 8);
   const uint8_t *kp = rec + 2 * KBR;
   const int g = lane >> 2, q = lane & 3;
+  // K2: 2-bit windows carry the channel scale on the A side: (code - 2) * s_c is one of
+  // {-2s, -s, 0, s}, exact in fp16, so one MMA against the raw q gives exact products
+  // (no hi/lo split of q * s_c); the centering adds 2 * sum_c q_c s_c (zero-point rows g + 8).
+  constexpr bool K2 = (BITS == 2) && (WQ_DEC_K2S != 0);
+  constexpr bool KC = K2 || (WQ_DEC_KCENTER != 0 && BITS < 16);
+  constexpr bool LO = (BITS < 16) && !KC && (WQ_DEC_QLO != 0);
   float b0[4] = {0.f, 0.f, 0.f, 0.f}, b1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int c0 = 0; c0 < NTT; c0 += CH) {
@@ -246,9 +260,14 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
           if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
           else mma16816(b0, am, qk.x, qk.y, b0);
         }
-        h0 = hmul2u(qk.x, pr.y);
-        h1 = hmul2u(qk.y, pr.w);
-        if constexpr (WQ_DEC_QLO) {
+        if constexpr (K2) {
+          h0 = pr.y;                                       // s01, s89: A-side scales
+          h1 = pr.w;
+        } else {
+          h0 = hmul2u(qk.x, pr.y);
+          h1 = hmul2u(qk.y, pr.w);
+        }
+        if constexpr (LO) {
           l0 = h2u(__hfma2(u2h(qk.x), u2h(pr.y), __hneg2(u2h(h0))));
           l1 = h2u(__hfma2(u2h(qk.y), u2h(pr.w), __hneg2(u2h(h1))));
         }
@@ -257,9 +276,15 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
       for (int t = 0; t < CH; t++) {
         uint32_t a[4];
 #pragma unroll
-        for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS>(wk[t], 4 * kt + r);
-        if constexpr (BITS < 16) {
-          if constexpr (WQ_DEC_QLO) {
+        for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS, KC>(wk[t], 4 * kt + r);
+        if constexpr (K2) {
+          // a[0], a[1]: channels 16 kt + 2q, +1 (rows g, g + 8); a[2], a[3]: + 8
+          a[0] = hmul2u(a[0], h0); a[1] = hmul2u(a[1], h0);
+          a[2] = hmul2u(a[2], h1); a[3] = hmul2u(a[3], h1);
+          if (kt & 1) mma16816(al[t], a, qk.x, qk.y, al[t]);
+          else mma16816(ah[t], a, qk.x, qk.y, ah[t]);
+        } else if constexpr (BITS < 16) {
+          if constexpr (LO) {
             mma16816(ah[t], a, h0, h1, ah[t]);
             mma16816(al[t], a, l0, l1, al[t]);
           } else {
@@ -276,7 +301,12 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
 #pragma unroll
     for (int t = 0; t < CH; t++)
 #pragma unroll
-      for (int i = 0; i < 4; i++) sc[t][i] = (ah[t][i] + al[t][i]) + (b0[i & 1] + b1[i & 1]);
+      for (int i = 0; i < 4; i++) {
+        sc[t][i] = (ah[t][i] + al[t][i]) + (b0[i & 1] + b1[i & 1]);
+        // centered K codes: + 2^(BITS-1) * sum_c q_c s_c (rows g + 8 of the zero-point MMA)
+        if constexpr (KC)
+          sc[t][i] += (float)(1 << (BITS - 1)) * (b0[2 + (i & 1)] + b1[2 + (i & 1)]);
+      }
     float vs[CH][2], vm[CH][2];
     if constexpr (BITS < 16) {
       const uint8_t *vp = kp + 4 * D + part * 4 * S;

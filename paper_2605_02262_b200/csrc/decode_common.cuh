@@ -22,10 +22,10 @@ constexpr int TS_PER_CTA = 200;        // debug & 8: per-CTA stamps + stage trac
 #define WQ_DEC_EOV 2000                // per-unit entry overhead in cost units of S*D/100
 #endif
 #ifndef WQ_DEC_C4
-#define WQ_DEC_C4 168                  // 4-bit window cost, units of S*D/100 (2-bit: 156)
+#define WQ_DEC_C4 174                  // 4-bit window cost, units of S*D/100 (2-bit: 156; r02 K2S refit 168 -> 174)
 #endif
 #ifndef WQ_DEC_C8
-#define WQ_DEC_C8 191                  // 8-bit window cost (r02 refit: 233 -> 191, C5 -3.3 %, C3 -3.6 %)
+#define WQ_DEC_C8 204                  // 8-bit window cost (r02 refit: 233 -> 191, C5 -3.3 %, C3 -3.6 %; K2S refit -> 204)
 #endif
 #ifndef WQ_DEC_C16
 #define WQ_DEC_C16 171                 // FP16 window cost, units of S*D/100 (r02 refit: 235 -> 171)
@@ -72,6 +72,8 @@ struct ItemGeo {
   //   8-bit 0.166, FP16 0.149 -> 156 : 168 : 191 : 171 in units of S*D/100 (round 1's
   //   156 : 170 : 233 : 235 left 8-bit-heavy CTAs idle ~7 us before the 2-bit ones);
   //   A/B over 4 tables: C5 34.96 -> 33.79 us, C3 38.81 -> 37.41 us, C4 unchanged.
+  //   After the exact 2-bit K side (WQ_DEC_K2S: 2-bit windows 0.129 us, 4-bit 0.148, 8-bit
+  //   0.176) 156 : 174 : 204 : 171 (A/B of 4 tables: C5 33.34 -> 32.84, C3 35.87 -> 35.71).
   //  tcgen05 kernel: the tensor work is asynchronous, an item costs its bytes plus
   //   a per-window dequantization term (same units).
   // fixed cost of one unit entry of a CTA (its epilogue, ~2 us: ~13 2-bit windows),
