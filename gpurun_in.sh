@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "fused_search or assign" > gpurun_out/t18.log 2>&1; echo t18=$? > gpurun_out/rc17.txt
-timeout 600 python tools/search_time.py C5 C3 C2 C4 > gpurun_out/search_time.log 2>&1
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_suite.log 2>&1; echo suite=$? >> gpurun_out/gpu_suite.log
+timeout 1200 bash tools/run_cfgs.sh > gpurun_out/run_cfgs.log 2>&1
