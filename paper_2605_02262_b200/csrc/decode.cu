@@ -48,9 +48,6 @@ constexpr int DT = (NCW + 1) * 32;      // threads per CTA: consumers + the prod
 #ifndef WQ_DEC_K2S
 #define WQ_DEC_K2S 1                     // 2-bit K side: A = (code - 2) * s_c (exact in fp16), B = q, one MMA
 #endif
-#ifndef WQ_DEC_TP
-#define WQ_DEC_TP 0                      // 1: 32-token b-bit windows tile-pipelined (do_window_tp)
-#endif
 #ifndef WQ_DEC_PAIR
 #define WQ_DEC_PAIR 0                    // 1: 2-bit windows in pairs (do_window2), S <= 32 (A/B: slower)
 #endif
@@ -338,112 +335,6 @@ WQ_DEV void do_window(const uint8_t *rec, const uint8_t *qs, float scale2,
     }
     __syncwarp();
   }
-}
-
-// Tile-pipelined 32-token window (b-bit, per-channel K / per-token V): tile 0's K side
-// and softmax, then ONE unrolled k-tile loop that interleaves tile 1's K-side MMAs with
-// tile 0's V-side MMAs (two independent instruction streams for the scheduler), then
-// tile 1's softmax and V side.  Same products and accumulation order per accumulator as
-// do_window; the online softmax runs per 16-token tile instead of per window.
-template <int D, int BITS, int SR = 32>
-WQ_DEV void do_window_tp(const uint8_t *rec, const uint8_t *qs, float scale2,
-                         WarpState &st, float (&o)[D / 16][4], uint8_t *scratch, int lane, int part = 0) {
-  constexpr int S = 32;
-  static_assert(BITS < 16, "b-bit records only");
-  constexpr int KBR = SR * D * BITS / 8;
-  constexpr int KT = D / 16;
-  constexpr int WPL = D * BITS / 64;
-  constexpr int TILE = 2 * D * BITS;
-  constexpr bool K2 = (BITS == 2) && (WQ_DEC_K2S != 0);
-  constexpr bool KC = K2 || (WQ_DEC_KCENTER != 0);
-  constexpr bool LO = !KC && (WQ_DEC_QLO != 0);
-  constexpr float HALF = (float)(1 << (BITS - 1));
-  const uint8_t *kcodes = rec + part * (S * D * BITS / 8);
-  const uint8_t *vcodes = rec + KBR + part * (S * D * BITS / 8);
-  const uint8_t *kp = rec + 2 * KBR;
-  const uint8_t *vp = kp + 4 * D + part * 4 * S;
-  const int g = lane >> 2, q = lane & 3;
-  float b0[4] = {0.f, 0.f, 0.f, 0.f}, b1[4] = {0.f, 0.f, 0.f, 0.f};
-  // K side of one k-tile for one tile: params, B operands, MMA(s) into (ah, al)
-  auto kstep = [&](const uint32_t (&wk)[WPL], int kt, float (&ah)[4], float (&al)[4], bool zp) {
-    const uint2 qk = lds64(qs + (kt * 32 + lane) * 8);
-    const uint4 pr = lds128(kp + (4 * kt + q) * 16);
-    if (zp && !WQ_EXP_NOZP) {
-      const uint32_t am[4] = {pr.x, pr.y, pr.z, pr.w};
-      if (kt & 1) mma16816(b1, am, qk.x, qk.y, b1);
-      else mma16816(b0, am, qk.x, qk.y, b0);
-    }
-    uint32_t a[4];
-#pragma unroll
-    for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS, KC>(wk, 4 * kt + r);
-    if constexpr (K2) {
-      a[0] = hmul2u(a[0], pr.y); a[1] = hmul2u(a[1], pr.y);
-      a[2] = hmul2u(a[2], pr.w); a[3] = hmul2u(a[3], pr.w);
-      if (kt & 1) mma16816(al, a, qk.x, qk.y, al);
-      else mma16816(ah, a, qk.x, qk.y, ah);
-    } else {
-      const uint32_t h0 = hmul2u(qk.x, pr.y), h1 = hmul2u(qk.y, pr.w);
-      if constexpr (LO) {
-        const uint32_t l0 = h2u(__hfma2(u2h(qk.x), u2h(pr.y), __hneg2(u2h(h0))));
-        const uint32_t l1 = h2u(__hfma2(u2h(qk.y), u2h(pr.w), __hneg2(u2h(h1))));
-        mma16816(ah, a, h0, h1, ah);
-        mma16816(al, a, l0, l1, al);
-      } else {
-        if (kt & 1) mma16816(al, a, h0, h1, al);
-        else mma16816(ah, a, h0, h1, ah);
-      }
-    }
-  };
-  auto finish = [&](const float (&ah)[4], const float (&al)[4], int t, float (&sc)[1][4], float (&vs)[1][2],
-                    float (&vm)[1][2]) {
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      sc[0][i] = (ah[i] + al[i]) + (b0[i & 1] + b1[i & 1]);
-      if constexpr (KC) sc[0][i] += HALF * (b0[2 + (i & 1)] + b1[2 + (i & 1)]);
-    }
-    const uint4 pr = lds128(vp + (4 * t + (g >> 1)) * 16);
-    const uint32_t sh = (g & 1) * 16;
-    vs[0][0] = __half2float(__ushort_as_half((unsigned short)(pr.x >> sh)));
-    vs[0][1] = __half2float(__ushort_as_half((unsigned short)(pr.y >> sh)));
-    vm[0][0] = fmaf(vs[0][0], HALF, __half2float(__ushort_as_half((unsigned short)(pr.z >> sh))));
-    vm[0][1] = fmaf(vs[0][1], HALF, __half2float(__ushort_as_half((unsigned short)(pr.w >> sh))));
-  };
-  float sc[1][4], vs[1][2], vm[1][2];
-  {
-    uint32_t wk[WPL];
-    load_chunk<D, BITS>(wk, kcodes, lane);
-    float ah[4] = {0.f, 0.f, 0.f, 0.f}, al[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int kt = 0; kt < KT; kt++) kstep(wk, kt, ah, al, true);
-    finish(ah, al, 0, sc, vs, vm);
-  }
-  softmax_tiles<1, KT>(sc, scale2, st, o, vs, vm, true, scratch, lane);
-  {
-    uint32_t pb[2];
-    ldsm_x2_t(pb, scratch + (lane & 15) * 16);
-    uint32_t wv[WPL], wk[WPL];
-    load_chunk<D, BITS>(wv, vcodes, lane);
-    load_chunk<D, BITS>(wk, kcodes + TILE, lane);
-    float ah[4] = {0.f, 0.f, 0.f, 0.f}, al[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int kt = 0; kt < KT; kt++) {
-      kstep(wk, kt, ah, al, false);
-      uint32_t a[4];
-#pragma unroll
-      for (int r = 0; r < 4; r++) a[r] = deq_pair<BITS, true>(wv, 4 * kt + r);
-      mma16816(o[kt], a, pb[0], pb[1], o[kt]);
-    }
-    finish(ah, al, 1, sc, vs, vm);
-  }
-  softmax_tiles<1, KT>(sc, scale2, st, o, vs, vm, true, scratch + 256, lane);
-  {
-    uint32_t pb[2];
-    ldsm_x2_t(pb, scratch + 256 + (lane & 15) * 16);
-    uint32_t wv[WPL];
-    load_chunk<D, BITS>(wv, vcodes + TILE, lane);
-    tile_pv<D, BITS>(wv, pb[0], pb[1], o);
-  }
-  __syncwarp();
 }
 
 // Two windows A and B of the same b-bit class (S <= 32) in one pass: their 2*S/16 tiles
@@ -952,7 +843,6 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
       // 2-bit stages (S <= 32) are consumed in PAIRS of windows (do_window2): a stage of n
       // records is ceil(n/2) work items, handed out round robin like single items
       constexpr bool PAIRS = WQ_DEC_PAIR && S <= 32 && !GRP;
-      constexpr bool TPW = WQ_DEC_TP && !GRP && !PAIRS && (S > WQ_DEC_SUB && WQ_DEC_SUB > 0 ? WQ_DEC_SUB : S) == 32;
       // records of more than WQ_DEC_SUB tokens are consumed as WQ_DEC_SUB-token parts, each
       // part one work item (a record of n parts keeps n warps busy)
       constexpr int SR16 = S / FS;                 // tokens of an FP16 item
@@ -978,17 +868,13 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
               const uint8_t *r0 = sbase + (size_t)(2 * k) * sz;
               if (2 * k + 1 < nrec) do_window2<D, S, 2>(r0, r0 + sz, qs, a.scale_log2, st, o, scratch, lane);
               else do_window<D, S, 2>(r0, qs, a.scale_log2, st, o, scratch, lane);
-            } else if constexpr (TPW) {
-              do_window_tp<D, 2, S>(rec, qs, a.scale_log2, st, o, scratch, lane, part);
             } else {
               do_window<D, SQ, 2, GRP, S>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum, part);
             }
           } else if (p == 1) {
-            if constexpr (TPW) do_window_tp<D, 4, S>(rec, qs, a.scale_log2, st, o, scratch, lane, part);
-            else do_window<D, SQ, 4, GRP, S>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum, part);
+            do_window<D, SQ, 4, GRP, S>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum, part);
           } else if (p == 2) {
-            if constexpr (TPW && (WQ_DEC_TP & 2)) do_window_tp<D, 8, S>(rec, qs, a.scale_log2, st, o, scratch, lane, part);
-            else do_window<D, SQ, 8, GRP, S>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum, part);
+            do_window<D, SQ, 8, GRP, S>(rec, qs, a.scale_log2, st, o, scratch, lane, qsum, part);
           } else if (p == 3) {
             do_window<D, SF, 16, false, SR16>(rec, qs, a.scale_log2, st, o, scratch, lane, make_float2(0.f, 0.f),
                                               part);
