@@ -772,7 +772,9 @@ WQ_DEV void decode_body(const DecodeArgs &a, const int vc, const int vn) {
       *reinterpret_cast<uint2 *>(qs + (kt * 32 + lane) * 8) = make_uint2(qf[kt][0], qf[kt][1]);
   };
   if (warp == 0 && (a.flags & WQ_DECODE_EARLY_)) griddep_wait();   // q / outputs / workspace
+  if (ts && tid == 0) ts[53] = gtime();
   if (warp == 0 && cp->ua < U) stage_q(cp->ua);
+  if (ts && tid == 0) ts[54] = gtime();
   for (;;) {
     const Entry &E = ent[uidx % SM::NUS];
     while (*reinterpret_cast<const volatile int *>(&E.tag) != uidx) {
