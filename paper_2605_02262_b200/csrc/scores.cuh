@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(ST) k_text_pool(const __half *__restrict__ txt
 }
 
 template <int NC, bool CENTER, bool HS>
-__global__ void __launch_bounds__(ST, WQ_SC_MINB) k_window_scores(const __half *__restrict__ vis, int64_t vrs,
+__global__ void __launch_bounds__(ST, CENTER ? 2 : WQ_SC_MINB) k_window_scores(const __half *__restrict__ vis, int64_t vrs,
                                                       int64_t vbs, int M, int N, int D, int S,
                                                       const double *__restrict__ tbar,
                                                       double *__restrict__ scores, int dh, int64_t hs) {
