@@ -58,7 +58,8 @@ constexpr int DT = (NCW + 1) * 32;      // threads per CTA: consumers + the prod
 #define WQ_DEC_PROFILE 0                 // per-CTA timestamps into the workspace (debug & 8)
 #endif
 #ifndef WQ_DEC_STAGE
-#define WQ_DEC_STAGE 32768
+#define WQ_DEC_STAGE 40960               // stage bytes for S <= 64 (4 stages; 32 KB x 5: C5 32.85 -> 32.64 us,
+                                         // C4 106.9 -> 106.5; S = 128 keeps 32 KB: its FP16 records split)
 #endif
 constexpr float LAZY_TH = 8.0f;         // log2 headroom of the lazy softmax rescale
 constexpr int KIND_REST = 4;
@@ -474,8 +475,10 @@ WQ_DEV void do_rest(const uint8_t *Kb, const uint8_t *Vb, int ntok, const uint8_
                                          // C4 S=128 185.4 -> 127.8 us, S=64 133.8 -> 127.9)
 #endif
 // FP16 items per window in reordered mode: 2 when a 64 KB record would leave a 2-stage ring
+template <int S>
+constexpr int stage_bytes() { return S >= 128 ? 32768 : WQ_DEC_STAGE; }
 template <int D, int S>
-constexpr int fsplit() { return 4 * S * D >= 2 * WQ_DEC_STAGE ? 2 : 1; }
+constexpr int fsplit() { return 4 * S * D >= 2 * stage_bytes<S>() ? 2 : 1; }
 
 template <int D, int S, int FS = 1>
 struct DecodeSmem {
@@ -483,7 +486,7 @@ struct DecodeSmem {
   // the largest quantized record when FP16 windows are split (FS > 1, reordered mode only)
   static constexpr int REC8 = S * D * 2 + 4 * D + 4 * S;
   static constexpr int BIG = FS > 1 ? (4 * S * D / FS > REC8 ? 4 * S * D / FS : REC8) : 4 * S * D;
-  static constexpr int STAGE = (BIG > WQ_DEC_STAGE) ? BIG : WQ_DEC_STAGE;
+  static constexpr int STAGE = (BIG > stage_bytes<S>()) ? BIG : stage_bytes<S>();
   static constexpr int RING = WQ_DEC_RING;
   static constexpr int NST = (RING / STAGE) < 2 ? 2 : RING / STAGE;
   static constexpr int KT = D / 16;
