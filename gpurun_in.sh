@@ -1,5 +1,3 @@
-timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_suite.log 2>&1; echo suite=$? >> gpurun_out/gpu_suite.log
-timeout 600 python tools/decode_ab.py --cfg C4_128 --layers 4 prod s32 > gpurun_out/ab_c4_128.log 2>&1
-timeout 600 python tools/decode_ab.py --cfg C4_64 --layers 4 prod s32 > gpurun_out/ab_c4_64.log 2>&1
-timeout 600 python tools/decode_ab.py --cfg C5 prod s32 > gpurun_out/ab_c5.log 2>&1
-timeout 600 python tools/decode_ab.py --cfg C1 prod s32 > gpurun_out/ab_c1.log 2>&1
+timeout 1200 bash tools/run_cfgs.sh > gpurun_out/run_cfgs.log 2>&1
+bash tools/prof_kernel.sh '^k_decode$' r02f 2
+rm -f gpurun_out/*.ncu-rep
